@@ -1,0 +1,215 @@
+/*
+ * moe_capi.h -- the C-ABI boundary of the B200-native MoE-layer inference path.
+ *
+ * Plain C: opaque handles, plain pointers and sizes, int status codes.  No
+ * C++ or torch types cross this boundary.  Every entry point below replaces
+ * (or, for the layer arithmetic the reference does not implement, completes)
+ * a reference interface, cited as file:line under /root/reference/proj:
+ *
+ *   moe_dynamic_dispatch_host   dynamic_dispatch    include/moesim/gating.hpp:69,
+ *                                                   src/gating.cpp:58-86
+ *   moe_static_dispatch_host    static_dispatch     include/moesim/gating.hpp:68,
+ *                                                   src/gating.cpp:30-56
+ *   moe_expert_capacity         expert_capacity     include/moesim/gating.hpp:31,
+ *                                                   src/gating.cpp:22-28
+ *   moe_inverse_order_host      combine<T> (its inverse permutation, the part
+ *                               that touches every slot) gating.hpp:107-184
+ *   moe_route_dynamic/_static   device-resident forms of the two dispatches
+ *   moe_gate_topk               (absent in the reference: SPEC.md:224) the gate
+ *                               that produces the TokenAssignment of
+ *                               include/moesim/trace.hpp:15-18
+ *   moe_grouped_ffn             (absent: SPEC.md:8) expert FFN
+ *   moe_combine                 weighted combine<T>, gating.hpp:107-184
+ *   moe_layer_*                 the whole MoE layer of PAPER.md:178-187 /
+ *                               :305-319 (gate -> dispatch -> FFN -> combine)
+ *   moe_exchange_counts         plan_dynamic_exchange payload phase,
+ *                               include/moesim/exchange.hpp:64-65,
+ *                               src/exchange.cpp:95-120
+ *   moe_cache_*                 the GPU-resident expert cache driven by
+ *                               access_batch, include/moesim/buffer.hpp:53-55
+ *
+ * Threading: one context per device (like a library handle).  Calls on one
+ * context are not thread-safe; different contexts are independent.  Device-
+ * pointer entry points are asynchronous and ordered on the caller's stream
+ * (a cudaStream_t passed as void*, NULL = legacy default stream); *_host entry
+ * points are synchronous.
+ *
+ * Errors: every call returns MOE_OK (0) or a moe_status; the message of the
+ * last failure on the calling thread is available from moe_last_error().  The
+ * C++ drop-in layer (include/moesim/gating.hpp) rethrows
+ * MOE_ERR_INVALID_ARGUMENT as std::invalid_argument with the reference's
+ * exact message text (src/gating.cpp:13-17,33-42,61,90,96,102).
+ */
+#ifndef MOE_CAPI_H_
+#define MOE_CAPI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOE_CAPI_VERSION 1
+
+typedef enum moe_status {
+  MOE_OK = 0,
+  MOE_ERR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+  MOE_ERR_CUDA = 2,             /* CUDA runtime / driver failure */
+  MOE_ERR_UNSUPPORTED = 3,      /* shape outside what the kernels handle */
+  MOE_ERR_OUT_OF_MEMORY = 4,
+  MOE_ERR_EXPERT_RANGE = 5      /* an expert id outside [0, E) (UB in the reference) */
+} moe_status;
+
+typedef enum moe_gating_mode {
+  MOE_GATING_STATIC = 0, /* GatingMode::kStatic,  gating.hpp:16 */
+  MOE_GATING_DYNAMIC = 1 /* GatingMode::kDynamic, gating.hpp:16 */
+} moe_gating_mode;
+
+typedef struct moe_ctx moe_ctx;
+typedef struct moe_layer moe_layer;
+
+int moe_version(void);
+const char* moe_status_string(int status);
+/* Message of the last failing call made by this thread ("" if none). */
+const char* moe_last_error(void);
+
+int moe_ctx_create(int device, moe_ctx** out);
+int moe_ctx_destroy(moe_ctx* ctx);
+/* Number of SMs of the context's device. */
+int moe_ctx_sm_count(const moe_ctx* ctx);
+
+/* ---------------------------------------------------------------- routing */
+
+/* gating.cpp:22-28.  Pure host arithmetic; returns the capacity (>= 0). */
+int moe_expert_capacity(double capacity_factor, int seq_len);
+
+/* Drop-in, host buffers, synchronous (the GPU does the work).
+ *   experts[t*k + j]  expert of assignment slot t*k+j (TokenAssignment::experts)
+ *   order[S*k], counts[E], splits[E+1]  exactly DynamicDispatchPlan's fields. */
+int moe_dynamic_dispatch_host(moe_ctx* ctx, const int32_t* experts, int S, int k, int E,
+                              int32_t* order, int32_t* counts, int32_t* splits);
+
+/* Drop-in static dispatch.  capacity = moe_expert_capacity(C, S); slots is
+ * E x capacity EXPERT-MAJOR (slots[e*cap + c] == plan.slots(e, c)), -1 for
+ * placeholders; dropped holds (token, expert) pairs in slot order. */
+int moe_static_dispatch_host(moe_ctx* ctx, const int32_t* experts, int S, int k, int E,
+                             double capacity_factor, int32_t* capacity, int32_t* slots,
+                             int64_t slots_len, int32_t* dropped, int32_t* n_dropped);
+
+/* Inverse of a dispatch permutation: pos[order[p]] = p for p < n (entries
+ * equal to -1 -- static placeholders -- are skipped).  pos has n_slots
+ * entries and is pre-filled with -1.  Host buffers, synchronous. */
+int moe_inverse_order_host(moe_ctx* ctx, const int32_t* order, int64_t n, int32_t* pos,
+                           int64_t n_slots);
+
+/* Device-resident routing (stream-ordered).  Any out-of-range expert id is
+ * reported by the next moe_check_errors(). pos (slot -> row) may be NULL. */
+int moe_route_dynamic(moe_ctx* ctx, const int32_t* expert_idx, int S, int k, int E,
+                      int32_t* counts, int32_t* splits, int32_t* order, int32_t* pos,
+                      void* stream);
+int moe_route_static(moe_ctx* ctx, const int32_t* expert_idx, int S, int k, int E, int capacity,
+                     int32_t* counts, int32_t* slots, int32_t* pos, int32_t* dropped,
+                     int32_t* n_dropped, void* stream);
+/* Synchronises `stream`; MOE_ERR_EXPERT_RANGE if a routing call since the
+ * last check met an out-of-range expert id (the flag is then cleared). */
+int moe_check_errors(moe_ctx* ctx, void* stream);
+
+/* ---------------------------------------------------------------- stages */
+
+/* Gate (bf16 X [S,TD], bf16 Wg [E,TD], both row-major) -> idx [S,k] int32,
+ * w [S,k] fp32 (softmax restricted to the chosen k, slot 0 = largest logit,
+ * ties -> lower id), optional fp32 logits [S,E].  E <= 512, k <= 8, TD % 64 == 0. */
+int moe_gate_topk(moe_ctx* ctx, const void* X, const void* Wg, int S, int TD, int E, int k,
+                  int32_t* idx, float* w, float* logits, void* stream);
+
+/* Xp[p] = X[order[p] / k] (zero row where order[p] == -1); bf16, TD % 8 == 0. */
+int moe_gather_rows(moe_ctx* ctx, const void* X, const int32_t* order, int rows, int k, int TD,
+                    void* Xp, void* stream);
+
+/* out[t] = sum_j Yw[pos[t*k+j]] (pos == -1 skipped), fp32 accumulate in j
+ * order, bf16 out. */
+int moe_combine(moe_ctx* ctx, const void* Yw, const int32_t* pos, int S, int k, int TD, void* out,
+                void* stream);
+
+/* Counter-based synthetic bf16 data, bit-identical to oracle/layer.py::synth:
+ * uniform on [-scale, scale). */
+int moe_fill_uniform_bf16(moe_ctx* ctx, void* dst, int64_t n, uint64_t seed, uint64_t tensor_id,
+                          float scale, void* stream);
+
+/* ---------------------------------------------------------------- layer */
+
+typedef struct moe_layer_desc {
+  int max_tokens;         /* S upper bound per forward call */
+  int token_dim;          /* TD: multiple of 128 */
+  int hidden_dim;         /* HD: multiple of 128 */
+  int num_experts;        /* E <= 512 */
+  int top_k;              /* k <= 8 */
+  int mode;               /* moe_gating_mode */
+  double capacity_factor; /* static mode only */
+  int tile_n;             /* grouped-FFN item width: 0 = auto, 128 or 256 */
+  int keep_logits;        /* 1: keep fp32 gate logits [S,E] for parity checks */
+} moe_layer_desc;
+
+/* Weights are caller-owned device buffers (bf16, row-major):
+ *   Wg [E, TD], W1 [E, HD, TD] (H = relu(x W1_e^T)), W2 [E, TD, HD]. */
+int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, const void* W1,
+                     const void* W2, moe_layer** out);
+int moe_layer_destroy(moe_layer* layer);
+
+/* One forward pass on device buffers: X [S,TD] bf16 -> out [S,TD] bf16.
+ * Stream-ordered, no host synchronisation (dynamic and static modes). */
+int moe_layer_forward(moe_layer* layer, const void* X, int S, void* out, void* stream);
+
+/* Same, with the forward captured once into a CUDA graph per (X, out, S,
+ * stream) and replayed afterwards. */
+int moe_layer_forward_graph(moe_layer* layer, const void* X, int S, void* out, void* stream);
+
+/* End-to-end host path: X_host [S,TD] bf16 -> out_host [S,TD] bf16, the H2D
+ * and D2H copies included; synchronous.  Host buffers should be pinned. */
+int moe_layer_forward_host(moe_layer* layer, const void* X_host, int S, void* out_host,
+                           void* stream);
+
+/* Device pointers of the layer's internal buffers (valid until destroy), for
+ * parity checks.  Any field may be NULL when not applicable. */
+typedef struct moe_layer_view {
+  int32_t* idx;        /* [S*k] */
+  float* w;            /* [S*k] */
+  float* logits;       /* [S*E] when keep_logits */
+  int32_t* counts;     /* [E] */
+  int32_t* splits;     /* [E+1] */
+  int32_t* order;      /* dynamic [S*k]; static [E*cap] */
+  int32_t* pos;        /* [S*k] */
+  int32_t* dropped;    /* static [2*S*k] */
+  int32_t* n_dropped;  /* static [1] */
+  void* xp;            /* bf16 [rows, TD] */
+  void* h;             /* bf16 [rows, HD] */
+  void* yw;            /* bf16 [rows, TD] */
+  int32_t* n_items;    /* [1] */
+  int rows;            /* rows of xp/h/yw used by the last forward */
+  int capacity;        /* static capacity of the last forward */
+  int tile_n;
+} moe_layer_view;
+int moe_layer_get_view(moe_layer* layer, moe_layer_view* view);
+
+/* Expert cache hook: make the FFN read expert e's weights from slot
+ * slot_of[e] of caller-owned pools W1_pool [n_slots, HD, TD] and
+ * W2_pool [n_slots, TD, HD] (device).  slot_of is a DEVICE int32 [E] table;
+ * pass NULL pools to return to the layer's own W1/W2. */
+int moe_layer_set_weight_pool(moe_layer* layer, const void* W1_pool, const void* W2_pool,
+                              int n_slots, const int32_t* slot_of);
+
+/* ---------------------------------------------------------------- EP */
+
+/* exchange.cpp:95-120, payload phase, as slot counts: counts[src*D + dst] =
+ * number of assignment slots whose token lives on src (token t on t % D,
+ * exchange.cpp:35-37) and whose expert lives on dst = device_of[e].  Host
+ * buffers, synchronous (computed on the GPU). */
+int moe_exchange_counts_host(moe_ctx* ctx, const int32_t* experts, int S, int k, int D,
+                             const int32_t* device_of, int E, int64_t* counts);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MOE_CAPI_H_ */

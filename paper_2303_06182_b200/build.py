@@ -1,0 +1,74 @@
+"""In-tree build of the native libraries (no JIT cache, so the .so files travel
+to the GPU box with the repo snapshot).
+
+  libmoe_b200.so     sm_100a kernels + C ABI        (nvcc, -gencode sm_100a)
+  libmoesim_b200.so  C++ drop-in of the reference moesim:: gating API, on top
+                     of the C ABI                   (g++ -std=c++20)
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+HOST = os.path.join(HERE, "host")
+INCLUDE = os.path.join(ROOT, "include")
+EIGEN_MIN = os.path.join(ROOT, "third_party", "eigen_min")
+LIB = os.path.join(HERE, "libmoe_b200.so")
+LIBCXX = os.path.join(HERE, "libmoesim_b200.so")
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _stale(target: str, deps) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _run(cmd, cwd=None):
+    print("+", " ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True, cwd=cwd)
+
+
+def build_cuda(force: bool = False, verbose_ptxas: bool = False) -> str:
+    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    deps = srcs + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + [
+        os.path.join(INCLUDE, "moe_capi.h"), __file__]
+    if not force and not _stale(LIB, deps):
+        return LIB
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+           "-cudart", "static", f"-I{INCLUDE}", "-o", LIB, *srcs]
+    if verbose_ptxas:
+        cmd.insert(1, "-Xptxas=-v")
+    _run(cmd)
+    return LIB
+
+
+def build_cxx(force: bool = False) -> str:
+    srcs = sorted(glob.glob(os.path.join(HOST, "*.cpp")))
+    if not srcs:
+        return ""
+    deps = srcs + glob.glob(os.path.join(INCLUDE, "moesim", "*.hpp")) + [LIB, __file__]
+    if not force and not _stale(LIBCXX, deps):
+        return LIBCXX
+    cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", f"-I{INCLUDE}",
+           f"-I{EIGEN_MIN}", "-o", LIBCXX, *srcs, f"-L{HERE}", "-lmoe_b200",
+           "-Wl,-rpath,$ORIGIN"]
+    _run(cmd)
+    return LIBCXX
+
+
+def build_all(force: bool = False) -> None:
+    build_cuda(force)
+    build_cxx(force)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv)

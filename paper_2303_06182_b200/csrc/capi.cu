@@ -1,0 +1,774 @@
+// C-ABI implementation: contexts, argument checking (reference error text),
+// host-buffer drop-in entry points, TMA descriptor setup and the MoE layer
+// (gate -> route -> gather -> grouped FFN x2 -> combine) with its workspace.
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/moe_capi.h"
+#include "moe_internal.h"
+
+namespace moe {
+int gate_box_rows(int E);
+}
+
+using namespace moe;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int status, const std::string& msg) {
+  g_last_error = msg;
+  return status;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(MOE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define MOE_CUDA(call)                                         \
+  do {                                                         \
+    cudaError_t _e = (call);                                   \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);        \
+  } while (0)
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+int get_encoder() {
+  if (g_encode) return MOE_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+    return fail(MOE_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return MOE_OK;
+}
+
+// Row-major bf16 matrix [rows, cols] viewed by TMA in boxes of 64 x box_rows
+// with the 128-byte swizzle the UMMA descriptors expect.
+int encode_bf16(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  int st = get_encoder();
+  if (st) return st;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d) rows=%llu cols=%llu box=%u",
+             (int)r, (unsigned long long)rows, (unsigned long long)cols, box_rows);
+    return fail(MOE_ERR_CUDA, buf);
+  }
+  return MOE_OK;
+}
+
+// Reference check_batch (gating.cpp:12-18), verbatim messages.
+int check_batch(int S, int k, int E) {
+  if (E < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "num_experts must be positive");
+  if (k < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "top_k must be positive");
+  if (k > E) return fail(MOE_ERR_INVALID_ARGUMENT, "top_k exceeds num_experts");
+  if (S < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "empty batch");
+  return MOE_OK;
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  int reserve(size_t count) {
+    if (count <= n) return MOE_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T) + 16);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      return fail(MOE_ERR_OUT_OF_MEMORY, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    n = count;
+    return MOE_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+__global__ void inverse_order_kernel(const int32_t* order, int64_t n, int32_t* pos) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int s = order[p];
+    if (s >= 0) pos[s] = (int32_t)p;
+  }
+}
+
+__global__ void exchange_counts_kernel(const int32_t* experts, int S, int k, int D,
+                                       const int32_t* device_of, int E,
+                                       unsigned long long* counts, int32_t* err) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)S * k;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int e = experts[i];
+    if (e < 0 || e >= E) {
+      atomicOr(err, 1);
+      continue;
+    }
+    const int src = (int)((i / k) % D);
+    atomicAdd(&counts[(int64_t)src * D + device_of[e]], 1ull);
+  }
+}
+
+}  // namespace
+
+struct moe_ctx {
+  int device = 0;
+  int sms = 0;
+  int route_max_blocks = 0;
+  int route_prepared_E = -1;
+  DevBuf<int32_t> block_hist, err_flag, drop_mark;
+  cudaStream_t scratch_stream = nullptr;
+
+  int prepare_route(int E) {
+    if (E > route_prepared_E) {
+      int mb = 0;
+      cudaError_t e = route_prepare(E, &mb);
+      if (e != cudaSuccess) return cuda_fail(e, "route_prepare");
+      route_max_blocks = mb;
+      route_prepared_E = E;
+    }
+    int st = block_hist.reserve((size_t)E * route_max_blocks + route_max_blocks);
+    if (st) return st;
+    st = err_flag.reserve(1);
+    if (st) return st;
+    return MOE_OK;
+  }
+};
+
+struct moe_layer {
+  moe_ctx* ctx = nullptr;
+  moe_layer_desc d{};
+  const void* Wg = nullptr;
+  const void* W1 = nullptr;
+  const void* W2 = nullptr;
+  int tile_n = 128;
+  int rows_max = 0;
+  int items_max = 0;
+  CUtensorMap tmWg, tmW1, tmW2, tmXp, tmH;
+  CUtensorMap tmX;
+  const void* tmX_ptr = nullptr;
+  int tmX_rows = 0;
+  // optional expert-cache weight pool
+  const int32_t* slot_of = nullptr;
+  DevBuf<int32_t> idx, pos, counts, splits, order, dropped, n_dropped, n_items, err;
+  DevBuf<float> w, wpos, logits;
+  DevBuf<FfnItem> items;
+  DevBuf<__nv_bfloat16> xp, h, yw, xin, yout;
+  int last_rows = 0;
+  int last_cap = 0;
+  // graph cache
+  cudaGraphExec_t gexec = nullptr;
+  const void* g_x = nullptr;
+  void* g_out = nullptr;
+  int g_S = -1;
+  cudaStream_t g_stream = nullptr;
+};
+
+extern "C" {
+
+int moe_version(void) { return MOE_CAPI_VERSION; }
+
+const char* moe_status_string(int s) {
+  switch (s) {
+    case MOE_OK: return "ok";
+    case MOE_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case MOE_ERR_CUDA: return "cuda error";
+    case MOE_ERR_UNSUPPORTED: return "unsupported shape";
+    case MOE_ERR_OUT_OF_MEMORY: return "out of memory";
+    case MOE_ERR_EXPERT_RANGE: return "expert id out of range";
+    default: return "unknown status";
+  }
+}
+
+const char* moe_last_error(void) { return g_last_error.c_str(); }
+
+int moe_ctx_create(int device, moe_ctx** out) {
+  if (!out) return fail(MOE_ERR_INVALID_ARGUMENT, "null output handle");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) return fail(MOE_ERR_CUDA, "no CUDA device available");
+  if (device < 0 || device >= n) return fail(MOE_ERR_INVALID_ARGUMENT, "device out of range");
+  MOE_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  MOE_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(MOE_ERR_UNSUPPORTED, "this library is built for sm_100a (B200) only");
+  auto* c = new moe_ctx();
+  c->device = device;
+  c->sms = prop.multiProcessorCount;
+  e = gemm_prepare();
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "gemm_prepare");
+  }
+  int st = get_encoder();
+  if (st) {
+    delete c;
+    return st;
+  }
+  *out = c;
+  return MOE_OK;
+}
+
+int moe_ctx_destroy(moe_ctx* ctx) {
+  if (!ctx) return MOE_OK;
+  cudaSetDevice(ctx->device);
+  ctx->block_hist.release();
+  ctx->err_flag.release();
+  ctx->drop_mark.release();
+  delete ctx;
+  return MOE_OK;
+}
+
+int moe_ctx_sm_count(const moe_ctx* ctx) { return ctx ? ctx->sms : 0; }
+
+int moe_expert_capacity(double capacity_factor, int seq_len) {
+  // gating.cpp:22-28
+  const double raw = capacity_factor * seq_len;
+  const double nearest = std::round(raw);
+  if (std::abs(raw - nearest) < 1e-9 * std::max(1.0, std::abs(raw)))
+    return static_cast<int>(nearest);
+  return static_cast<int>(std::ceil(raw));
+}
+
+static int route_common(moe_ctx* ctx, const int32_t* expert_idx, int S, int k, int E, int cap,
+                        int32_t* counts, int32_t* splits, int32_t* order, int32_t* pos,
+                        const float* gate_w, float* wpos, int32_t* dropped, int32_t* n_dropped,
+                        FfnItem* items, int32_t* n_items, int tile_n, const int32_t* key_map,
+                        int num_keys_in, cudaStream_t stream) {
+  int st = ctx->prepare_route(E);
+  if (st) return st;
+  if (cap > 0) {
+    st = ctx->drop_mark.reserve((size_t)S * k);
+    if (st) return st;
+  }
+  RouteArgs a{};
+  a.expert_idx = expert_idx;
+  a.key_map = key_map;
+  a.num_keys_in = num_keys_in;
+  a.num_experts = E;
+  a.total_slots = S * k;
+  a.top_k = k;
+  a.capacity = cap;
+  a.tile_n = tile_n;
+  a.counts = counts;
+  a.splits = splits;
+  a.order = order;
+  a.pos = pos;
+  a.gate_w = gate_w;
+  a.wpos = wpos;
+  a.dropped = dropped;
+  a.n_dropped = n_dropped;
+  a.drop_mark = ctx->drop_mark.p;
+  a.block_hist = ctx->block_hist.p;
+  a.items = items;
+  a.n_items = n_items;
+  a.error_flag = ctx->err_flag.p;
+  cudaError_t e = launch_route(a, ctx->route_max_blocks, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "route kernel launch");
+  return MOE_OK;
+}
+
+int moe_route_dynamic(moe_ctx* ctx, const int32_t* expert_idx, int S, int k, int E,
+                      int32_t* counts, int32_t* splits, int32_t* order, int32_t* pos,
+                      void* stream) {
+  if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
+  int st = check_batch(S, k, E);
+  if (st) return st;
+  if (!expert_idx || !counts || !splits || !order)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "null buffer");
+  return route_common(ctx, expert_idx, S, k, E, 0, counts, splits, order, pos, nullptr, nullptr,
+                      nullptr, nullptr, nullptr, nullptr, 128, nullptr, 0,
+                      (cudaStream_t)stream);
+}
+
+int moe_route_static(moe_ctx* ctx, const int32_t* expert_idx, int S, int k, int E, int capacity,
+                     int32_t* counts, int32_t* slots, int32_t* pos, int32_t* dropped,
+                     int32_t* n_dropped, void* stream) {
+  if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
+  int st = check_batch(S, k, E);
+  if (st) return st;
+  if (capacity <= 0) return fail(MOE_ERR_INVALID_ARGUMENT, "zero capacity");
+  if (!expert_idx || !counts || !slots || !dropped || !n_dropped)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "null buffer");
+  st = ctx->prepare_route(E);
+  if (st) return st;
+  // splits scratch lives in block_hist's tail-free area: use a small buffer
+  static thread_local DevBuf<int32_t> splits;
+  st = splits.reserve((size_t)E + 1);
+  if (st) return st;
+  return route_common(ctx, expert_idx, S, k, E, capacity, counts, splits.p, slots, pos, nullptr,
+                      nullptr, dropped, n_dropped, nullptr, nullptr, 128, nullptr, 0,
+                      (cudaStream_t)stream);
+}
+
+int moe_check_errors(moe_ctx* ctx, void* stream) {
+  if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
+  MOE_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  if (!ctx->err_flag.p) return MOE_OK;
+  int32_t flag = 0;
+  MOE_CUDA(cudaMemcpy(&flag, ctx->err_flag.p, sizeof flag, cudaMemcpyDeviceToHost));
+  if (flag) {
+    MOE_CUDA(cudaMemset(ctx->err_flag.p, 0, sizeof(int32_t)));
+    return fail(MOE_ERR_EXPERT_RANGE, "expert id out of range [0, num_experts)");
+  }
+  return MOE_OK;
+}
+
+int moe_dynamic_dispatch_host(moe_ctx* ctx, const int32_t* experts, int S, int k, int E,
+                              int32_t* order, int32_t* counts, int32_t* splits) {
+  if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
+  int st = check_batch(S, k, E);
+  if (st) return st;
+  MOE_CUDA(cudaSetDevice(ctx->device));
+  const size_t n = (size_t)S * k;
+  int32_t *d_idx = nullptr, *d_order = nullptr, *d_counts = nullptr, *d_splits = nullptr;
+  MOE_CUDA(cudaMalloc(&d_idx, n * 4));
+  MOE_CUDA(cudaMalloc(&d_order, n * 4));
+  MOE_CUDA(cudaMalloc(&d_counts, (size_t)E * 4));
+  MOE_CUDA(cudaMalloc(&d_splits, (size_t)(E + 1) * 4));
+  int rc = MOE_OK;
+  cudaError_t e = cudaMemcpy(d_idx, experts, n * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) rc = cuda_fail(e, "H2D experts");
+  if (!rc) rc = moe_route_dynamic(ctx, d_idx, S, k, E, d_counts, d_splits, d_order, nullptr, 0);
+  if (!rc) rc = moe_check_errors(ctx, 0);
+  if (!rc) {
+    cudaMemcpy(order, d_order, n * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(counts, d_counts, (size_t)E * 4, cudaMemcpyDeviceToHost);
+    e = cudaMemcpy(splits, d_splits, (size_t)(E + 1) * 4, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = cuda_fail(e, "D2H plan");
+  }
+  cudaFree(d_idx);
+  cudaFree(d_order);
+  cudaFree(d_counts);
+  cudaFree(d_splits);
+  return rc;
+}
+
+int moe_static_dispatch_host(moe_ctx* ctx, const int32_t* experts, int S, int k, int E,
+                             double capacity_factor, int32_t* capacity, int32_t* slots,
+                             int64_t slots_len, int32_t* dropped, int32_t* n_dropped) {
+  if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
+  int st = check_batch(S, k, E);
+  if (st) return st;
+  // gating.cpp:37-42
+  if (capacity_factor <= 0.0)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "capacity factor must be positive in static mode");
+  const int cap = moe_expert_capacity(capacity_factor, S);
+  if (cap <= 0) return fail(MOE_ERR_INVALID_ARGUMENT, "zero capacity");
+  *capacity = cap;
+  if ((int64_t)E * cap > slots_len) return fail(MOE_ERR_INVALID_ARGUMENT, "slots buffer too small");
+  MOE_CUDA(cudaSetDevice(ctx->device));
+  const size_t n = (size_t)S * k, cells = (size_t)E * cap;
+  int32_t *d_idx, *d_slots, *d_counts, *d_drop, *d_nd;
+  MOE_CUDA(cudaMalloc(&d_idx, n * 4));
+  MOE_CUDA(cudaMalloc(&d_slots, cells * 4));
+  MOE_CUDA(cudaMalloc(&d_counts, (size_t)E * 4));
+  MOE_CUDA(cudaMalloc(&d_drop, 2 * n * 4));
+  MOE_CUDA(cudaMalloc(&d_nd, 4));
+  int rc = MOE_OK;
+  cudaError_t e = cudaMemcpy(d_idx, experts, n * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) rc = cuda_fail(e, "H2D experts");
+  if (!rc) rc = moe_route_static(ctx, d_idx, S, k, E, cap, d_counts, d_slots, nullptr, d_drop, d_nd, 0);
+  if (!rc) rc = moe_check_errors(ctx, 0);
+  if (!rc) {
+    cudaMemcpy(slots, d_slots, cells * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(n_dropped, d_nd, 4, cudaMemcpyDeviceToHost);
+    e = cudaMemcpy(dropped, d_drop, (size_t)(*n_dropped) * 2 * 4, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = cuda_fail(e, "D2H plan");
+  }
+  cudaFree(d_idx);
+  cudaFree(d_slots);
+  cudaFree(d_counts);
+  cudaFree(d_drop);
+  cudaFree(d_nd);
+  return rc;
+}
+
+int moe_inverse_order_host(moe_ctx* ctx, const int32_t* order, int64_t n, int32_t* pos,
+                           int64_t n_slots) {
+  if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
+  if (n < 0 || n_slots < 0) return fail(MOE_ERR_INVALID_ARGUMENT, "negative size");
+  for (int64_t i = 0; i < n; ++i)
+    if (order[i] < -1 || order[i] >= n_slots)
+      return fail(MOE_ERR_INVALID_ARGUMENT, "combine: payload count mismatch vs. plan");
+  MOE_CUDA(cudaSetDevice(ctx->device));
+  int32_t *d_order = nullptr, *d_pos = nullptr;
+  MOE_CUDA(cudaMalloc(&d_order, (size_t)n * 4 + 4));
+  MOE_CUDA(cudaMalloc(&d_pos, (size_t)n_slots * 4 + 4));
+  int rc = MOE_OK;
+  cudaMemcpy(d_order, order, (size_t)n * 4, cudaMemcpyHostToDevice);
+  cudaMemset(d_pos, 0xff, (size_t)n_slots * 4);
+  if (n > 0) inverse_order_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256>>>(d_order, n, d_pos);
+  cudaError_t e = cudaMemcpy(pos, d_pos, (size_t)n_slots * 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) rc = cuda_fail(e, "inverse order");
+  cudaFree(d_order);
+  cudaFree(d_pos);
+  return rc;
+}
+
+int moe_exchange_counts_host(moe_ctx* ctx, const int32_t* experts, int S, int k, int D,
+                             const int32_t* device_of, int E, int64_t* counts) {
+  if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
+  int st = check_batch(S, k, E);
+  if (st) return st;
+  if (D < 1 || E % D != 0)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "num_experts must divide evenly across devices");
+  for (int e = 0; e < E; ++e)
+    if (device_of[e] < 0 || device_of[e] >= D)
+      return fail(MOE_ERR_INVALID_ARGUMENT, "device_of out of range");
+  MOE_CUDA(cudaSetDevice(ctx->device));
+  st = ctx->prepare_route(E);
+  if (st) return st;
+  int32_t *d_e = nullptr, *d_dev = nullptr;
+  unsigned long long* d_c = nullptr;
+  MOE_CUDA(cudaMalloc(&d_e, (size_t)S * k * 4));
+  MOE_CUDA(cudaMalloc(&d_dev, (size_t)E * 4));
+  MOE_CUDA(cudaMalloc(&d_c, (size_t)D * D * 8));
+  cudaMemcpy(d_e, experts, (size_t)S * k * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(d_dev, device_of, (size_t)E * 4, cudaMemcpyHostToDevice);
+  cudaMemset(d_c, 0, (size_t)D * D * 8);
+  exchange_counts_kernel<<<std::max(1, std::min(4096, (S * k + 255) / 256)), 256>>>(
+      d_e, S, k, D, d_dev, E, d_c, ctx->err_flag.p);
+  int rc = moe_check_errors(ctx, 0);
+  if (!rc) {
+    cudaError_t e = cudaMemcpy(counts, d_c, (size_t)D * D * 8, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = cuda_fail(e, "D2H counts");
+  }
+  cudaFree(d_e);
+  cudaFree(d_dev);
+  cudaFree(d_c);
+  return rc;
+}
+
+int moe_gate_topk(moe_ctx* ctx, const void* X, const void* Wg, int S, int TD, int E, int k,
+                  int32_t* idx, float* w, float* logits, void* stream) {
+  if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
+  int st = check_batch(S, k, E);
+  if (st) return st;
+  if (E > 512 || k > 8 || TD % 64 != 0)
+    return fail(MOE_ERR_UNSUPPORTED, "gate supports E <= 512, k <= 8, TD % 64 == 0");
+  cudaError_t e = gate_prepare(E);
+  if (e != cudaSuccess) return cuda_fail(e, "gate_prepare");
+  CUtensorMap tmX, tmWg;
+  st = encode_bf16(&tmX, X, S, TD, 128);
+  if (st) return st;
+  st = encode_bf16(&tmWg, Wg, E, TD, gate_box_rows(E));
+  if (st) return st;
+  GateArgs a{S, TD, E, k, idx, w, logits};
+  e = launch_gate(tmX, tmWg, a, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "gate launch");
+  return MOE_OK;
+}
+
+int moe_gather_rows(moe_ctx* ctx, const void* X, const int32_t* order, int rows, int k, int TD,
+                    void* Xp, void* stream) {
+  if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
+  if (TD % 8 != 0) return fail(MOE_ERR_UNSUPPORTED, "TD must be a multiple of 8");
+  cudaError_t e = launch_gather_rows((const __nv_bfloat16*)X, order, rows, k, TD,
+                                     (__nv_bfloat16*)Xp, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "gather launch");
+  return MOE_OK;
+}
+
+int moe_combine(moe_ctx* ctx, const void* Yw, const int32_t* pos, int S, int k, int TD, void* out,
+                void* stream) {
+  if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
+  if (TD % 8 != 0) return fail(MOE_ERR_UNSUPPORTED, "TD must be a multiple of 8");
+  cudaError_t e = launch_combine((const __nv_bfloat16*)Yw, pos, S, k, TD, (__nv_bfloat16*)out,
+                                 (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "combine launch");
+  return MOE_OK;
+}
+
+int moe_fill_uniform_bf16(moe_ctx* ctx, void* dst, int64_t n, uint64_t seed, uint64_t tensor_id,
+                          float scale, void* stream) {
+  if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
+  cudaError_t e = launch_fill_uniform_bf16((__nv_bfloat16*)dst, n, seed, tensor_id, scale,
+                                           (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "fill launch");
+  return MOE_OK;
+}
+
+// ------------------------------------------------------------------ layer
+
+int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, const void* W1,
+                     const void* W2, moe_layer** out) {
+  if (!ctx || !desc || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  const moe_layer_desc& d = *desc;
+  int st = check_batch(d.max_tokens, d.top_k, d.num_experts);
+  if (st) return st;
+  if (d.token_dim % 128 || d.hidden_dim % 128 || d.token_dim <= 0 || d.hidden_dim <= 0)
+    return fail(MOE_ERR_UNSUPPORTED, "token_dim and hidden_dim must be positive multiples of 128");
+  if (d.num_experts > 512 || d.top_k > 8)
+    return fail(MOE_ERR_UNSUPPORTED, "num_experts <= 512 and top_k <= 8 are supported");
+  if (d.mode != MOE_GATING_STATIC && d.mode != MOE_GATING_DYNAMIC)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "unknown gating mode");
+  if (d.mode == MOE_GATING_STATIC && d.capacity_factor <= 0.0)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "capacity factor must be positive in static mode");
+  if (!Wg || !W1 || !W2) return fail(MOE_ERR_INVALID_ARGUMENT, "null weight pointer");
+  MOE_CUDA(cudaSetDevice(ctx->device));
+  cudaError_t ce = gate_prepare(d.num_experts);
+  if (ce != cudaSuccess) return cuda_fail(ce, "gate_prepare");
+
+  auto* L = new moe_layer();
+  L->ctx = ctx;
+  L->d = d;
+  L->Wg = Wg;
+  L->W1 = W1;
+  L->W2 = W2;
+  const int S = d.max_tokens, k = d.top_k, E = d.num_experts;
+  int cap = 0;
+  if (d.mode == MOE_GATING_STATIC) {
+    cap = moe_expert_capacity(d.capacity_factor, S);
+    if (cap <= 0) {
+      delete L;
+      return fail(MOE_ERR_INVALID_ARGUMENT, "zero capacity");
+    }
+  }
+  const long rows_l = d.mode == MOE_GATING_STATIC ? (long)E * cap : (long)S * k;
+  if (rows_l > (1L << 30)) {
+    delete L;
+    return fail(MOE_ERR_UNSUPPORTED, "too many expert rows");
+  }
+  L->rows_max = (int)rows_l;
+  const double avg = (double)L->rows_max / E;
+  L->tile_n = d.tile_n ? d.tile_n : (avg > 160.0 ? 256 : 128);
+  if (L->tile_n != 128 && L->tile_n != 256) {
+    delete L;
+    return fail(MOE_ERR_INVALID_ARGUMENT, "tile_n must be 0, 128 or 256");
+  }
+  L->items_max = d.mode == MOE_GATING_STATIC ? E * ((cap + L->tile_n - 1) / L->tile_n)
+                                             : (S * k) / L->tile_n + E + 1;
+  const size_t TD = d.token_dim, HD = d.hidden_dim, R = L->rows_max;
+  // +16 rows of slack so a B tile of the last item never leaves the tensor
+  const size_t Rp = R + 256;
+  if ((st = L->idx.reserve((size_t)S * k)) || (st = L->w.reserve((size_t)S * k)) ||
+      (st = L->pos.reserve((size_t)S * k)) || (st = L->counts.reserve(E)) ||
+      (st = L->splits.reserve(E + 1)) || (st = L->order.reserve(R)) ||
+      (st = L->wpos.reserve(R)) || (st = L->items.reserve(L->items_max)) ||
+      (st = L->n_items.reserve(1)) || (st = L->err.reserve(1)) ||
+      (st = L->xp.reserve(Rp * TD)) || (st = L->h.reserve(Rp * HD)) ||
+      (st = L->yw.reserve(R * TD))) {
+    moe_layer_destroy(L);
+    return st;
+  }
+  if (d.mode == MOE_GATING_STATIC &&
+      ((st = L->dropped.reserve((size_t)2 * S * k)) || (st = L->n_dropped.reserve(1)))) {
+    moe_layer_destroy(L);
+    return st;
+  }
+  if (d.keep_logits && (st = L->logits.reserve((size_t)S * E))) {
+    moe_layer_destroy(L);
+    return st;
+  }
+  cudaMemset(L->xp.p, 0, Rp * TD * 2);
+  cudaMemset(L->h.p, 0, Rp * HD * 2);
+  if ((st = encode_bf16(&L->tmWg, Wg, E, TD, moe::gate_box_rows(E))) ||
+      (st = encode_bf16(&L->tmW1, W1, (uint64_t)E * HD, TD, 128)) ||
+      (st = encode_bf16(&L->tmW2, W2, (uint64_t)E * TD, HD, 128)) ||
+      (st = encode_bf16(&L->tmXp, L->xp.p, Rp, TD, 16)) ||
+      (st = encode_bf16(&L->tmH, L->h.p, Rp, HD, 16))) {
+    moe_layer_destroy(L);
+    return st;
+  }
+  if ((st = ctx->prepare_route(E))) {
+    moe_layer_destroy(L);
+    return st;
+  }
+  if (d.mode == MOE_GATING_STATIC && (st = ctx->drop_mark.reserve((size_t)S * k))) {
+    moe_layer_destroy(L);
+    return st;
+  }
+  *out = L;
+  return MOE_OK;
+}
+
+int moe_layer_destroy(moe_layer* L) {
+  if (!L) return MOE_OK;
+  cudaSetDevice(L->ctx->device);
+  if (L->gexec) cudaGraphExecDestroy(L->gexec);
+  L->idx.release();
+  L->w.release();
+  L->pos.release();
+  L->counts.release();
+  L->splits.release();
+  L->order.release();
+  L->wpos.release();
+  L->items.release();
+  L->n_items.release();
+  L->err.release();
+  L->dropped.release();
+  L->n_dropped.release();
+  L->logits.release();
+  L->xp.release();
+  L->h.release();
+  L->yw.release();
+  L->xin.release();
+  L->yout.release();
+  delete L;
+  return MOE_OK;
+}
+
+static int layer_forward_impl(moe_layer* L, const void* X, int S, void* out, cudaStream_t s) {
+  const moe_layer_desc& d = L->d;
+  if (S < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "empty batch");
+  if (S > d.max_tokens) return fail(MOE_ERR_INVALID_ARGUMENT, "S exceeds max_tokens");
+  const int k = d.top_k, E = d.num_experts, TD = d.token_dim, HD = d.hidden_dim;
+  int st;
+  if (X != L->tmX_ptr || S != L->tmX_rows) {
+    if ((st = encode_bf16(&L->tmX, X, (uint64_t)S, TD, 128))) return st;
+    L->tmX_ptr = X;
+    L->tmX_rows = S;
+  }
+  // 1. gate
+  GateArgs ga{S, TD, E, k, L->idx.p, L->w.p, d.keep_logits ? L->logits.p : nullptr};
+  cudaError_t e = launch_gate(L->tmX, L->tmWg, ga, s);
+  if (e != cudaSuccess) return cuda_fail(e, "gate launch");
+  // 2. route
+  int cap = 0, rows = S * k;
+  if (d.mode == MOE_GATING_STATIC) {
+    cap = moe_expert_capacity(d.capacity_factor, S);
+    rows = E * cap;
+  }
+  L->last_rows = rows;
+  L->last_cap = cap;
+  st = route_common(L->ctx, L->idx.p, S, k, E, cap, L->counts.p, L->splits.p, L->order.p,
+                    L->pos.p, L->w.p, L->wpos.p, L->dropped.p, L->n_dropped.p, L->items.p,
+                    L->n_items.p, L->tile_n, nullptr, 0, s);
+  if (st) return st;
+  // 3. gather token rows into expert-grouped order
+  e = launch_gather_rows((const __nv_bfloat16*)X, L->order.p, rows, k, TD, L->xp.p, s);
+  if (e != cudaSuccess) return cuda_fail(e, "gather launch");
+  // 4. grouped FFN
+  GemmArgs g1{L->items.p, L->n_items.p, L->slot_of, HD, TD, kEpiReluBf16, L->h.p, nullptr};
+  e = launch_grouped_gemm(L->tmW1, L->tmXp, g1, L->tile_n, L->ctx->sms, s);
+  if (e != cudaSuccess) return cuda_fail(e, "grouped gemm 1 launch");
+  GemmArgs g2{L->items.p, L->n_items.p, L->slot_of, TD, HD, kEpiScaleBf16, L->yw.p, L->wpos.p};
+  e = launch_grouped_gemm(L->tmW2, L->tmH, g2, L->tile_n, L->ctx->sms, s);
+  if (e != cudaSuccess) return cuda_fail(e, "grouped gemm 2 launch");
+  // 5. combine
+  e = launch_combine(L->yw.p, L->pos.p, S, k, TD, (__nv_bfloat16*)out, s);
+  if (e != cudaSuccess) return cuda_fail(e, "combine launch");
+  return MOE_OK;
+}
+
+int moe_layer_forward(moe_layer* L, const void* X, int S, void* out, void* stream) {
+  if (!L || !X || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  return layer_forward_impl(L, X, S, out, (cudaStream_t)stream);
+}
+
+int moe_layer_forward_graph(moe_layer* L, const void* X, int S, void* out, void* stream) {
+  if (!L || !X || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!L->gexec || L->g_x != X || L->g_out != out || L->g_S != S || L->g_stream != s) {
+    if (L->gexec) {
+      cudaGraphExecDestroy(L->gexec);
+      L->gexec = nullptr;
+    }
+    if (s == nullptr) return fail(MOE_ERR_INVALID_ARGUMENT, "graph capture needs a non-default stream");
+    MOE_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    int st = layer_forward_impl(L, X, S, out, s);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(s, &graph);
+    if (st) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "end capture");
+    e = cudaGraphInstantiate(&L->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+      L->gexec = nullptr;
+      return cuda_fail(e, "graph instantiate");
+    }
+    L->g_x = X;
+    L->g_out = out;
+    L->g_S = S;
+    L->g_stream = s;
+  }
+  MOE_CUDA(cudaGraphLaunch(L->gexec, s));
+  return MOE_OK;
+}
+
+int moe_layer_forward_host(moe_layer* L, const void* X_host, int S, void* out_host, void* stream) {
+  if (!L || !X_host || !out_host) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  const size_t bytes = (size_t)L->d.max_tokens * L->d.token_dim * 2;
+  int st;
+  if ((st = L->xin.reserve(bytes / 2)) || (st = L->yout.reserve(bytes / 2))) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t nb = (size_t)S * L->d.token_dim * 2;
+  MOE_CUDA(cudaMemcpyAsync(L->xin.p, X_host, nb, cudaMemcpyHostToDevice, s));
+  st = layer_forward_impl(L, L->xin.p, S, L->yout.p, s);
+  if (st) return st;
+  MOE_CUDA(cudaMemcpyAsync(out_host, L->yout.p, nb, cudaMemcpyDeviceToHost, s));
+  MOE_CUDA(cudaStreamSynchronize(s));
+  return moe_check_errors(L->ctx, s);
+}
+
+int moe_layer_get_view(moe_layer* L, moe_layer_view* v) {
+  if (!L || !v) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  v->idx = L->idx.p;
+  v->w = L->w.p;
+  v->logits = L->logits.p;
+  v->counts = L->counts.p;
+  v->splits = L->splits.p;
+  v->order = L->order.p;
+  v->pos = L->pos.p;
+  v->dropped = L->dropped.p;
+  v->n_dropped = L->n_dropped.p;
+  v->xp = L->xp.p;
+  v->h = L->h.p;
+  v->yw = L->yw.p;
+  v->n_items = L->n_items.p;
+  v->rows = L->last_rows;
+  v->capacity = L->last_cap;
+  v->tile_n = L->tile_n;
+  return MOE_OK;
+}
+
+int moe_layer_set_weight_pool(moe_layer* L, const void* W1_pool, const void* W2_pool, int n_slots,
+                              const int32_t* slot_of) {
+  if (!L) return fail(MOE_ERR_INVALID_ARGUMENT, "null layer");
+  const moe_layer_desc& d = L->d;
+  int st;
+  if (!W1_pool || !W2_pool) {
+    if ((st = encode_bf16(&L->tmW1, L->W1, (uint64_t)d.num_experts * d.hidden_dim, d.token_dim, 128)) ||
+        (st = encode_bf16(&L->tmW2, L->W2, (uint64_t)d.num_experts * d.token_dim, d.hidden_dim, 128)))
+      return st;
+    L->slot_of = nullptr;
+  } else {
+    if (n_slots < 1 || !slot_of) return fail(MOE_ERR_INVALID_ARGUMENT, "bad weight pool");
+    if ((st = encode_bf16(&L->tmW1, W1_pool, (uint64_t)n_slots * d.hidden_dim, d.token_dim, 128)) ||
+        (st = encode_bf16(&L->tmW2, W2_pool, (uint64_t)n_slots * d.token_dim, d.hidden_dim, 128)))
+      return st;
+    L->slot_of = slot_of;
+  }
+  if (L->gexec) {
+    cudaGraphExecDestroy(L->gexec);
+    L->gexec = nullptr;
+  }
+  return MOE_OK;
+}
+
+}  // extern "C"

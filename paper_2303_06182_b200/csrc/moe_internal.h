@@ -1,0 +1,88 @@
+// Internal (non-ABI) declarations shared by the CUDA translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace moe {
+
+// One unit of grouped-FFN work: `len` (<= tile_n) consecutive rows of the
+// expert-grouped activation matrix, all routed to `expert`.
+struct FfnItem {
+  int expert;
+  int row0;
+  int len;
+  int pad;
+};
+
+struct RouteArgs {
+  const int32_t* expert_idx;  // [total_slots] expert id per assignment slot
+  const int32_t* key_map;     // optional expert -> sort key relabel (EP); null = identity
+  int num_keys_in;            // size of key_map's domain
+  int num_experts;            // number of sort keys (E, or E after relabel)
+  int total_slots;            // k * S
+  int top_k;
+  int capacity;               // 0 = dynamic gating, else static capacity per expert
+  int chunk;                  // filled by launch_route
+  int tile_n;                 // FFN item width (rows per item)
+  int32_t* counts;            // [E]
+  int32_t* splits;            // [E+1]
+  int32_t* order;             // dynamic: [kS]; static: [E*cap] slot table (-1 = placeholder)
+  int32_t* pos;               // optional [kS] slot -> row (-1 = dropped)
+  const float* gate_w;        // optional [kS] gate weight per slot
+  float* wpos;                // optional [rows] gate weight per row (0 for placeholders)
+  int32_t* dropped;           // static: [2*kS] (token, expert) pairs in slot order
+  int32_t* n_dropped;         // static: [1]
+  int32_t* drop_mark;         // static scratch [kS]
+  int32_t* block_hist;        // scratch [E * max_blocks]
+  FfnItem* items;             // optional [<= E*ceil(rows/tile_n)] FFN work list
+  int32_t* n_items;           // [1]
+  int32_t* error_flag;        // [1] set to 1 on an out-of-range expert id
+};
+
+size_t route_smem_bytes(int E);
+cudaError_t route_prepare(int E, int* max_blocks);
+cudaError_t launch_route(RouteArgs a, int max_blocks, cudaStream_t stream);
+
+// ---- grouped expert FFN (tcgen05)
+enum EpilogueMode { kEpiReluBf16 = 0, kEpiScaleBf16 = 1 };
+
+struct GemmArgs {
+  const FfnItem* items;
+  const int32_t* n_items;
+  const int32_t* slot_of;  // optional expert -> weight-slot (expert cache); null = identity
+  int m_total;             // rows of one expert's weight matrix (HD for W1, TD for W2)
+  int k_total;             // reduction length (TD for W1, HD for W2)
+  int mode;                // EpilogueMode
+  __nv_bfloat16* out;      // [rows, m_total]
+  const float* wpos;       // kEpiScaleBf16: gate weight per row
+};
+
+cudaError_t gemm_prepare();
+// tmA: weights [slots*m_total, k_total]; tmB: activations [rows, k_total]
+cudaError_t launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB,
+                                const GemmArgs& args, int tile_n, int grid,
+                                cudaStream_t stream);
+
+// ---- gate (tcgen05): logits = X Wg^T, softmax-restricted top-k
+struct GateArgs {
+  int S, TD, E, k;
+  int32_t* idx;     // [S*k]
+  float* w;         // [S*k]
+  float* logits;    // optional [S*E]
+};
+cudaError_t gate_prepare(int E);
+cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateArgs& a,
+                        cudaStream_t stream);
+
+// ---- bandwidth kernels
+cudaError_t launch_gather_rows(const __nv_bfloat16* X, const int32_t* order, int rows, int k,
+                               int TD, __nv_bfloat16* Xp, cudaStream_t stream);
+cudaError_t launch_combine(const __nv_bfloat16* Yw, const int32_t* pos, int S, int k, int TD,
+                           __nv_bfloat16* out, cudaStream_t stream);
+cudaError_t launch_fill_uniform_bf16(__nv_bfloat16* dst, int64_t n, uint64_t seed,
+                                     uint64_t tensor_id, float scale, cudaStream_t stream);
+
+}  // namespace moe

@@ -1,0 +1,146 @@
+// Bandwidth-bound row kernels around the grouped FFN:
+//   gather   Xp[p] = X[order[p] / k]  (zero row for static placeholders)
+//            -- the paper's O(S*D) "indexing operation",
+//               counted by the reference as gather_elements = k*S*TD
+//               (proj/src/gating.cpp:123)
+//   combine  out[t] = sum_j Yw[pos[t*k+j]]  (gate weights were applied in the
+//            GEMM2 epilogue; dropped slots, pos = -1, contribute nothing)
+//            -- the weighted form of combine<T> (proj/include/moesim/
+//               gating.hpp:107-184): each token gathers its k expert outputs
+//               in assignment-slot order (j = 0..k-1), so the fp32 sum order
+//               is fixed and the result is deterministic.
+//   fill     counter-based synthetic data (bit-identical to oracle/layer.py)
+// One warp per row, 16-byte vector accesses, 4 independent loads in flight
+// per lane.
+#include "moe_internal.h"
+
+namespace moe {
+
+namespace {
+
+__global__ void __launch_bounds__(256)
+    gather_rows_kernel(const uint4* __restrict__ X, const int32_t* __restrict__ order, int rows,
+                       int k, int vec_per_row, uint4* __restrict__ Xp) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int p = warp; p < rows; p += nwarps) {
+    const int slot = order[p];
+    uint4* dst = Xp + static_cast<size_t>(p) * vec_per_row;
+    if (slot < 0) {
+      for (int v = lane; v < vec_per_row; v += 32) dst[v] = make_uint4(0, 0, 0, 0);
+      continue;
+    }
+    const uint4* src = X + static_cast<size_t>(slot / k) * vec_per_row;
+    int v = lane;
+    for (; v + 96 < vec_per_row; v += 128) {
+      const uint4 a = __ldg(src + v), b = __ldg(src + v + 32), c = __ldg(src + v + 64),
+                  d = __ldg(src + v + 96);
+      dst[v] = a;
+      dst[v + 32] = b;
+      dst[v + 64] = c;
+      dst[v + 96] = d;
+    }
+    for (; v < vec_per_row; v += 32) dst[v] = __ldg(src + v);
+  }
+}
+
+__device__ __forceinline__ void add_bf16x8(float (&acc)[8], const uint4& v) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    acc[2 * i] += f.x;
+    acc[2 * i + 1] += f.y;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    combine_kernel(const uint4* __restrict__ Yw, const int32_t* __restrict__ pos, int S, int k,
+                   int vec_per_row, uint4* __restrict__ out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp; t < S; t += nwarps) {
+    for (int v = lane; v < vec_per_row; v += 32) {
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int j = 0; j < k; ++j) {
+        const int p = pos[static_cast<size_t>(t) * k + j];
+        if (p >= 0) add_bf16x8(acc, __ldg(Yw + static_cast<size_t>(p) * vec_per_row + v));
+      }
+      uint4 o;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+      out[static_cast<size_t>(t) * vec_per_row + v] = o;
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// value(i) = (int(h >> 40) - 2^23) * 2^-23 * scale, h = mix64(seed*phi +
+// tensor_id*c + i): uniform on [-scale, scale), exactly reproducible on the
+// CPU (oracle/layer.py::synth) because every step is an exact integer op or a
+// single IEEE fp32 rounding.
+__global__ void fill_uniform_bf16_kernel(__nv_bfloat16* dst, int64_t n, uint64_t seed,
+                                         uint64_t tensor_id, float scale) {
+  const uint64_t base = seed * 0x9E3779B97F4A7C15ull + tensor_id * 0xD1B54A32D192ED03ull;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t h = mix64(base + static_cast<uint64_t>(i));
+    const int32_t u = static_cast<int32_t>(h >> 40) - (1 << 23);
+    const float x = __fmul_rn(static_cast<float>(u) * 0x1p-23f, scale);
+    dst[i] = __float2bfloat16_rn(x);
+  }
+}
+
+int grid_for(int64_t warps_needed, int sms) {
+  const int64_t blocks = (warps_needed + 7) / 8;
+  const int64_t cap = static_cast<int64_t>(sms) * 16;
+  return static_cast<int>(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
+}
+
+int sm_count() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+}  // namespace
+
+cudaError_t launch_gather_rows(const __nv_bfloat16* X, const int32_t* order, int rows, int k,
+                               int TD, __nv_bfloat16* Xp, cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  gather_rows_kernel<<<grid_for(rows, sm_count()), 256, 0, stream>>>(
+      reinterpret_cast<const uint4*>(X), order, rows, k, TD / 8, reinterpret_cast<uint4*>(Xp));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine(const __nv_bfloat16* Yw, const int32_t* pos, int S, int k, int TD,
+                           __nv_bfloat16* out, cudaStream_t stream) {
+  if (S <= 0) return cudaSuccess;
+  combine_kernel<<<grid_for(S, sm_count()), 256, 0, stream>>>(
+      reinterpret_cast<const uint4*>(Yw), pos, S, k, TD / 8, reinterpret_cast<uint4*>(out));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_uniform_bf16(__nv_bfloat16* dst, int64_t n, uint64_t seed,
+                                     uint64_t tensor_id, float scale, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  fill_uniform_bf16_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(dst, n, seed, tensor_id,
+                                                                          scale);
+  return cudaGetLastError();
+}
+
+}  // namespace moe

@@ -1,0 +1,69 @@
+"""CPU tests of the C-ABI boundary: the library loads, exports every symbol
+include/moe_capi.h declares, and fails loudly (no CPU fallback) without a GPU.
+"""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from paper_2303_06182_b200 import _capi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "moe_capi.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(moe_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_symbols_listed_in_binding():
+    assert declared_symbols() == sorted(_capi.EXPORTED)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _capi.load()
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    assert lib.moe_version() == 1
+
+
+def test_cxx_dropin_library_exports_reference_api():
+    path = os.path.join(ROOT, "paper_2303_06182_b200", "libmoesim_b200.so")
+    assert os.path.exists(path)
+    out = os.popen(f"nm -DC {path}").read()
+    for sym in ["moesim::dynamic_dispatch(moesim::Batch const&, moesim::GatingConfig const&)",
+                "moesim::static_dispatch(moesim::Batch const&, moesim::GatingConfig const&)",
+                "moesim::expert_capacity(double, int)", "moesim::waste_factor(int, double, int)",
+                "moesim::dispatch_mask_elements(int, int, double)",
+                "moesim::dispatch_cost_counts(moesim::DynamicDispatchPlan const&, int)",
+                "moesim::debug_json[abi:cxx11](moesim::StaticDispatchPlan const&)",
+                "moesim::debug_json[abi:cxx11](moesim::DynamicDispatchPlan const&)"]:
+        assert sym in out, sym
+
+
+def test_pure_host_entry_points_work_without_gpu():
+    lib = _capi.load()
+    assert lib.moe_expert_capacity(0.05, 2048) == 103
+    assert lib.moe_expert_capacity(0.1, 30) == 3
+    assert lib.moe_status_string(5) == b"expert id out of range"
+
+
+def test_no_silent_cpu_fallback_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    lib = _capi.load()
+    h = C.c_void_p()
+    st = lib.moe_ctx_create(0, C.byref(h))
+    assert st == _capi.MOE_ERR_CUDA
+    assert b"no CUDA device" in lib.moe_last_error()
+    # the drop-in gating API raises instead of computing on the CPU
+    from paper_2303_06182_b200 import gating as G
+
+    G._ctx = None
+    with pytest.raises(_capi.MoeError):
+        G.dynamic_dispatch(G.Batch([G.TokenAssignment([0], [1.0])]), G.GatingConfig(2, 1))
