@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""bench.py -- MoE-layer tokens/s & p50 latency, dynamic gating, on B200.
+
+Metric (BASELINE.json): "MoE-layer tokens/s & p50 latency, dynamic gating,
+1/2/4/8 B200 vs CPU ref".  Workload at N=1: configs[1], the LM MoE layer
+(TD=1024, HD=4096, E=512, top-2, batch 8 x seq 2048 = 16384 tokens), dynamic
+gating, bf16 weights/activations with fp32 accumulation, random-init experts,
+synthetic tokens.
+
+A step = one MoE-layer forward (gate + top-k, dispatch, gather, grouped expert
+FFN, combine) over one batch of tokens resident in HBM.  Timing: W warm-up
+steps, then K steps bracketed by barrier + cuda synchronize, CUDA events on the
+launching stream, max over ranks.  The per-step working set (8.7 GB of expert
+weights) is ~70x the 126 MB L2, so no L2 flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                  [--workload lm|mt|cfg1|lm-static|mt-static]
+
+N > 1 (torchrun): one rank per GPU; each rank runs the full layer on its own
+16384 tokens with all experts resident (replicas, weak scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (S, TD, HD, E, k, mode, C, description)
+    "lm": (16384, 1024, 4096, 512, 2, "dynamic", 0.0,
+           "configs[1]: LM MoE layer TD=1024 HD=4096 E=512 top-2, batch 8 x seq 2048, dynamic gating"),
+    "lm-static": (16384, 1024, 4096, 512, 2, "static", 0.05,
+                  "configs[1] comparison: LM layer, static gating CF=0.05 (cap 820)"),
+    "mt": (6144, 2048, 8192, 128, 2, "dynamic", 0.0,
+           "configs[2]: MT MoE layer TD=2048 HD=8192 E=128 top-2, batch 48 x seq 128, dynamic gating"),
+    "mt-static": (6144, 2048, 8192, 128, 2, "static", 1.0,
+                  "configs[2] comparison: MT layer, static gating CF=1 (cap 6144)"),
+    "cfg1": (2048, 1024, 4096, 8, 1, "dynamic", 0.0,
+             "configs[0] shape: LM layer TD=1024 HD=4096 E=8 top-1, 2048 tokens"),
+}
+STAGES = ["gate_topk", "route", "gather", "ffn_gemm1", "ffn_gemm2", "combine"]
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampler (runs across the timed region)."""
+
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.t_start = self.t_stop = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+        t0 = time.time()
+        while not self.rows and time.time() - t0 < 5:
+            time.sleep(0.02)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), line.strip()))
+
+    def mark_start(self):
+        self.t_start = time.time()
+
+    def mark_stop(self):
+        self.t_stop = time.time()
+
+    def stop(self):
+        if self.proc:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        inside = [r for (t, r) in self.rows if self.t_start and self.t_start - 0.06 <= t <= (self.t_stop or t) + 0.06]
+        use = inside or [r for (_, r) in self.rows[-3:]]
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in use:
+            f = [x.strip() for x in r.split(",")]
+            try:
+                sm.append(float(f[2]))
+                mx.append(float(f[3]))
+            except Exception:
+                continue
+            for n, v in zip(names, f[6:10]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(use), "samples_in_timed_region": len(inside)}
+
+
+def ffn_bytes(rows, active, TD, HD):
+    """Algorithmic HBM bytes of the grouped FFN (both launches), bf16:
+    each active expert's W1 and W2 read once, Xp read, H written then read,
+    Yw written."""
+    g1 = active * HD * TD * 2 + rows * TD * 2 + rows * HD * 2
+    g2 = active * TD * HD * 2 + rows * HD * 2 + rows * TD * 2
+    return g1, g2
+
+
+def layer_roofline(S, TD, HD, E, k, active, hbm_gbs, tflops):
+    """F = 2 S TD E + 4 k S TD HD; B = S TD 2 + E TD 2 +
+    A 2 TD HD 2 + S TD 2 (bf16).  T_roof = max(F / P_tc, B / BW)."""
+    F = 2.0 * S * TD * E + 4.0 * k * S * TD * HD
+    B = S * TD * 2 + E * TD * 2 + active * 2 * TD * HD * 2 + S * TD * 2
+    return max(F / (tflops * 1e12), B / (hbm_gbs * 1e9)), F, B
+
+
+def load_traffic(workload):
+    """dram bytes per FFN launch pair from a committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ffn_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(workload)
+    except Exception:
+        return None
+
+
+def dist_setup():
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path for this layer on the host
+    cores (oracle/cpu_layer.py; routing = the reference's gating.cpp compiled
+    verbatim), each step a bounded sample of the same workload."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle.cpu_layer import cpu_layer_sample
+
+    S, TD, HD, E, k, mode, C, desc = WORKLOADS[args.workload]
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_layer_sample(S, TD, HD, E, k, n_sample_experts=2)
+    vals, secs = [], []
+    r = None
+    for _ in range(max(1, min(args.steps, 3))):
+        r = cpu_layer_sample(S, TD, HD, E, k)
+        vals.append(r["tokens_per_s"])
+        secs.append(r["seconds_per_layer"])
+    vals.sort()
+    v = vals[len(vals) // 2]
+    secs.sort()
+    sample = (f"full-batch gate/top-k/dispatch/combine + expert FFN for experts 0..7 "
+              f"({r['sampled_slots']}/{r['total_slots']} slots) scaled to all slots; "
+              f"dispatch = {r['dispatch_impl']}; numpy/OpenBLAS fp32")
+    line = {
+        "metric": "MoE-layer tokens/s (dynamic gating)", "value": v, "unit": "tokens/s",
+        "impl": "reference", "n_gpus": world, "steps": len(vals), "warmup": min(args.warmup, 1),
+        "ms_per_step": secs[len(secs) // 2] * 1e3, "p50_ms": secs[len(secs) // 2] * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (counter-hash uniform tokens; random-init experts)",
+        "config": {"workload": desc, "S": S, "TD": TD, "HD": HD, "E": E, "top_k": k, "gating": mode},
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": r["cores"], "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "breakdown_s": r["breakdown_s"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args):
+    import numpy as np
+    import torch
+
+    from paper_2303_06182_b200 import _capi
+    from paper_2303_06182_b200.layer import LayerShape, MoeLayer, make_tokens, make_weights
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    S, TD, HD, E, k, mode, C, desc = WORKLOADS[args.workload]
+    hbm_gbs, tflops, peak_kind = measured_peaks()
+    shape = LayerShape(TD, HD, E, k)
+    seed = 2303061820 + rank
+    weights = make_weights(shape, seed=2303061820)
+    layer = MoeLayer(shape, S, mode=mode, capacity_factor=C if mode == "static" else 1.0, weights=weights,
+                     tile_n=args.tile_n)
+    x = make_tokens(S, TD, seed=seed)
+    out = torch.empty_like(x)
+    stream = torch.cuda.Stream()
+    lib = layer.ctx.lib
+    K, W = args.steps, args.warmup
+    _capi.check(lib.moe_layer_enable_timing(layer.h, K))
+
+    with torch.cuda.stream(stream):
+        for _ in range(W):
+            layer.forward(x, out, stream=stream)
+    stream.synchronize()
+    layer.check_errors(stream)
+    v = layer.view()
+    counts = v["counts"].cpu().numpy()
+    active = int((counts > 0).sum()) if mode == "dynamic" else E
+    rows = int(v["rows"])
+    # reset the timing ring so slot i <-> timed step i
+    _capi.check(lib.moe_layer_enable_timing(layer.h, K))
+
+    sampler = ClockSampler(local) if not args.no_clocks else None
+    if sampler:
+        sampler.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.mark_start()
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+        for _ in range(K):
+            layer.forward(x, out, stream=stream)
+        ev1.record(stream)
+    stream.synchronize()
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.mark_stop()
+    barrier(world)
+    elapsed_ms = ev0.elapsed_time(ev1)
+    layer.check_errors(stream)
+    stage = np.zeros((K, len(STAGES)), np.float64)
+    import ctypes
+
+    buf = (ctypes.c_float * len(STAGES))()
+    for i in range(K):
+        _capi.check(lib.moe_layer_stage_times(layer.h, i, ctypes.cast(buf, ctypes.c_void_p)))
+        stage[i] = list(buf)
+    step_ms = stage.sum(1)
+    elapsed_max = max_over_ranks(elapsed_ms, world)
+    p50 = float(np.median(step_ms))
+    p50_max = max_over_ranks(p50, world)
+    if sampler:
+        sampler.stop()
+    clocks = sampler.summary() if sampler else None
+
+    # ---- e2e through the public C-ABI host path (pinned host in/out, copies in the timed region)
+    xh = x.cpu().pin_memory()
+    oh = torch.empty_like(xh).pin_memory()
+    Ke = max(3, min(K, args.e2e_steps))
+    for _ in range(2):
+        layer.forward_host(xh, oh, stream=stream)
+    barrier(world)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(Ke):
+        layer.forward_host(xh, oh, stream=stream)
+    e1.record(stream)
+    e1.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / Ke, world)
+
+    if rank != 0:
+        return
+    ms_per_step = elapsed_max / K
+    value = world * S / (ms_per_step * 1e-3)
+    mean_stage = stage.mean(0)
+    g1b, g2b = ffn_bytes(rows, active, TD, HD)
+    ffn_ms = mean_stage[3] + mean_stage[4]
+    achieved = (g1b + g2b) / (ffn_ms * 1e-3) / 1e9
+    traffic = load_traffic(args.workload)
+    t_roof, F, B = layer_roofline(S, TD, HD, E, k, active, hbm_gbs, tflops)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle.cpu_layer import cpu_layer_sample
+
+        r = cpu_layer_sample(S, TD, HD, E, k)
+        cpu = {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": r["cores"], "kind": "port",
+               "sample": (f"full-batch gate/top-k/dispatch/combine + expert FFN for experts 0..7 "
+                          f"({r['sampled_slots']}/{r['total_slots']} slots) scaled to all slots; dispatch = "
+                          f"{r['dispatch_impl']}; numpy/OpenBLAS fp32; {r['measured_cpu_seconds']:.1f} s measured"),
+               "breakdown_s": r["breakdown_s"]}
+    line = {
+        "metric": "MoE-layer tokens/s (dynamic gating)" if mode == "dynamic" else "MoE-layer tokens/s (static gating)",
+        "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms_per_step, "p50_ms": p50_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (counter-hash uniform tokens; random-init experts, std 1/sqrt(fan-in))",
+        "config": {"workload": desc, "S_per_gpu": S, "TD": TD, "HD": HD, "E": E, "top_k": k, "gating": mode,
+                   "capacity_factor": C if mode == "static" else None, "rows": rows, "active_experts": active,
+                   "tile_n": int(v["tile_n"]),
+                   "parallelism": f"replicas x{world} (all experts on every GPU)" if world > 1 else "single GPU",
+                   "l2": "no flush: per-step working set (expert weights, %.1f GB) >> 126 MB L2" % (
+                       2 * active * TD * HD * 2 / 1e9)},
+        "roofline": {"kernel": "grouped_gemm_kernel (FFN GEMM1 + GEMM2)", "bound": "hbm",
+                     "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s", "frac": achieved / hbm_gbs,
+                     "peak_kind": peak_kind, "algorithmic_bytes_per_step": g1b + g2b,
+                     "traffic": traffic},
+        "layer_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms_per_step, "flops": F,
+                           "bytes": B, "peaks": {"hbm_gbs": hbm_gbs, "bf16_tflops": tflops}},
+        "stage_ms": {n: float(m) for n, m in zip(STAGES, mean_stage)},
+        "gpu_launches": 6 * K,
+        "e2e": {"value": world * S / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": S * TD * 2, "d2h_bytes_per_step": S * TD * 2,
+                "api": "moe_layer_forward_host (C ABI, pinned host buffers)"},
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "gpu": torch.cuda.get_device_name(local),
+    }
+    print(json.dumps(line), flush=True)
+    if args.json_out:
+        with open(args.json_out, "w") as f:
+            json.dump(line, f, indent=1)
+    layer.close()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference", "ours"])
+    ap.add_argument("--workload", default="lm", choices=sorted(WORKLOADS))
+    ap.add_argument("--tile-n", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--json-out", default="")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -170,6 +170,15 @@ int moe_layer_forward_graph(moe_layer* layer, const void* X, int S, void* out, v
 int moe_layer_forward_host(moe_layer* layer, const void* X_host, int S, void* out_host,
                            void* stream);
 
+/* Per-stage CUDA-event timing of moe_layer_forward (eager path only).
+ * Stages: 0 gate, 1 route, 2 gather, 3 FFN GEMM1, 4 FFN GEMM2, 5 combine.
+ * enable: n_slots > 0 allocates a ring of n_slots event sets; call i records
+ * into slot i % n_slots.  stage_times reads slot `slot` (synchronises on its
+ * last event) into ms[MOE_NUM_STAGES]. */
+#define MOE_NUM_STAGES 6
+int moe_layer_enable_timing(moe_layer* layer, int n_slots);
+int moe_layer_stage_times(moe_layer* layer, int slot, float* ms);
+
 /* Device pointers of the layer's internal buffers (valid until destroy), for
  * parity checks.  Any field may be NULL when not applicable. */
 typedef struct moe_layer_view {

@@ -30,7 +30,7 @@ EXPORTED = [
     "moe_check_errors", "moe_gate_topk", "moe_gather_rows", "moe_combine", "moe_fill_uniform_bf16",
     "moe_layer_create", "moe_layer_destroy", "moe_layer_forward", "moe_layer_forward_graph",
     "moe_layer_forward_host", "moe_layer_get_view", "moe_layer_set_weight_pool",
-    "moe_exchange_counts_host",
+    "moe_exchange_counts_host", "moe_layer_enable_timing", "moe_layer_stage_times",
 ]
 
 
@@ -107,6 +107,8 @@ def load(path: str = LIB_PATH):
     _sig(lib.moe_layer_get_view, I, P, C.POINTER(LayerView))
     _sig(lib.moe_layer_set_weight_pool, I, P, P, P, I, P)
     _sig(lib.moe_exchange_counts_host, I, P, P, I, I, I, P, I, P)
+    _sig(lib.moe_layer_enable_timing, I, P, I)
+    _sig(lib.moe_layer_stage_times, I, P, I, P)
     _lib = lib
     return lib
 

@@ -149,8 +149,12 @@ struct moe_ctx {
     }
     int st = block_hist.reserve((size_t)E * route_max_blocks + route_max_blocks);
     if (st) return st;
-    st = err_flag.reserve(1);
-    if (st) return st;
+    if (!err_flag.p) {
+      st = err_flag.reserve(1);
+      if (st) return st;
+      cudaError_t e = cudaMemset(err_flag.p, 0, sizeof(int32_t));
+      if (e != cudaSuccess) return cuda_fail(e, "clear error flag");
+    }
     return MOE_OK;
   }
 };
@@ -176,6 +180,10 @@ struct moe_layer {
   DevBuf<__nv_bfloat16> xp, h, yw, xin, yout;
   int last_rows = 0;
   int last_cap = 0;
+  // per-stage timing ring (eager path)
+  std::vector<cudaEvent_t> tev;
+  int t_slots = 0;
+  long t_calls = 0;
   // graph cache
   cudaGraphExec_t gexec = nullptr;
   const void* g_x = nullptr;
@@ -608,6 +616,7 @@ int moe_layer_destroy(moe_layer* L) {
   if (!L) return MOE_OK;
   cudaSetDevice(L->ctx->device);
   if (L->gexec) cudaGraphExecDestroy(L->gexec);
+  for (cudaEvent_t e : L->tev) cudaEventDestroy(e);
   L->idx.release();
   L->w.release();
   L->pos.release();
@@ -630,8 +639,17 @@ int moe_layer_destroy(moe_layer* L) {
   return MOE_OK;
 }
 
-static int layer_forward_impl(moe_layer* L, const void* X, int S, void* out, cudaStream_t s) {
+static int layer_forward_impl(moe_layer* L, const void* X, int S, void* out, cudaStream_t s,
+                              bool timed = false) {
   const moe_layer_desc& d = L->d;
+  cudaEvent_t* ev = nullptr;
+  if (timed && L->t_slots > 0) {
+    ev = &L->tev[(size_t)(L->t_calls % L->t_slots) * (MOE_NUM_STAGES + 1)];
+    ++L->t_calls;
+  }
+  auto mark = [&](int i) {
+    if (ev) cudaEventRecord(ev[i], s);
+  };
   if (S < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "empty batch");
   if (S > d.max_tokens) return fail(MOE_ERR_INVALID_ARGUMENT, "S exceeds max_tokens");
   const int k = d.top_k, E = d.num_experts, TD = d.token_dim, HD = d.hidden_dim;
@@ -642,6 +660,7 @@ static int layer_forward_impl(moe_layer* L, const void* X, int S, void* out, cud
     L->tmX_rows = S;
   }
   // 1. gate
+  mark(0);
   GateArgs ga{S, TD, E, k, L->idx.p, L->w.p, d.keep_logits ? L->logits.p : nullptr};
   cudaError_t e = launch_gate(L->tmX, L->tmWg, ga, s);
   if (e != cudaSuccess) return cuda_fail(e, "gate launch");
@@ -653,29 +672,59 @@ static int layer_forward_impl(moe_layer* L, const void* X, int S, void* out, cud
   }
   L->last_rows = rows;
   L->last_cap = cap;
+  mark(1);
   st = route_common(L->ctx, L->idx.p, S, k, E, cap, L->counts.p, L->splits.p, L->order.p,
                     L->pos.p, L->w.p, L->wpos.p, L->dropped.p, L->n_dropped.p, L->items.p,
                     L->n_items.p, L->tile_n, nullptr, 0, s);
   if (st) return st;
   // 3. gather token rows into expert-grouped order
+  mark(2);
   e = launch_gather_rows((const __nv_bfloat16*)X, L->order.p, rows, k, TD, L->xp.p, s);
   if (e != cudaSuccess) return cuda_fail(e, "gather launch");
   // 4. grouped FFN
+  mark(3);
   GemmArgs g1{L->items.p, L->n_items.p, L->slot_of, HD, TD, kEpiReluBf16, L->h.p, nullptr};
   e = launch_grouped_gemm(L->tmW1, L->tmXp, g1, L->tile_n, L->ctx->sms, s);
   if (e != cudaSuccess) return cuda_fail(e, "grouped gemm 1 launch");
+  mark(4);
   GemmArgs g2{L->items.p, L->n_items.p, L->slot_of, TD, HD, kEpiScaleBf16, L->yw.p, L->wpos.p};
   e = launch_grouped_gemm(L->tmW2, L->tmH, g2, L->tile_n, L->ctx->sms, s);
   if (e != cudaSuccess) return cuda_fail(e, "grouped gemm 2 launch");
   // 5. combine
+  mark(5);
   e = launch_combine(L->yw.p, L->pos.p, S, k, TD, (__nv_bfloat16*)out, s);
   if (e != cudaSuccess) return cuda_fail(e, "combine launch");
+  mark(6);
   return MOE_OK;
 }
 
 int moe_layer_forward(moe_layer* L, const void* X, int S, void* out, void* stream) {
   if (!L || !X || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
-  return layer_forward_impl(L, X, S, out, (cudaStream_t)stream);
+  return layer_forward_impl(L, X, S, out, (cudaStream_t)stream, true);
+}
+
+int moe_layer_enable_timing(moe_layer* L, int n_slots) {
+  if (!L || n_slots < 0) return fail(MOE_ERR_INVALID_ARGUMENT, "bad timing request");
+  for (cudaEvent_t e : L->tev) cudaEventDestroy(e);
+  L->tev.clear();
+  L->t_slots = 0;
+  L->t_calls = 0;
+  for (int i = 0; i < n_slots * (MOE_NUM_STAGES + 1); ++i) {
+    cudaEvent_t e;
+    MOE_CUDA(cudaEventCreate(&e));
+    L->tev.push_back(e);
+  }
+  L->t_slots = n_slots;
+  return MOE_OK;
+}
+
+int moe_layer_stage_times(moe_layer* L, int slot, float* ms) {
+  if (!L || !ms || slot < 0 || slot >= L->t_slots)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "bad timing slot");
+  cudaEvent_t* ev = &L->tev[(size_t)slot * (MOE_NUM_STAGES + 1)];
+  MOE_CUDA(cudaEventSynchronize(ev[MOE_NUM_STAGES]));
+  for (int i = 0; i < MOE_NUM_STAGES; ++i) MOE_CUDA(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
+  return MOE_OK;
 }
 
 int moe_layer_forward_graph(moe_layer* L, const void* X, int S, void* out, void* stream) {

@@ -20,6 +20,8 @@
 // running top-k in registers, optional fp32 logits store for parity checks.
 #include <float.h>
 
+#include <mutex>
+
 #include "moe_internal.h"
 #include "ptx.cuh"
 
@@ -237,9 +239,16 @@ __global__ void __launch_bounds__(256, 1)
 int gate_box_rows(int E) { return gate_layout(E).box_rows; }
 
 cudaError_t gate_prepare(int E) {
+  // process-wide kernel attribute: only raise it (see route_prepare)
+  static std::mutex mu;
+  static int granted = 0;
   const GateLayout L = gate_layout(E);
-  return cudaFuncSetAttribute(gate_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              L.smem);
+  std::lock_guard<std::mutex> lock(mu);
+  if (L.smem <= granted) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(gate_topk_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem);
+  if (e == cudaSuccess) granted = L.smem;
+  return e;
 }
 
 cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateArgs& a,

@@ -19,6 +19,8 @@
 // slot-order compaction of the dropped assignments and the placeholder fill.
 #include <cooperative_groups.h>
 
+#include <mutex>
+
 #include "moe_internal.h"
 
 namespace cg = cooperative_groups;
@@ -302,10 +304,23 @@ cudaError_t launch_route(RouteArgs a, int max_blocks, cudaStream_t stream) {
 }
 
 cudaError_t route_prepare(int E, int* max_blocks) {
+  // The dynamic-smem limit is a process-wide attribute of the kernel: only
+  // ever raise it, so a context prepared for a large E is never undercut by
+  // another one preparing a small E.
+  static std::mutex mu;
+  static size_t granted = 0;
   const size_t smem = route_smem_bytes(E);
-  cudaError_t err = cudaFuncSetAttribute(route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-  if (err != cudaSuccess) return err;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (smem > granted) {
+      cudaError_t err = cudaFuncSetAttribute(
+          route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (err != cudaSuccess) return err;
+      granted = smem;
+    }
+  }
+  cudaError_t err;
   int per_sm = 0, dev = 0, sms = 0;
   err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, route_kernel, kRouteThreads, smem);
   if (err != cudaSuccess) return err;
