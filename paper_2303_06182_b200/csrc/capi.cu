@@ -147,7 +147,7 @@ struct moe_ctx {
       route_max_blocks = mb;
       route_prepared_E = E;
     }
-    int st = block_hist.reserve((size_t)E * route_max_blocks + route_max_blocks);
+    int st = block_hist.reserve((size_t)E * (route_max_blocks + 4) + route_max_blocks);
     if (st) return st;
     if (!err_flag.p) {
       st = err_flag.reserve(1);
