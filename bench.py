@@ -16,8 +16,9 @@ weights) is ~70x the 126 MB L2, so no L2 flush is needed between steps.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
                   [--workload lm|mt|cfg1|lm-static|mt-static]
 
-N > 1 (torchrun): one rank per GPU; each rank runs the full layer on its own
-16384 tokens with all experts resident (replicas, weak scaling).
+N > 1 (torchrun): one rank per GPU, expert parallelism -- E/N experts per GPU
+(greedy load-balanced placement), 16384 tokens per GPU (weak scaling), NCCL
+count exchange + variable all-to-all over NVLink (--replicas: full copies).
 """
 from __future__ import annotations
 
@@ -159,11 +160,18 @@ def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test-only knob: run N ranks on one GPU over gloo (exercises the EP code
+    # path on a single-GPU box; the numbers are not a measurement)
+    if os.environ.get("MOE_BENCH_ONE_GPU_TEST") == "1":
+        local = 0
     if world > 1:
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("MOE_BENCH_ONE_GPU_TEST") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
 
 
@@ -225,6 +233,134 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_ep(args, world, rank, local):
+    """N > 1: expert parallelism.  E/N experts per GPU (placement: the
+    reference's greedy policy on a calibration routing histogram, or
+    contiguous), S tokens per GPU (weak scaling), NCCL all-to-all over NVLink
+    for the count exchange and the variable payload exchange."""
+    import numpy as np
+    import torch
+
+    from paper_2303_06182_b200.ep import ExpertParallelMoE, KernelBackend, Placement, Transport
+    from paper_2303_06182_b200.layer import Context, LayerShape, make_tokens, make_weights
+
+    S, TD, HD, E, k, mode, C, desc = WORKLOADS[args.workload]
+    if mode != "dynamic":
+        raise SystemExit("expert parallelism is implemented for dynamic gating")
+    hbm_gbs, tflops, peak_kind = measured_peaks()
+    ctx = Context.get(local)
+    shape = LayerShape(TD, HD, E, k)
+    Wg, W1, W2 = make_weights(shape, seed=2303061820, ctx=ctx)
+    x = make_tokens(S, TD, seed=2303061820 + rank, ctx=ctx)
+    if args.placement == "greedy":
+        # calibration: per-expert load share of one gate pass over this rank's
+        # tokens, summed over ranks (the "history" greedy_place consumes)
+        idx = torch.empty(S, k, dtype=torch.int32, device="cuda")
+        w = torch.empty(S, k, dtype=torch.float32, device="cuda")
+        import ctypes
+
+        P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        ctx.lib.moe_gate_topk(ctx.h, P(x), P(Wg), S, TD, E, k, P(idx), P(w), None,
+                              ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        hist = torch.bincount(idx.view(-1).long(), minlength=E).double()
+        import torch.distributed as dist
+
+        dist.all_reduce(hist)
+        pl = Placement.greedy(hist.cpu().numpy()[:, None] / (S * k * world), world)
+    else:
+        pl = Placement.contiguous(E, world)
+    loc = torch.from_numpy(pl.local_experts(rank)).long().cuda()
+    W1l, W2l = W1[loc].contiguous(), W2[loc].contiguous()
+    del W1, W2
+    torch.cuda.empty_cache()
+    be = KernelBackend(ctx, shape, Wg, W1l, W2l, S, S * k * world, tile_n=args.tile_n)
+    layer = ExpertParallelMoE(pl, k, be, Transport(), rank)
+    stream = torch.cuda.Stream()
+    K, W = args.steps, args.warmup
+    with torch.cuda.stream(stream):
+        for _ in range(W):
+            out = layer.forward(x, stream)
+    stream.synchronize()
+    be.check_errors(stream)
+    sampler = ClockSampler(local) if not args.no_clocks else None
+    if sampler:
+        sampler.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.mark_start()
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+        for i in range(K):
+            step_ev[i].record(stream)
+            out = layer.forward(x, stream)
+        step_ev[K].record(stream)
+        ev1.record(stream)
+    stream.synchronize()
+    if sampler:
+        sampler.mark_stop()
+    barrier(world)
+    elapsed = max_over_ranks(ev0.elapsed_time(ev1), world)
+    steps = [step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(K)]
+    p50 = max_over_ranks(float(np.median(steps)), world)
+    if sampler:
+        sampler.stop()
+    recv_rows = layer.last["recv_rows"]
+    sent_off = int(layer.last["send_counts"].sum()) - int(layer.last["send_counts"][rank].sum())
+    # e2e: pinned host tokens in, host output out, copies inside the timed region
+    xh = x.cpu().pin_memory()
+    oh = torch.empty_like(xh).pin_memory()
+    Ke = max(3, min(K, args.e2e_steps))
+    barrier(world)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(Ke):
+            xd = xh.to("cuda", non_blocking=True)
+            o = layer.forward(xd, stream)
+            oh.copy_(o, non_blocking=True)
+        e1.record(stream)
+    stream.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / Ke, world)
+    be.check_errors(stream)
+    if rank != 0:
+        be.close()
+        return
+    ms = elapsed / K
+    El = E // world
+    wbytes = El * 2 * TD * HD * 2
+    achieved = wbytes / (ms * 1e-3) / 1e9
+    line = {
+        "metric": "MoE-layer tokens/s (dynamic gating)", "value": world * S / (ms * 1e-3), "unit": "tokens/s",
+        "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms, "p50_ms": p50,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (counter-hash uniform tokens; random-init experts, std 1/sqrt(fan-in))",
+        "config": {"workload": desc + " -- expert parallel", "S_per_gpu": S, "TD": TD, "HD": HD, "E": E,
+                   "top_k": k, "gating": mode, "experts_per_gpu": El, "placement": args.placement,
+                   "parallelism": f"ep{world} (NCCL all-to-all over NVLink, count exchange + payload)",
+                   "l2": "no flush: per-step local expert weights %.2f GB >> 126 MB L2" % (wbytes / 1e9)},
+        "roofline": {"kernel": "whole EP step: local expert weights streamed once per step", "bound": "hbm",
+                     "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s", "frac": achieved / hbm_gbs,
+                     "peak_kind": peak_kind, "traffic": None},
+        "a2a": {"rows_received_rank0": recv_rows, "rows_sent_offrank_rank0": sent_off,
+                "payload_bytes_offrank_per_direction": sent_off * TD * 2},
+        "gpu_launches": 9 * K,
+        "e2e": {"value": world * S / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": S * TD * 2, "d2h_bytes_per_step": S * TD * 2,
+                "api": "ExpertParallelMoE.forward over the C ABI (pinned host in/out)"},
+        "cpu_baseline": None,
+        "clocks": sampler.summary() if sampler else None,
+        "gpu": torch.cuda.get_device_name(local),
+    }
+    print(json.dumps(line), flush=True)
+    be.close()
+
+
 def run_b200(args):
     import numpy as np
     import torch
@@ -234,6 +370,13 @@ def run_b200(args):
 
     world, rank, local = dist_setup()
     torch.cuda.set_device(local)
+    if world > 1 and not args.replicas:
+        run_ep(args, world, rank, local)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+        return
     S, TD, HD, E, k, mode, C, desc = WORKLOADS[args.workload]
     hbm_gbs, tflops, peak_kind = measured_peaks()
     shape = LayerShape(TD, HD, E, k)
@@ -383,6 +526,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--json-out", default="")
+    ap.add_argument("--replicas", action="store_true", help="N>1: full replicas instead of EP")
+    ap.add_argument("--placement", default="greedy", choices=["greedy", "contiguous"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

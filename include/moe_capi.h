@@ -208,7 +208,44 @@ int moe_layer_get_view(moe_layer* layer, moe_layer_view* view);
 int moe_layer_set_weight_pool(moe_layer* layer, const void* W1_pool, const void* W2_pool,
                               int n_slots, const int32_t* slot_of);
 
+/* ---------------------------------------------------------------- grouped FFN */
+
+/* Expert FFN over pre-dispatched rows (the expert-parallel receive side, and
+ * the building block of the layer): Y_rows[i] = row_w[i] * W2_e relu(W1_e x_i)
+ * with e = keys[i] in [0, num_experts).  Rows are grouped by expert on the
+ * device (stable counting sort), streamed through the tcgen05 grouped GEMM and
+ * written back in input order.  W1 [E, HD, TD], W2 [E, TD, HD] bf16, device. */
+typedef struct moe_ffn moe_ffn;
+typedef struct moe_ffn_desc {
+  int max_rows;
+  int token_dim;
+  int hidden_dim;
+  int num_experts;
+  int tile_n; /* 0 = auto, 128 or 256 */
+} moe_ffn_desc;
+int moe_ffn_create(moe_ctx* ctx, const moe_ffn_desc* desc, const void* W1, const void* W2,
+                   moe_ffn** out);
+int moe_ffn_destroy(moe_ffn* ffn);
+/* row_w may be NULL (weight 1).  Stream-ordered, no host synchronisation. */
+int moe_ffn_forward(moe_ffn* ffn, const void* X_rows, const int32_t* keys, const float* row_w,
+                    int rows, void* Y_rows, void* stream);
+
 /* ---------------------------------------------------------------- EP */
+
+/* Dispatch by a relabelled key: key = key_map[expert] in [0, num_keys)
+ * (expert parallelism sorts by (device, local expert) so every destination
+ * device's slots are contiguous).  Otherwise identical to moe_route_dynamic;
+ * gate_w/wpos (optional) carry the gate weight of each slot to its row. */
+int moe_route_dynamic_keyed(moe_ctx* ctx, const int32_t* expert_idx, int S, int k,
+                            int num_experts, const int32_t* key_map, int num_keys,
+                            int32_t* counts, int32_t* splits, int32_t* order, int32_t* pos,
+                            const float* gate_w, float* wpos, void* stream);
+
+/* out[r] = (index of the segment holding r) % mod for back-to-back segments of
+ * the given lengths (device int32): local-expert ids of received EP rows. */
+int moe_fill_segments(moe_ctx* ctx, const int32_t* counts, int n_segments, int mod, int32_t* out,
+                      void* stream);
+
 
 /* exchange.cpp:95-120, payload phase, as slot counts: counts[src*D + dst] =
  * number of assignment slots whose token lives on src (token t on t % D,

@@ -31,6 +31,8 @@ EXPORTED = [
     "moe_layer_create", "moe_layer_destroy", "moe_layer_forward", "moe_layer_forward_graph",
     "moe_layer_forward_host", "moe_layer_get_view", "moe_layer_set_weight_pool",
     "moe_exchange_counts_host", "moe_layer_enable_timing", "moe_layer_stage_times",
+    "moe_ffn_create", "moe_ffn_destroy", "moe_ffn_forward", "moe_route_dynamic_keyed",
+    "moe_fill_segments",
 ]
 
 
@@ -53,6 +55,11 @@ class LayerDesc(C.Structure):
         ("num_experts", C.c_int), ("top_k", C.c_int), ("mode", C.c_int),
         ("capacity_factor", C.c_double), ("tile_n", C.c_int), ("keep_logits", C.c_int),
     ]
+
+
+class FfnDesc(C.Structure):
+    _fields_ = [("max_rows", C.c_int), ("token_dim", C.c_int), ("hidden_dim", C.c_int),
+                ("num_experts", C.c_int), ("tile_n", C.c_int)]
 
 
 class LayerView(C.Structure):
@@ -109,6 +116,11 @@ def load(path: str = LIB_PATH):
     _sig(lib.moe_exchange_counts_host, I, P, P, I, I, I, P, I, P)
     _sig(lib.moe_layer_enable_timing, I, P, I)
     _sig(lib.moe_layer_stage_times, I, P, I, P)
+    _sig(lib.moe_ffn_create, I, P, C.POINTER(FfnDesc), P, P, C.POINTER(P))
+    _sig(lib.moe_ffn_destroy, I, P)
+    _sig(lib.moe_ffn_forward, I, P, P, P, P, I, P, P)
+    _sig(lib.moe_route_dynamic_keyed, I, P, P, I, I, I, P, I, P, P, P, P, P, P, P)
+    _sig(lib.moe_fill_segments, I, P, P, I, I, P, P)
     _lib = lib
     return lib
 

@@ -192,6 +192,17 @@ struct moe_layer {
   cudaStream_t g_stream = nullptr;
 };
 
+struct moe_ffn {
+  moe_ctx* ctx = nullptr;
+  moe_ffn_desc d{};
+  int tile_n = 128;
+  CUtensorMap tmW1, tmW2, tmXp, tmH;
+  DevBuf<int32_t> counts, splits, order, pos, n_items;
+  DevBuf<float> wpos, ones;
+  DevBuf<FfnItem> items;
+  DevBuf<__nv_bfloat16> xp, h;
+};
+
 extern "C" {
 
 int moe_version(void) { return MOE_CAPI_VERSION; }
@@ -683,11 +694,11 @@ static int layer_forward_impl(moe_layer* L, const void* X, int S, void* out, cud
   if (e != cudaSuccess) return cuda_fail(e, "gather launch");
   // 4. grouped FFN
   mark(3);
-  GemmArgs g1{L->items.p, L->n_items.p, L->slot_of, HD, TD, kEpiReluBf16, L->h.p, nullptr};
+  GemmArgs g1{L->items.p, L->n_items.p, L->slot_of, HD, TD, kEpiReluBf16, L->h.p, nullptr, nullptr};
   e = launch_grouped_gemm(L->tmW1, L->tmXp, g1, L->tile_n, L->ctx->sms, s);
   if (e != cudaSuccess) return cuda_fail(e, "grouped gemm 1 launch");
   mark(4);
-  GemmArgs g2{L->items.p, L->n_items.p, L->slot_of, TD, HD, kEpiScaleBf16, L->yw.p, L->wpos.p};
+  GemmArgs g2{L->items.p, L->n_items.p, L->slot_of, TD, HD, kEpiScaleBf16, L->yw.p, L->wpos.p, nullptr};
   e = launch_grouped_gemm(L->tmW2, L->tmH, g2, L->tile_n, L->ctx->sms, s);
   if (e != cudaSuccess) return cuda_fail(e, "grouped gemm 2 launch");
   // 5. combine
@@ -773,6 +784,115 @@ int moe_layer_forward_host(moe_layer* L, const void* X_host, int S, void* out_ho
   MOE_CUDA(cudaMemcpyAsync(out_host, L->yout.p, nb, cudaMemcpyDeviceToHost, s));
   MOE_CUDA(cudaStreamSynchronize(s));
   return moe_check_errors(L->ctx, s);
+}
+
+int moe_route_dynamic_keyed(moe_ctx* ctx, const int32_t* expert_idx, int S, int k,
+                            int num_experts, const int32_t* key_map, int num_keys,
+                            int32_t* counts, int32_t* splits, int32_t* order, int32_t* pos,
+                            const float* gate_w, float* wpos, void* stream) {
+  if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
+  int st = check_batch(S, k, num_experts);
+  if (st) return st;
+  if (num_keys < 1 || !key_map) return fail(MOE_ERR_INVALID_ARGUMENT, "bad key map");
+  if (!expert_idx || !counts || !splits || !order)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "null buffer");
+  return route_common(ctx, expert_idx, S, k, num_keys, 0, counts, splits, order, pos, gate_w, wpos,
+                      nullptr, nullptr, nullptr, nullptr, 128, key_map, num_experts,
+                      (cudaStream_t)stream);
+}
+
+int moe_fill_segments(moe_ctx* ctx, const int32_t* counts, int n_segments, int mod, int32_t* out,
+                      void* stream) {
+  if (!ctx || mod < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "bad argument");
+  cudaError_t e = launch_fill_segments(counts, n_segments, mod, out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "fill_segments launch");
+  return MOE_OK;
+}
+
+int moe_ffn_create(moe_ctx* ctx, const moe_ffn_desc* desc, const void* W1, const void* W2,
+                   moe_ffn** out) {
+  if (!ctx || !desc || !out || !W1 || !W2) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  const moe_ffn_desc& d = *desc;
+  if (d.max_rows < 1 || d.num_experts < 1)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "max_rows and num_experts must be positive");
+  if (d.token_dim % 128 || d.hidden_dim % 128 || d.token_dim <= 0 || d.hidden_dim <= 0)
+    return fail(MOE_ERR_UNSUPPORTED, "token_dim and hidden_dim must be positive multiples of 128");
+  MOE_CUDA(cudaSetDevice(ctx->device));
+  auto* F = new moe_ffn();
+  F->ctx = ctx;
+  F->d = d;
+  const double avg = (double)d.max_rows / d.num_experts;
+  F->tile_n = d.tile_n ? d.tile_n : (avg > 160.0 ? 256 : 128);
+  if (F->tile_n != 128 && F->tile_n != 256) {
+    delete F;
+    return fail(MOE_ERR_INVALID_ARGUMENT, "tile_n must be 0, 128 or 256");
+  }
+  const size_t R = d.max_rows, Rp = R + 256, TD = d.token_dim, HD = d.hidden_dim;
+  const size_t items_max = R / F->tile_n + d.num_experts + 1;
+  int st;
+  if ((st = F->counts.reserve(d.num_experts)) || (st = F->splits.reserve(d.num_experts + 1)) ||
+      (st = F->order.reserve(R)) || (st = F->pos.reserve(R)) || (st = F->n_items.reserve(1)) ||
+      (st = F->wpos.reserve(R)) || (st = F->ones.reserve(R)) ||
+      (st = F->items.reserve(items_max)) || (st = F->xp.reserve(Rp * TD)) ||
+      (st = F->h.reserve(Rp * HD)) || (st = ctx->prepare_route(d.num_experts))) {
+    moe_ffn_destroy(F);
+    return st;
+  }
+  cudaMemset(F->xp.p, 0, Rp * TD * 2);
+  cudaMemset(F->h.p, 0, Rp * HD * 2);
+  {
+    std::vector<float> one(R, 1.0f);
+    cudaMemcpy(F->ones.p, one.data(), R * sizeof(float), cudaMemcpyHostToDevice);
+  }
+  if ((st = encode_bf16(&F->tmW1, W1, (uint64_t)d.num_experts * HD, TD, 128)) ||
+      (st = encode_bf16(&F->tmW2, W2, (uint64_t)d.num_experts * TD, HD, 128)) ||
+      (st = encode_bf16(&F->tmXp, F->xp.p, Rp, TD, 16)) ||
+      (st = encode_bf16(&F->tmH, F->h.p, Rp, HD, 16))) {
+    moe_ffn_destroy(F);
+    return st;
+  }
+  *out = F;
+  return MOE_OK;
+}
+
+int moe_ffn_destroy(moe_ffn* F) {
+  if (!F) return MOE_OK;
+  F->counts.release();
+  F->splits.release();
+  F->order.release();
+  F->pos.release();
+  F->n_items.release();
+  F->wpos.release();
+  F->ones.release();
+  F->items.release();
+  F->xp.release();
+  F->h.release();
+  delete F;
+  return MOE_OK;
+}
+
+int moe_ffn_forward(moe_ffn* F, const void* X_rows, const int32_t* keys, const float* row_w,
+                    int rows, void* Y_rows, void* stream) {
+  if (!F || !X_rows || !keys || !Y_rows) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (rows < 0 || rows > F->d.max_rows) return fail(MOE_ERR_INVALID_ARGUMENT, "rows out of range");
+  if (rows == 0) return MOE_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int TD = F->d.token_dim, HD = F->d.hidden_dim;
+  int st = route_common(F->ctx, keys, rows, 1, F->d.num_experts, 0, F->counts.p, F->splits.p,
+                        F->order.p, F->pos.p, row_w ? row_w : F->ones.p, F->wpos.p, nullptr,
+                        nullptr, F->items.p, F->n_items.p, F->tile_n, nullptr, 0, s);
+  if (st) return st;
+  cudaError_t e = launch_gather_rows((const __nv_bfloat16*)X_rows, F->order.p, rows, 1, TD,
+                                     F->xp.p, s);
+  if (e != cudaSuccess) return cuda_fail(e, "gather launch");
+  GemmArgs g1{F->items.p, F->n_items.p, nullptr, HD, TD, kEpiReluBf16, F->h.p, nullptr, nullptr};
+  e = launch_grouped_gemm(F->tmW1, F->tmXp, g1, F->tile_n, F->ctx->sms, s);
+  if (e != cudaSuccess) return cuda_fail(e, "grouped gemm 1 launch");
+  GemmArgs g2{F->items.p, F->n_items.p, nullptr, TD, HD, kEpiScaleBf16, (__nv_bfloat16*)Y_rows,
+              F->wpos.p, F->order.p};
+  e = launch_grouped_gemm(F->tmW2, F->tmH, g2, F->tile_n, F->ctx->sms, s);
+  if (e != cudaSuccess) return cuda_fail(e, "grouped gemm 2 launch");
+  return MOE_OK;
 }
 
 int moe_layer_get_view(moe_layer* L, moe_layer_view* v) {

@@ -58,6 +58,7 @@ struct GemmArgs {
   int mode;                // EpilogueMode
   __nv_bfloat16* out;      // [rows, m_total]
   const float* wpos;       // kEpiScaleBf16: gate weight per row
+  const int32_t* out_rows; // optional row remap of the output (row r -> out_rows[r])
 };
 
 cudaError_t gemm_prepare();
@@ -82,6 +83,8 @@ cudaError_t launch_gather_rows(const __nv_bfloat16* X, const int32_t* order, int
                                int TD, __nv_bfloat16* Xp, cudaStream_t stream);
 cudaError_t launch_combine(const __nv_bfloat16* Yw, const int32_t* pos, int S, int k, int TD,
                            __nv_bfloat16* out, cudaStream_t stream);
+cudaError_t launch_fill_segments(const int32_t* counts, int n_segments, int mod, int32_t* out,
+                                 cudaStream_t stream);
 cudaError_t launch_fill_uniform_bf16(__nv_bfloat16* dst, int64_t n, uint64_t seed,
                                      uint64_t tensor_id, float scale, cudaStream_t stream);
 

@@ -99,6 +99,24 @@ __global__ void fill_uniform_bf16_kernel(__nv_bfloat16* dst, int64_t n, uint64_t
   }
 }
 
+// out[r] = (segment of r) % mod, segments laid out back to back with the
+// given lengths (one warp per segment).
+__global__ void fill_segments_kernel(const int32_t* __restrict__ counts, int n, int mod,
+                                     int32_t* __restrict__ out) {
+  // exclusive offsets recomputed per segment: n is small (D * E_local)
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int s = warp; s < n; s += nwarps) {
+    int off = 0;
+    for (int i = lane; i < s; i += 32) off += counts[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(0xffffffffu, off, o);
+    const int len = counts[s];
+    for (int r = lane; r < len; r += 32) out[off + r] = s % mod;
+  }
+}
+
 int grid_for(int64_t warps_needed, int sms) {
   const int64_t blocks = (warps_needed + 7) / 8;
   const int64_t cap = static_cast<int64_t>(sms) * 16;
@@ -130,6 +148,14 @@ cudaError_t launch_combine(const __nv_bfloat16* Yw, const int32_t* pos, int S, i
   if (S <= 0) return cudaSuccess;
   combine_kernel<<<grid_for(S, sm_count()), 256, 0, stream>>>(
       reinterpret_cast<const uint4*>(Yw), pos, S, k, TD / 8, reinterpret_cast<uint4*>(out));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_segments(const int32_t* counts, int n_segments, int mod, int32_t* out,
+                                 cudaStream_t stream) {
+  if (n_segments <= 0) return cudaSuccess;
+  fill_segments_kernel<<<grid_for(n_segments, sm_count()), 256, 0, stream>>>(counts, n_segments,
+                                                                             mod, out);
   return cudaGetLastError();
 }
 
