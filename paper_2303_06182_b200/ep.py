@@ -141,17 +141,19 @@ class KernelBackend:
         self.lib = ctx.lib
         self.shape = shape
         self.Wg = Wg
+        # the FFN's TMA descriptors hold raw pointers: keep the tensors alive
+        self.W1_local, self.W2_local = W1_local, W2_local
         E_l = W1_local.shape[0]
         d = _capi.FfnDesc(max_recv_rows, shape.token_dim, shape.hidden_dim, E_l, tile_n)
         h = C.c_void_p()
         check(self.lib.moe_ffn_create(ctx.h, C.byref(d), _p(W1_local), _p(W2_local), C.byref(h)))
-        self.ffn = h
+        self.ffn_h = h
         self.max_recv_rows = max_recv_rows
 
     def close(self):
-        if getattr(self, "ffn", None):
-            self.lib.moe_ffn_destroy(self.ffn)
-            self.ffn = None
+        if getattr(self, "ffn_h", None):
+            self.lib.moe_ffn_destroy(self.ffn_h)
+            self.ffn_h = None
 
     def gate(self, x, k, stream):
         S = x.shape[0]
@@ -195,7 +197,7 @@ class KernelBackend:
         if R:
             if R > self.max_recv_rows:
                 raise RuntimeError(f"received {R} rows > max_recv_rows {self.max_recv_rows}")
-            check(self.lib.moe_ffn_forward(self.ffn, _p(xr), _p(keys), _p(wr), R, _p(yr), _s(stream)))
+            check(self.lib.moe_ffn_forward(self.ffn_h, _p(xr), _p(keys), _p(wr), R, _p(yr), _s(stream)))
         return yr
 
     def combine(self, yb, pos, S, k, stream):

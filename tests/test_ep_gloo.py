@@ -25,6 +25,24 @@ from paper_2303_06182_b200.ep import ExpertParallelMoE, Placement, Transport
 SEED = 7
 
 
+def collect(procs, q, n, timeout):
+    """Results of n worker processes; fails fast if a worker dies."""
+    import queue
+    import time
+
+    out, t0 = [], time.time()
+    while len(out) < n:
+        try:
+            out.append(q.get(timeout=2))
+        except queue.Empty:
+            dead = [p for p in procs if p.exitcode not in (None, 0)]
+            if dead:
+                raise AssertionError(f"worker exited with code {dead[0].exitcode}")
+            if time.time() - t0 > timeout:
+                raise AssertionError("workers timed out")
+    return out
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -115,7 +133,7 @@ def test_expert_parallel_matches_single_process(placement_kind):
              for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=120) for _ in range(world)]
+    res = collect(procs, q, world, 120)
     for p in procs:
         p.join(60)
         assert p.exitcode == 0

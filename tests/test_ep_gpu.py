@@ -19,6 +19,24 @@ pytestmark = pytest.mark.gpu
 SEED = 2303061820
 
 
+def collect(procs, q, n, timeout):
+    """Results of n worker processes; fails fast if a worker dies."""
+    import queue
+    import time
+
+    out, t0 = [], time.time()
+    while len(out) < n:
+        try:
+            out.append(q.get(timeout=2))
+        except queue.Empty:
+            dead = [p for p in procs if p.exitcode not in (None, 0)]
+            if dead:
+                raise AssertionError(f"worker exited with code {dead[0].exitcode}")
+            if time.time() - t0 > timeout:
+                raise AssertionError("workers timed out")
+    return out
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -69,7 +87,7 @@ def test_expert_parallel_two_ranks_matches_single_gpu(S, TD, HD, E, k):
     procs = [ctx.Process(target=_worker, args=(r, world, port, S, TD, HD, E, k, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=600) for _ in range(world)]
+    res = collect(procs, q, world, 600)
     for p in procs:
         p.join(120)
         assert p.exitcode == 0
