@@ -230,6 +230,34 @@ int moe_ffn_destroy(moe_ffn* ffn);
 int moe_ffn_forward(moe_ffn* ffn, const void* X_rows, const int32_t* keys, const float* row_w,
                     int rows, void* Y_rows, void* stream);
 
+/* ---------------------------------------------------------------- expert cache */
+
+/* GPU-resident expert cache for a dynamic-gating layer:
+ * all experts' weights live in caller-owned pinned host memory (W1_host
+ * [E, HD, TD], W2_host [E, TD, HD] bf16); n_slots of them are resident on the
+ * GPU.  Per forward the active experts are visited in increasing id order with
+ * the reference's access_batch decisions (include/moesim/buffer.hpp:53-55,
+ * src/buffer.cpp:57-130; policy 0 = LIFO, 1 = FIFO); misses are copied with
+ * cudaMemcpyAsync on a side stream, in waves so that no slot is overwritten
+ * while its expert's FFN is pending.  One host sync per forward (the counts). */
+typedef struct moe_cache moe_cache;
+int moe_cache_create(moe_layer* layer, const void* W1_host, const void* W2_host, int n_slots,
+                     int policy, moe_cache** out);
+int moe_cache_destroy(moe_cache* cache);
+int moe_cache_forward(moe_cache* cache, const void* X, int S, void* out, void* stream);
+int moe_cache_forward_routed(moe_cache* cache, const void* X, const int32_t* idx, const float* w,
+                             int S, void* out, void* stream);
+/* totals5: accesses, hits, misses, evictions, bytes copied (cumulative);
+ * last5: accesses, hits, misses, evictions, waves of the last forward. */
+int moe_cache_stats(const moe_cache* cache, int64_t* totals5, int* last5);
+/* Resident experts, oldest first (CacheState::insertion_order). */
+int moe_cache_resident(const moe_cache* cache, int32_t* experts, int* n);
+
+/* Forward with caller-provided routing (idx [S,k] int32, w [S,k] fp32 on the
+ * device) instead of the gate: trace replay and skewed synthetic workloads. */
+int moe_layer_forward_routed(moe_layer* layer, const void* X, const int32_t* idx, const float* w,
+                             int S, void* out, void* stream);
+
 /* ---------------------------------------------------------------- EP */
 
 /* Dispatch by a relabelled key: key = key_map[expert] in [0, num_keys)

@@ -38,6 +38,26 @@ struct TokenTrace {
   int num_batches() const { return static_cast<int>(batches.size()); }
 };
 
+// Synthetic routing workload (reference trace.hpp:52-61): per batch, Zipf(skew)
+// popularity over a random subset of ceil(active_fraction * E) experts, kept
+// for the next batch with probability `persistence`; each token draws k
+// distinct experts proportionally to popularity.  Used here to drive skewed
+// routing into the GPU layer (expert-cache workloads, trace replay).
+struct SyntheticSpec {
+  int num_experts = 0;
+  int top_k = 1;
+  int num_batches = 1;
+  int seq_len = 1;
+  double zipf_skew = 0.0;
+  double persistence = 0.0;
+  double active_fraction = 1.0;
+  std::uint64_t seed = 0;
+};
+
+// Deterministic for a given spec; bit-identical to the reference generator
+// (same std::mt19937_64 stream, trace.cpp:174-259; tests/test_trace_gen.py).
+TokenTrace gen_synthetic_trace(const SyntheticSpec& spec);
+
 // Expert x batch load shares (each column sums to 1).
 struct LoadMatrix {
   Eigen::MatrixXd share;

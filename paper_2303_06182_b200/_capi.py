@@ -32,7 +32,8 @@ EXPORTED = [
     "moe_layer_forward_host", "moe_layer_get_view", "moe_layer_set_weight_pool",
     "moe_exchange_counts_host", "moe_layer_enable_timing", "moe_layer_stage_times",
     "moe_ffn_create", "moe_ffn_destroy", "moe_ffn_forward", "moe_route_dynamic_keyed",
-    "moe_fill_segments",
+    "moe_fill_segments", "moe_cache_create", "moe_cache_destroy", "moe_cache_forward",
+    "moe_cache_forward_routed", "moe_cache_stats", "moe_cache_resident", "moe_layer_forward_routed",
 ]
 
 
@@ -121,6 +122,13 @@ def load(path: str = LIB_PATH):
     _sig(lib.moe_ffn_forward, I, P, P, P, P, I, P, P)
     _sig(lib.moe_route_dynamic_keyed, I, P, P, I, I, I, P, I, P, P, P, P, P, P, P)
     _sig(lib.moe_fill_segments, I, P, P, I, I, P, P)
+    _sig(lib.moe_cache_create, I, P, P, P, I, I, C.POINTER(P))
+    _sig(lib.moe_cache_destroy, I, P)
+    _sig(lib.moe_cache_forward, I, P, P, I, P, P)
+    _sig(lib.moe_cache_forward_routed, I, P, P, P, P, I, P, P)
+    _sig(lib.moe_cache_stats, I, P, P, P)
+    _sig(lib.moe_cache_resident, I, P, P, P)
+    _sig(lib.moe_layer_forward_routed, I, P, P, P, P, I, P, P)
     _lib = lib
     return lib
 

@@ -1,0 +1,274 @@
+// Expert buffering: a GPU-resident cache of expert weights
+// backed by pinned host memory, filled with cudaMemcpyAsync on a side stream.
+//
+// Decisions follow the reference's access_batch exactly
+// (proj/src/buffer.cpp:57-130, LIFO / FIFO): the batch's active experts are
+// visited serially in increasing id order; a miss inserts the expert, and when
+// the cache is full it first evicts the most recently inserted resident that
+// is inactive in this batch, otherwise the newest (LIFO) / oldest (FIFO).
+//
+// On the GPU the experts of a batch run concurrently, so the serial semantics
+// need one extra rule: a resident whose FFN is scheduled in the current wave
+// must not be overwritten before that wave finishes.  The batch is therefore
+// split into waves (contiguous expert-id ranges, hence contiguous rows and
+// FFN items): a wave closes right before a miss would evict one of its own
+// experts.  Per wave:
+//   copy stream:    wait(previous wave's FFN) -> H2D copies of its misses
+//   compute stream: wait(its copies) -> slot table H2D -> GEMM1/GEMM2 over
+//                   the items of its expert range
+// The routing counts reach the host once per layer call (the host sync the
+// cache needs to know the active set, shared with the EP count exchange in
+// the paper's design).
+#include <algorithm>
+
+#include "capi_state.h"
+
+struct moe_cache {
+  moe_layer* L = nullptr;
+  int n_slots = 0;
+  int policy = 0;  // 0 LIFO, 1 FIFO (buffer.hpp:16 CachePolicy order)
+  const uint8_t* w1h = nullptr;
+  const uint8_t* w2h = nullptr;
+  size_t w1_bytes = 0, w2_bytes = 0;
+  DevBuf<__nv_bfloat16> pool1, pool2;
+  DevBuf<int32_t> slot_dev;
+  std::vector<int32_t*> slot_host;  // pinned staging, one table per wave
+  int32_t* counts_host = nullptr;   // pinned [E]
+  std::vector<int> order;           // residents, oldest first (CacheState::insertion_order)
+  std::vector<int> slot_of;         // expert -> slot or -1
+  std::vector<int> free_slots;
+  int64_t accesses = 0, hits = 0, misses = 0, evictions = 0, copies_bytes = 0;
+  int last_stats[5] = {0, 0, 0, 0, 0};  // accesses, hits, misses, evictions, waves
+  std::vector<int> last_active;
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> ev_copy, ev_ffn;
+};
+
+namespace {
+
+struct Wave {
+  int e_lo, e_hi;                              // expert id range [e_lo, e_hi]
+  std::vector<std::pair<int, int>> loads;      // (expert, slot) to copy before the wave
+  std::vector<std::pair<int, int>> table;      // (expert, slot) of every wave expert
+};
+
+int ensure_events(moe_cache* C, size_t n) {
+  while (C->ev_copy.size() < n) {
+    cudaEvent_t a, b;
+    MOE_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    MOE_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    C->ev_copy.push_back(a);
+    C->ev_ffn.push_back(b);
+  }
+  const int E = C->L->d.num_experts;
+  while (C->slot_host.size() < n) {
+    int32_t* p = nullptr;
+    MOE_CUDA(cudaMallocHost(&p, sizeof(int32_t) * E));
+    C->slot_host.push_back(p);
+  }
+  return MOE_OK;
+}
+
+// access_batch (buffer.cpp:57-130) over `active` (sorted, unique), emitting
+// the GPU schedule.  Returns the waves.
+std::vector<Wave> plan_batch(moe_cache* C, const std::vector<int>& active, int* stats) {
+  std::vector<Wave> waves;
+  Wave cur;
+  cur.e_lo = -1;
+  std::vector<char> in_wave(C->slot_of.size(), 0);
+  std::vector<char> is_active(C->slot_of.size(), 0);
+  for (int x : active) is_active[x] = 1;
+  auto close_wave = [&]() {
+    if (cur.e_lo >= 0) {
+      for (auto& es : cur.table) in_wave[es.first] = 0;
+      waves.push_back(std::move(cur));
+    }
+    cur = Wave();
+    cur.e_lo = -1;
+  };
+  for (int x : active) {
+    ++stats[0];
+    const bool resident = C->slot_of[x] >= 0;
+    if (resident) {
+      ++stats[1];
+    } else {
+      ++stats[2];
+      int slot;
+      if ((int)C->order.size() == C->n_slots) {
+        int victim = -1;
+        for (auto it = C->order.rbegin(); it != C->order.rend(); ++it)
+          if (!is_active[*it]) {
+            victim = *it;
+            break;
+          }
+        if (victim < 0) victim = C->policy == 0 ? C->order.back() : C->order.front();
+        // the victim's weights are still needed by the current wave: close it
+        if (in_wave[victim]) close_wave();
+        C->order.erase(std::find(C->order.begin(), C->order.end(), victim));
+        slot = C->slot_of[victim];
+        C->slot_of[victim] = -1;
+        ++stats[3];
+      } else {
+        slot = C->free_slots.back();
+        C->free_slots.pop_back();
+      }
+      C->order.push_back(x);
+      C->slot_of[x] = slot;
+      if (cur.e_lo < 0) cur.e_lo = x;
+      cur.loads.emplace_back(x, slot);
+    }
+    if (cur.e_lo < 0) cur.e_lo = x;
+    cur.e_hi = x;
+    cur.table.emplace_back(x, C->slot_of[x]);
+    in_wave[x] = 1;
+  }
+  close_wave();
+  return waves;
+}
+
+int cache_forward(moe_cache* C, const void* X, int S, const int32_t* idx, const float* w, void* out,
+                  cudaStream_t s) {
+  moe_layer* L = C->L;
+  const int E = L->d.num_experts;
+  int st = layer_front(L, X, S, idx, w, s, nullptr);
+  if (st) return st;
+  // the one host sync: which experts are active in this batch
+  MOE_CUDA(cudaMemcpyAsync(C->counts_host, L->counts.p, sizeof(int32_t) * E,
+                           cudaMemcpyDeviceToHost, s));
+  MOE_CUDA(cudaStreamSynchronize(s));
+  std::vector<int> active;
+  for (int e = 0; e < E; ++e)
+    if (C->counts_host[e] > 0) active.push_back(e);
+  int stats[4] = {0, 0, 0, 0};
+  const std::vector<Wave> waves = plan_batch(C, active, stats);
+  if ((st = ensure_events(C, waves.size()))) return st;
+  for (size_t wv = 0; wv < waves.size(); ++wv) {
+    const Wave& W = waves[wv];
+    // copies: after the previous wave's FFN (its slots may be overwritten)
+    if (wv > 0) MOE_CUDA(cudaStreamWaitEvent(C->copy_stream, C->ev_ffn[wv - 1], 0));
+    for (auto& es : W.loads) {
+      const size_t e = (size_t)es.first, slot = (size_t)es.second;
+      MOE_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(C->pool1.p) + slot * C->w1_bytes,
+                               C->w1h + e * C->w1_bytes, C->w1_bytes, cudaMemcpyHostToDevice,
+                               C->copy_stream));
+      MOE_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(C->pool2.p) + slot * C->w2_bytes,
+                               C->w2h + e * C->w2_bytes, C->w2_bytes, cudaMemcpyHostToDevice,
+                               C->copy_stream));
+      C->copies_bytes += (int64_t)(C->w1_bytes + C->w2_bytes);
+    }
+    MOE_CUDA(cudaEventRecord(C->ev_copy[wv], C->copy_stream));
+    // compute: the wave's slot table, then its experts' FFN items
+    int32_t* tab = C->slot_host[wv];
+    for (auto& es : W.table) tab[es.first] = es.second;
+    MOE_CUDA(cudaStreamWaitEvent(s, C->ev_copy[wv], 0));
+    MOE_CUDA(cudaMemcpyAsync(C->slot_dev.p + W.e_lo, tab + W.e_lo,
+                             sizeof(int32_t) * (W.e_hi - W.e_lo + 1), cudaMemcpyHostToDevice, s));
+    if ((st = layer_ffn(L, s, W.e_lo, W.e_hi + 1, nullptr))) return st;
+    MOE_CUDA(cudaEventRecord(C->ev_ffn[wv], s));
+  }
+  C->accesses += stats[0];
+  C->hits += stats[1];
+  C->misses += stats[2];
+  C->evictions += stats[3];
+  for (int i = 0; i < 4; ++i) C->last_stats[i] = stats[i];
+  C->last_stats[4] = (int)waves.size();
+  C->last_active = active;
+  return layer_back(L, S, out, s, nullptr);
+}
+
+}  // namespace
+
+extern "C" {
+
+int moe_cache_create(moe_layer* L, const void* W1_host, const void* W2_host, int n_slots,
+                     int policy, moe_cache** out) {
+  if (!L || !W1_host || !W2_host || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (n_slots < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "cache_size must be >= 1");
+  if (policy != 0 && policy != 1)
+    return fail(MOE_ERR_UNSUPPORTED, "the GPU cache implements LIFO (0) and FIFO (1)");
+  if (L->d.mode != MOE_GATING_DYNAMIC)
+    return fail(MOE_ERR_UNSUPPORTED, "expert buffering is implemented for dynamic gating");
+  MOE_CUDA(cudaSetDevice(L->ctx->device));
+  auto* C = new moe_cache();
+  C->L = L;
+  C->n_slots = std::min(n_slots, L->d.num_experts);
+  C->policy = policy;
+  C->w1h = static_cast<const uint8_t*>(W1_host);
+  C->w2h = static_cast<const uint8_t*>(W2_host);
+  const size_t TD = L->d.token_dim, HD = L->d.hidden_dim, E = L->d.num_experts;
+  C->w1_bytes = HD * TD * 2;
+  C->w2_bytes = TD * HD * 2;
+  int st;
+  if ((st = C->pool1.reserve((size_t)C->n_slots * HD * TD)) ||
+      (st = C->pool2.reserve((size_t)C->n_slots * TD * HD)) || (st = C->slot_dev.reserve(E))) {
+    moe_cache_destroy(C);
+    return st;
+  }
+  cudaMemset(C->slot_dev.p, 0, sizeof(int32_t) * E);
+  if (cudaMallocHost(&C->counts_host, sizeof(int32_t) * E) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&C->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    moe_cache_destroy(C);
+    return fail(MOE_ERR_CUDA, "cache host buffers / stream");
+  }
+  C->slot_of.assign(E, -1);
+  for (int i = C->n_slots - 1; i >= 0; --i) C->free_slots.push_back(i);
+  if ((st = moe_layer_set_weight_pool(L, C->pool1.p, C->pool2.p, C->n_slots, C->slot_dev.p))) {
+    moe_cache_destroy(C);
+    return st;
+  }
+  *out = C;
+  return MOE_OK;
+}
+
+int moe_cache_destroy(moe_cache* C) {
+  if (!C) return MOE_OK;
+  if (C->L) moe_layer_set_weight_pool(C->L, nullptr, nullptr, 0, nullptr);
+  if (C->copy_stream) {
+    cudaStreamSynchronize(C->copy_stream);
+    cudaStreamDestroy(C->copy_stream);
+  }
+  for (auto e : C->ev_copy) cudaEventDestroy(e);
+  for (auto e : C->ev_ffn) cudaEventDestroy(e);
+  for (auto p : C->slot_host) cudaFreeHost(p);
+  if (C->counts_host) cudaFreeHost(C->counts_host);
+  C->pool1.release();
+  C->pool2.release();
+  C->slot_dev.release();
+  delete C;
+  return MOE_OK;
+}
+
+int moe_cache_forward(moe_cache* C, const void* X, int S, void* out, void* stream) {
+  if (!C || !X || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  return cache_forward(C, X, S, nullptr, nullptr, out, (cudaStream_t)stream);
+}
+
+int moe_cache_forward_routed(moe_cache* C, const void* X, const int32_t* idx, const float* w, int S,
+                             void* out, void* stream) {
+  if (!C || !X || !idx || !w || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  return cache_forward(C, X, S, idx, w, out, (cudaStream_t)stream);
+}
+
+int moe_cache_stats(const moe_cache* C, int64_t* totals5, int* last5) {
+  if (!C) return fail(MOE_ERR_INVALID_ARGUMENT, "null cache");
+  if (totals5) {
+    totals5[0] = C->accesses;
+    totals5[1] = C->hits;
+    totals5[2] = C->misses;
+    totals5[3] = C->evictions;
+    totals5[4] = C->copies_bytes;
+  }
+  if (last5)
+    for (int i = 0; i < 5; ++i) last5[i] = C->last_stats[i];
+  return MOE_OK;
+}
+
+int moe_cache_resident(const moe_cache* C, int32_t* experts, int* n) {
+  if (!C || !n) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  *n = (int)C->order.size();
+  if (experts)
+    for (size_t i = 0; i < C->order.size(); ++i) experts[i] = C->order[i];
+  return MOE_OK;
+}
+
+}  // extern "C"

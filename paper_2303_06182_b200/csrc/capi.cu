@@ -1,110 +1,11 @@
 // C-ABI implementation: contexts, argument checking (reference error text),
 // host-buffer drop-in entry points, TMA descriptor setup and the MoE layer
 // (gate -> route -> gather -> grouped FFN x2 -> combine) with its workspace.
-#include <cudaTypedefs.h>
-
-#include <cmath>
-#include <cstdio>
-#include <cstring>
 #include <mutex>
-#include <string>
-#include <vector>
 
-#include "../../include/moe_capi.h"
-#include "moe_internal.h"
-
-namespace moe {
-int gate_box_rows(int E);
-}
-
-using namespace moe;
+#include "capi_state.h"
 
 namespace {
-
-thread_local std::string g_last_error;
-
-int fail(int status, const std::string& msg) {
-  g_last_error = msg;
-  return status;
-}
-
-int cuda_fail(cudaError_t e, const char* what) {
-  return fail(MOE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-#define MOE_CUDA(call)                                         \
-  do {                                                         \
-    cudaError_t _e = (call);                                   \
-    if (_e != cudaSuccess) return cuda_fail(_e, #call);        \
-  } while (0)
-
-PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
-
-int get_encoder() {
-  if (g_encode) return MOE_OK;
-  void* fn = nullptr;
-  cudaDriverEntryPointQueryResult q;
-  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
-  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
-    return fail(MOE_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
-  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  return MOE_OK;
-}
-
-// Row-major bf16 matrix [rows, cols] viewed by TMA in boxes of 64 x box_rows
-// with the 128-byte swizzle the UMMA descriptors expect.
-int encode_bf16(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
-  int st = get_encoder();
-  if (st) return st;
-  cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {64, box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
-                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    char buf[160];
-    snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d) rows=%llu cols=%llu box=%u",
-             (int)r, (unsigned long long)rows, (unsigned long long)cols, box_rows);
-    return fail(MOE_ERR_CUDA, buf);
-  }
-  return MOE_OK;
-}
-
-// Reference check_batch (gating.cpp:12-18), verbatim messages.
-int check_batch(int S, int k, int E) {
-  if (E < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "num_experts must be positive");
-  if (k < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "top_k must be positive");
-  if (k > E) return fail(MOE_ERR_INVALID_ARGUMENT, "top_k exceeds num_experts");
-  if (S < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "empty batch");
-  return MOE_OK;
-}
-
-template <class T>
-struct DevBuf {
-  T* p = nullptr;
-  size_t n = 0;
-  int reserve(size_t count) {
-    if (count <= n) return MOE_OK;
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-    cudaError_t e = cudaMalloc(&p, count * sizeof(T) + 16);
-    if (e != cudaSuccess) {
-      p = nullptr;
-      return fail(MOE_ERR_OUT_OF_MEMORY, std::string("cudaMalloc: ") + cudaGetErrorString(e));
-    }
-    n = count;
-    return MOE_OK;
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-  }
-};
 
 __global__ void inverse_order_kernel(const int32_t* order, int64_t n, int32_t* pos) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
@@ -130,78 +31,6 @@ __global__ void exchange_counts_kernel(const int32_t* experts, int S, int k, int
 }
 
 }  // namespace
-
-struct moe_ctx {
-  int device = 0;
-  int sms = 0;
-  int route_max_blocks = 0;
-  int route_prepared_E = -1;
-  DevBuf<int32_t> block_hist, err_flag, drop_mark;
-  cudaStream_t scratch_stream = nullptr;
-
-  int prepare_route(int E) {
-    if (E > route_prepared_E) {
-      int mb = 0;
-      cudaError_t e = route_prepare(E, &mb);
-      if (e != cudaSuccess) return cuda_fail(e, "route_prepare");
-      route_max_blocks = mb;
-      route_prepared_E = E;
-    }
-    int st = block_hist.reserve((size_t)E * (route_max_blocks + 4) + route_max_blocks);
-    if (st) return st;
-    if (!err_flag.p) {
-      st = err_flag.reserve(1);
-      if (st) return st;
-      cudaError_t e = cudaMemset(err_flag.p, 0, sizeof(int32_t));
-      if (e != cudaSuccess) return cuda_fail(e, "clear error flag");
-    }
-    return MOE_OK;
-  }
-};
-
-struct moe_layer {
-  moe_ctx* ctx = nullptr;
-  moe_layer_desc d{};
-  const void* Wg = nullptr;
-  const void* W1 = nullptr;
-  const void* W2 = nullptr;
-  int tile_n = 128;
-  int rows_max = 0;
-  int items_max = 0;
-  CUtensorMap tmWg, tmW1, tmW2, tmXp, tmH;
-  CUtensorMap tmX;
-  const void* tmX_ptr = nullptr;
-  int tmX_rows = 0;
-  // optional expert-cache weight pool
-  const int32_t* slot_of = nullptr;
-  DevBuf<int32_t> idx, pos, counts, splits, order, dropped, n_dropped, n_items, err;
-  DevBuf<float> w, wpos, logits;
-  DevBuf<FfnItem> items;
-  DevBuf<__nv_bfloat16> xp, h, yw, xin, yout;
-  int last_rows = 0;
-  int last_cap = 0;
-  // per-stage timing ring (eager path)
-  std::vector<cudaEvent_t> tev;
-  int t_slots = 0;
-  long t_calls = 0;
-  // graph cache
-  cudaGraphExec_t gexec = nullptr;
-  const void* g_x = nullptr;
-  void* g_out = nullptr;
-  int g_S = -1;
-  cudaStream_t g_stream = nullptr;
-};
-
-struct moe_ffn {
-  moe_ctx* ctx = nullptr;
-  moe_ffn_desc d{};
-  int tile_n = 128;
-  CUtensorMap tmW1, tmW2, tmXp, tmH;
-  DevBuf<int32_t> counts, splits, order, pos, n_items;
-  DevBuf<float> wpos, ones;
-  DevBuf<FfnItem> items;
-  DevBuf<__nv_bfloat16> xp, h;
-};
 
 extern "C" {
 
@@ -270,11 +99,12 @@ int moe_expert_capacity(double capacity_factor, int seq_len) {
   return static_cast<int>(std::ceil(raw));
 }
 
-static int route_common(moe_ctx* ctx, const int32_t* expert_idx, int S, int k, int E, int cap,
+extern "C++" {
+int moe::capi::route_common(moe_ctx* ctx, const int32_t* expert_idx, int S, int k, int E, int cap,
                         int32_t* counts, int32_t* splits, int32_t* order, int32_t* pos,
                         const float* gate_w, float* wpos, int32_t* dropped, int32_t* n_dropped,
                         FfnItem* items, int32_t* n_items, int tile_n, const int32_t* key_map,
-                        int num_keys_in, cudaStream_t stream) {
+                        int num_keys_in, cudaStream_t stream, int32_t* item_off) {
   int st = ctx->prepare_route(E);
   if (st) return st;
   if (cap > 0) {
@@ -302,11 +132,13 @@ static int route_common(moe_ctx* ctx, const int32_t* expert_idx, int S, int k, i
   a.block_hist = ctx->block_hist.p;
   a.items = items;
   a.n_items = n_items;
+  a.item_off = item_off;
   a.error_flag = ctx->err_flag.p;
   cudaError_t e = launch_route(a, ctx->route_max_blocks, stream);
   if (e != cudaSuccess) return cuda_fail(e, "route kernel launch");
   return MOE_OK;
 }
+}  // extern "C++"
 
 int moe_route_dynamic(moe_ctx* ctx, const int32_t* expert_idx, int S, int k, int E,
                       int32_t* counts, int32_t* splits, int32_t* order, int32_t* pos,
@@ -587,6 +419,7 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
       (st = L->splits.reserve(E + 1)) || (st = L->order.reserve(R)) ||
       (st = L->wpos.reserve(R)) || (st = L->items.reserve(L->items_max)) ||
       (st = L->n_items.reserve(1)) || (st = L->err.reserve(1)) ||
+      (st = L->item_off.reserve((size_t)E + 1)) ||
       (st = L->xp.reserve(Rp * TD)) || (st = L->h.reserve(Rp * HD)) ||
       (st = L->yw.reserve(R * TD))) {
     moe_layer_destroy(L);
@@ -638,6 +471,7 @@ int moe_layer_destroy(moe_layer* L) {
   L->items.release();
   L->n_items.release();
   L->err.release();
+  L->item_off.release();
   L->dropped.release();
   L->n_dropped.release();
   L->logits.release();
@@ -650,31 +484,33 @@ int moe_layer_destroy(moe_layer* L) {
   return MOE_OK;
 }
 
-static int layer_forward_impl(moe_layer* L, const void* X, int S, void* out, cudaStream_t s,
-                              bool timed = false) {
+// Front of the layer: gate (or caller-provided routing), dispatch, gather.
+// idx_in/w_in non-null = routed forward (trace replay, skewed workloads).
+extern "C++" {
+int moe::capi::layer_front(moe_layer* L, const void* X, int S, const int32_t* idx_in,
+                       const float* w_in, cudaStream_t s, cudaEvent_t* ev) {
   const moe_layer_desc& d = L->d;
-  cudaEvent_t* ev = nullptr;
-  if (timed && L->t_slots > 0) {
-    ev = &L->tev[(size_t)(L->t_calls % L->t_slots) * (MOE_NUM_STAGES + 1)];
-    ++L->t_calls;
-  }
   auto mark = [&](int i) {
     if (ev) cudaEventRecord(ev[i], s);
   };
   if (S < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "empty batch");
   if (S > d.max_tokens) return fail(MOE_ERR_INVALID_ARGUMENT, "S exceeds max_tokens");
-  const int k = d.top_k, E = d.num_experts, TD = d.token_dim, HD = d.hidden_dim;
+  const int k = d.top_k, E = d.num_experts, TD = d.token_dim;
   int st;
-  if (X != L->tmX_ptr || S != L->tmX_rows) {
-    if ((st = encode_bf16(&L->tmX, X, (uint64_t)S, TD, 128))) return st;
-    L->tmX_ptr = X;
-    L->tmX_rows = S;
-  }
+  const int32_t* idx = idx_in ? idx_in : L->idx.p;
+  const float* w = idx_in ? w_in : L->w.p;
   // 1. gate
   mark(0);
-  GateArgs ga{S, TD, E, k, L->idx.p, L->w.p, d.keep_logits ? L->logits.p : nullptr};
-  cudaError_t e = launch_gate(L->tmX, L->tmWg, ga, s);
-  if (e != cudaSuccess) return cuda_fail(e, "gate launch");
+  if (!idx_in) {
+    if (X != L->tmX_ptr || S != L->tmX_rows) {
+      if ((st = encode_bf16(&L->tmX, X, (uint64_t)S, TD, 128))) return st;
+      L->tmX_ptr = X;
+      L->tmX_rows = S;
+    }
+    GateArgs ga{S, TD, E, k, L->idx.p, L->w.p, d.keep_logits ? L->logits.p : nullptr};
+    cudaError_t e = launch_gate(L->tmX, L->tmWg, ga, s);
+    if (e != cudaSuccess) return cuda_fail(e, "gate launch");
+  }
   // 2. route
   int cap = 0, rows = S * k;
   if (d.mode == MOE_GATING_STATIC) {
@@ -684,29 +520,74 @@ static int layer_forward_impl(moe_layer* L, const void* X, int S, void* out, cud
   L->last_rows = rows;
   L->last_cap = cap;
   mark(1);
-  st = route_common(L->ctx, L->idx.p, S, k, E, cap, L->counts.p, L->splits.p, L->order.p,
-                    L->pos.p, L->w.p, L->wpos.p, L->dropped.p, L->n_dropped.p, L->items.p,
-                    L->n_items.p, L->tile_n, nullptr, 0, s);
+  st = route_common(L->ctx, idx, S, k, E, cap, L->counts.p, L->splits.p, L->order.p, L->pos.p, w,
+                    L->wpos.p, L->dropped.p, L->n_dropped.p, L->items.p, L->n_items.p, L->tile_n,
+                    nullptr, 0, s, L->item_off.p);
   if (st) return st;
   // 3. gather token rows into expert-grouped order
   mark(2);
-  e = launch_gather_rows((const __nv_bfloat16*)X, L->order.p, rows, k, TD, L->xp.p, s);
+  cudaError_t e = launch_gather_rows((const __nv_bfloat16*)X, L->order.p, rows, k, TD, L->xp.p, s);
   if (e != cudaSuccess) return cuda_fail(e, "gather launch");
-  // 4. grouped FFN
+  return MOE_OK;
+}
+}  // extern "C++"
+
+// Grouped FFN over the items of experts [e_lo, e_hi) (all items if e_lo < 0).
+extern "C++" {
+int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaEvent_t* ev) {
+  const int TD = L->d.token_dim, HD = L->d.hidden_dim;
+  auto mark = [&](int i) {
+    if (ev) cudaEventRecord(ev[i], s);
+  };
+  const int32_t* off = e_lo >= 0 ? L->item_off.p : nullptr;
   mark(3);
-  GemmArgs g1{L->items.p, L->n_items.p, L->slot_of, HD, TD, kEpiReluBf16, L->h.p, nullptr, nullptr};
-  e = launch_grouped_gemm(L->tmW1, L->tmXp, g1, L->tile_n, L->ctx->sms, s);
+  GemmArgs g1{L->items.p, L->n_items.p, L->slot_of, HD, TD, kEpiReluBf16, L->h.p, nullptr, nullptr,
+              off, e_lo, e_hi};
+  cudaError_t e = launch_grouped_gemm(L->tmW1, L->tmXp, g1, L->tile_n, L->ctx->sms, s);
   if (e != cudaSuccess) return cuda_fail(e, "grouped gemm 1 launch");
   mark(4);
-  GemmArgs g2{L->items.p, L->n_items.p, L->slot_of, TD, HD, kEpiScaleBf16, L->yw.p, L->wpos.p, nullptr};
+  GemmArgs g2{L->items.p, L->n_items.p, L->slot_of, TD, HD, kEpiScaleBf16, L->yw.p, L->wpos.p,
+              nullptr, off, e_lo, e_hi};
   e = launch_grouped_gemm(L->tmW2, L->tmH, g2, L->tile_n, L->ctx->sms, s);
   if (e != cudaSuccess) return cuda_fail(e, "grouped gemm 2 launch");
-  // 5. combine
+  return MOE_OK;
+}
+}  // extern "C++"
+
+extern "C++" {
+int moe::capi::layer_back(moe_layer* L, int S, void* out, cudaStream_t s, cudaEvent_t* ev) {
+  auto mark = [&](int i) {
+    if (ev) cudaEventRecord(ev[i], s);
+  };
   mark(5);
-  e = launch_combine(L->yw.p, L->pos.p, S, k, TD, (__nv_bfloat16*)out, s);
+  cudaError_t e = launch_combine(L->yw.p, L->pos.p, S, L->d.top_k, L->d.token_dim,
+                                 (__nv_bfloat16*)out, s);
   if (e != cudaSuccess) return cuda_fail(e, "combine launch");
   mark(6);
   return MOE_OK;
+}
+}  // extern "C++"
+
+extern "C++" {
+static int layer_forward_impl(moe_layer* L, const void* X, int S, void* out, cudaStream_t s,
+                              bool timed = false, const int32_t* idx_in = nullptr,
+                              const float* w_in = nullptr) {
+  cudaEvent_t* ev = nullptr;
+  if (timed && L->t_slots > 0) {
+    ev = &L->tev[(size_t)(L->t_calls % L->t_slots) * (MOE_NUM_STAGES + 1)];
+    ++L->t_calls;
+  }
+  int st;
+  if ((st = layer_front(L, X, S, idx_in, w_in, s, ev))) return st;
+  if ((st = layer_ffn(L, s, -1, -1, ev))) return st;
+  return layer_back(L, S, out, s, ev);
+}
+}  // extern "C++"
+
+int moe_layer_forward_routed(moe_layer* L, const void* X, const int32_t* idx, const float* w, int S,
+                             void* out, void* stream) {
+  if (!L || !X || !out || !idx || !w) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  return layer_forward_impl(L, X, S, out, (cudaStream_t)stream, true, idx, w);
 }
 
 int moe_layer_forward(moe_layer* L, const void* X, int S, void* out, void* stream) {

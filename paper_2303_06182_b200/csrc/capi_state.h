@@ -1,0 +1,199 @@
+// Internal state of the C ABI: context / layer / FFN objects, device-buffer
+// helper, error reporting and TMA descriptor encoding.  Shared by capi.cu
+// (routing, layer, FFN entry points) and cache.cu (expert cache).
+#pragma once
+
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/moe_capi.h"
+#include "moe_internal.h"
+
+namespace moe {
+int gate_box_rows(int E);
+
+namespace capi {
+
+inline thread_local std::string g_last_error;
+
+inline int fail(int status, const std::string& msg) {
+  g_last_error = msg;
+  return status;
+}
+
+inline int cuda_fail(cudaError_t e, const char* what) {
+  return fail(MOE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define MOE_CUDA(call)                                         \
+  do {                                                         \
+    cudaError_t _e = (call);                                   \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);        \
+  } while (0)
+
+inline PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+inline int get_encoder() {
+  if (g_encode) return MOE_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+    return fail(MOE_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return MOE_OK;
+}
+
+// Row-major bf16 matrix [rows, cols] viewed by TMA in boxes of 64 x box_rows
+// with the 128-byte swizzle the UMMA descriptors expect.
+inline int encode_bf16(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  int st = get_encoder();
+  if (st) return st;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d) rows=%llu cols=%llu box=%u",
+             (int)r, (unsigned long long)rows, (unsigned long long)cols, box_rows);
+    return fail(MOE_ERR_CUDA, buf);
+  }
+  return MOE_OK;
+}
+
+// Reference check_batch (gating.cpp:12-18), verbatim messages.
+inline int check_batch(int S, int k, int E) {
+  if (E < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "num_experts must be positive");
+  if (k < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "top_k must be positive");
+  if (k > E) return fail(MOE_ERR_INVALID_ARGUMENT, "top_k exceeds num_experts");
+  if (S < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "empty batch");
+  return MOE_OK;
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  int reserve(size_t count) {
+    if (count <= n) return MOE_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T) + 16);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      return fail(MOE_ERR_OUT_OF_MEMORY, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    n = count;
+    return MOE_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+
+}  // namespace capi
+}  // namespace moe
+
+using namespace moe;
+using namespace moe::capi;
+
+struct moe_ctx {
+  int device = 0;
+  int sms = 0;
+  int route_max_blocks = 0;
+  int route_prepared_E = -1;
+  DevBuf<int32_t> block_hist, err_flag, drop_mark;
+  cudaStream_t scratch_stream = nullptr;
+
+  int prepare_route(int E) {
+    if (E > route_prepared_E) {
+      int mb = 0;
+      cudaError_t e = route_prepare(E, &mb);
+      if (e != cudaSuccess) return cuda_fail(e, "route_prepare");
+      route_max_blocks = mb;
+      route_prepared_E = E;
+    }
+    int st = block_hist.reserve((size_t)E * (route_max_blocks + 4) + route_max_blocks);
+    if (st) return st;
+    if (!err_flag.p) {
+      st = err_flag.reserve(1);
+      if (st) return st;
+      cudaError_t e = cudaMemset(err_flag.p, 0, sizeof(int32_t));
+      if (e != cudaSuccess) return cuda_fail(e, "clear error flag");
+    }
+    return MOE_OK;
+  }
+};
+
+struct moe_layer {
+  moe_ctx* ctx = nullptr;
+  moe_layer_desc d{};
+  const void* Wg = nullptr;
+  const void* W1 = nullptr;
+  const void* W2 = nullptr;
+  int tile_n = 128;
+  int rows_max = 0;
+  int items_max = 0;
+  CUtensorMap tmWg, tmW1, tmW2, tmXp, tmH;
+  CUtensorMap tmX;
+  const void* tmX_ptr = nullptr;
+  int tmX_rows = 0;
+  // optional expert-cache weight pool
+  const int32_t* slot_of = nullptr;
+  DevBuf<int32_t> idx, pos, counts, splits, order, dropped, n_dropped, n_items, err, item_off;
+  DevBuf<float> w, wpos, logits;
+  DevBuf<FfnItem> items;
+  DevBuf<__nv_bfloat16> xp, h, yw, xin, yout;
+  int last_rows = 0;
+  int last_cap = 0;
+  // per-stage timing ring (eager path)
+  std::vector<cudaEvent_t> tev;
+  int t_slots = 0;
+  long t_calls = 0;
+  // graph cache
+  cudaGraphExec_t gexec = nullptr;
+  const void* g_x = nullptr;
+  void* g_out = nullptr;
+  int g_S = -1;
+  cudaStream_t g_stream = nullptr;
+};
+
+struct moe_ffn {
+  moe_ctx* ctx = nullptr;
+  moe_ffn_desc d{};
+  int tile_n = 128;
+  CUtensorMap tmW1, tmW2, tmXp, tmH;
+  DevBuf<int32_t> counts, splits, order, pos, n_items;
+  DevBuf<float> wpos, ones;
+  DevBuf<FfnItem> items;
+  DevBuf<__nv_bfloat16> xp, h;
+};
+
+
+namespace moe {
+namespace capi {
+int route_common(moe_ctx* ctx, const int32_t* expert_idx, int S, int k, int E, int cap,
+                 int32_t* counts, int32_t* splits, int32_t* order, int32_t* pos,
+                 const float* gate_w, float* wpos, int32_t* dropped, int32_t* n_dropped,
+                 FfnItem* items, int32_t* n_items, int tile_n, const int32_t* key_map,
+                 int num_keys_in, cudaStream_t stream, int32_t* item_off = nullptr);
+int layer_front(moe_layer* L, const void* X, int S, const int32_t* idx_in, const float* w_in,
+                cudaStream_t s, cudaEvent_t* ev);
+int layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaEvent_t* ev);
+int layer_back(moe_layer* L, int S, void* out, cudaStream_t s, cudaEvent_t* ev);
+}  // namespace capi
+}  // namespace moe

@@ -79,7 +79,10 @@ __global__ void __launch_bounds__(256, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int n_items = *g.n_items;
+  // optional expert range (expert-cache waves): items of experts [e_lo, e_hi)
+  const int item0 = g.item_off ? g.item_off[g.e_lo] : 0;
+  const int n_items = g.item_off ? g.item_off[g.e_hi] - item0 : *g.n_items;
+  const FfnItem* items = g.items + item0;
   const int MT = g.m_total / kBlockM;
   const int KB = g.k_total / kBlockK;
   const int total = n_items * MT;
@@ -91,7 +94,7 @@ __global__ void __launch_bounds__(256, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const FfnItem it = g.items[t / MT];
+      const FfnItem it = items[t / MT];
       const int m = t % MT;
       const int nrows = (it.len + 15) & ~15;
       const int wslot = g.slot_of ? g.slot_of[it.expert] : it.expert;
@@ -118,7 +121,7 @@ __global__ void __launch_bounds__(256, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const FfnItem it = g.items[t / MT];
+      const FfnItem it = items[t / MT];
       const int n = (it.len + 15) & ~15;
       const uint32_t idesc = ptx::idesc_bf16(kBlockM, n);
       ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(256, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const FfnItem it = g.items[t / MT];
+      const FfnItem it = items[t / MT];
       const int m = t % MT;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();

@@ -39,6 +39,7 @@ struct RouteArgs {
   int32_t* block_hist;        // scratch [E * max_blocks]
   FfnItem* items;             // optional [<= E*ceil(rows/tile_n)] FFN work list
   int32_t* n_items;           // [1]
+  int32_t* item_off;          // optional [E+1]: first item of each expert (expert cache waves)
   int32_t* error_flag;        // [1] set to 1 on an out-of-range expert id
 };
 
@@ -59,6 +60,8 @@ struct GemmArgs {
   __nv_bfloat16* out;      // [rows, m_total]
   const float* wpos;       // kEpiScaleBf16: gate weight per row
   const int32_t* out_rows; // optional row remap of the output (row r -> out_rows[r])
+  const int32_t* item_off; // optional: run only the items of experts [e_lo, e_hi)
+  int e_lo, e_hi;
 };
 
 cudaError_t gemm_prepare();

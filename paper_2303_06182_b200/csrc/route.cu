@@ -284,6 +284,10 @@ __global__ void __launch_bounds__(kSingle ? kSingleThreads : kMultiThreads)
         a.items[it] = item;
       }
     }
+    if (a.item_off) {
+      for (int e = threadIdx.x; e < E; e += blockDim.x) a.item_off[e] = before[e];
+      if (threadIdx.x == 0) a.item_off[E] = n_items;
+    }
     if (threadIdx.x == 0) *a.n_items = n_items;
   }
 

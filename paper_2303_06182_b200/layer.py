@@ -125,6 +125,17 @@ class MoeLayer:
 
     __call__ = forward
 
+    def forward_routed(self, x: torch.Tensor, idx: torch.Tensor, w: torch.Tensor,
+                       out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """Forward with caller-provided routing (idx [S,k] int32, w [S,k] fp32
+        on the device) instead of the gate -- trace replay / skewed workloads."""
+        assert idx.dtype == torch.int32 and w.dtype == torch.float32 and idx.shape == w.shape
+        if out is None:
+            out = torch.empty_like(x)
+        check(self.ctx.lib.moe_layer_forward_routed(self.h, _p(x), _p(idx.contiguous()), _p(w.contiguous()),
+                                                     x.shape[0], _p(out), _stream_ptr(stream)))
+        return out
+
     def forward_host(self, x_host: torch.Tensor, out_host: torch.Tensor, stream=None):
         """End-to-end: pinned host bf16 in -> pinned host bf16 out (copies inside)."""
         check(self.ctx.lib.moe_layer_forward_host(self.h, _p(x_host), x_host.shape[0], _p(out_host),
@@ -214,3 +225,62 @@ def make_tokens(S: int, TD: int, device=None, seed: int = SEED, ctx=None):
     ctx = ctx or Context.get(device)
     x = torch.empty(S, TD, dtype=torch.bfloat16, device=torch.device("cuda", ctx.device))
     return fill_uniform_bf16(x, seed, 1, math.sqrt(3.0), ctx)
+
+
+class ExpertCache:
+    """GPU-resident LIFO/FIFO expert cache over pinned host weights
+    (moe_cache_*).  While attached, the layer reads its
+    expert weights from the cache's slot pool: run forwards through the cache."""
+
+    POLICIES = {"lifo": 0, "fifo": 1}
+
+    def __init__(self, layer: MoeLayer, n_slots: int, policy: str = "lifo", W1_host=None, W2_host=None):
+        self.layer = layer
+        self.ctx = layer.ctx
+        self.W1_host = W1_host if W1_host is not None else layer.W1.cpu().pin_memory()
+        self.W2_host = W2_host if W2_host is not None else layer.W2.cpu().pin_memory()
+        for t in (self.W1_host, self.W2_host):
+            assert t.is_pinned() and t.dtype == torch.bfloat16 and t.is_contiguous()
+        h = C.c_void_p()
+        check(self.ctx.lib.moe_cache_create(layer.h, _p(self.W1_host), _p(self.W2_host), n_slots,
+                                            self.POLICIES[policy], C.byref(h)))
+        self.h = h
+        self.n_slots = n_slots
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.moe_cache_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def forward(self, x, out=None, stream=None):
+        out = torch.empty_like(x) if out is None else out
+        check(self.ctx.lib.moe_cache_forward(self.h, _p(x), x.shape[0], _p(out), _stream_ptr(stream)))
+        return out
+
+    def forward_routed(self, x, idx, w, out=None, stream=None):
+        out = torch.empty_like(x) if out is None else out
+        check(self.ctx.lib.moe_cache_forward_routed(self.h, _p(x), _p(idx.contiguous()), _p(w.contiguous()),
+                                                    x.shape[0], _p(out), _stream_ptr(stream)))
+        return out
+
+    def stats(self) -> dict:
+        tot = (C.c_int64 * 5)()
+        last = (C.c_int * 5)()
+        check(self.ctx.lib.moe_cache_stats(self.h, C.cast(tot, C.c_void_p), C.cast(last, C.c_void_p)))
+        keys = ["accesses", "hits", "misses", "evictions"]
+        d = {k: int(v) for k, v in zip(keys, tot[:4])}
+        d["bytes_copied"] = int(tot[4])
+        d["last"] = {k: int(v) for k, v in zip(keys + ["waves"], last[:5])}
+        return d
+
+    def resident(self) -> list:
+        n = C.c_int(0)
+        buf = (C.c_int32 * max(self.n_slots, 1))()
+        check(self.ctx.lib.moe_cache_resident(self.h, C.cast(buf, C.c_void_p), C.byref(n)))
+        return [int(x) for x in buf[:n.value]]
