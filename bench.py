@@ -460,7 +460,8 @@ def run_b200(args):
     seed = 2303061820 + rank
     weights = make_weights(shape, seed=2303061820)
     layer = MoeLayer(shape, S, mode=mode, capacity_factor=C if mode == "static" else 1.0, weights=weights,
-                     tile_n=args.tile_n)
+                     tile_n=args.tile_n, fuse_combine=args.fuse_combine,
+                     split_ffn=args.split_ffn)
     x = make_tokens(S, TD, seed=seed)
     out = torch.empty_like(x)
     stream = torch.cuda.Stream()
@@ -607,6 +608,8 @@ def main():
     ap.add_argument("--placement", default="greedy", choices=["greedy", "contiguous"])
     ap.add_argument("--cache-slots", type=int, default=0, help="mt-cache: GPU slots (default E/4)")
     ap.add_argument("--tokens", type=int, default=0, help="override tokens per step (mt-cache)")
+    ap.add_argument("--fuse-combine", action="store_true", help="combine in the GEMM2 epilogue (A/B)")
+    ap.add_argument("--split-ffn", action="store_true", help="GEMM1/GEMM2 as two launches (A/B)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -149,6 +149,13 @@ typedef struct moe_layer_desc {
   double capacity_factor; /* static mode only */
   int tile_n;             /* grouped-FFN item width: 0 = auto, 128 or 256 */
   int keep_logits;        /* 1: keep fp32 gate logits [S,E] for parity checks */
+  int fuse_combine;       /* 1: dynamic gating combines inside the GEMM2
+                             epilogue (last-arrival sums the k partials);
+                             0 (default): separate combine kernel -- measured
+                             equal speed, profiles/r01_fusion_ab.md */
+  int split_ffn;          /* 1: GEMM1 and GEMM2 as two launches (H through HBM);
+                             0 (default): one fused persistent launch with H
+                             kept in L2 */
 } moe_layer_desc;
 
 /* Weights are caller-owned device buffers (bf16, row-major):

@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmoe_b200.so")
+LIB_PATH = os.environ.get("MOE_LIB_PATH") or os.path.join(_HERE, "libmoe_b200.so")  # override: A/B builds
 
 MOE_OK = 0
 MOE_ERR_INVALID_ARGUMENT = 1
@@ -55,6 +55,7 @@ class LayerDesc(C.Structure):
         ("max_tokens", C.c_int), ("token_dim", C.c_int), ("hidden_dim", C.c_int),
         ("num_experts", C.c_int), ("top_k", C.c_int), ("mode", C.c_int),
         ("capacity_factor", C.c_double), ("tile_n", C.c_int), ("keep_logits", C.c_int),
+        ("fuse_combine", C.c_int), ("split_ffn", C.c_int),
     ]
 
 

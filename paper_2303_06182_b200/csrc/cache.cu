@@ -130,6 +130,7 @@ int cache_forward(moe_cache* C, const void* X, int S, const int32_t* idx, const 
                   cudaStream_t s) {
   moe_layer* L = C->L;
   const int E = L->d.num_experts;
+  L->fwd_out = out;
   int st = layer_front(L, X, S, idx, w, s, nullptr);
   if (st) return st;
   // the one host sync: which experts are active in this batch

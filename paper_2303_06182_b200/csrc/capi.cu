@@ -65,6 +65,7 @@ int moe_ctx_create(int device, moe_ctx** out) {
   c->device = device;
   c->sms = prop.multiProcessorCount;
   e = gemm_prepare();
+  if (e == cudaSuccess) e = fused_ffn_prepare();
   if (e != cudaSuccess) {
     delete c;
     return cuda_fail(e, "gemm_prepare");
@@ -420,6 +421,8 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
       (st = L->wpos.reserve(R)) || (st = L->items.reserve(L->items_max)) ||
       (st = L->n_items.reserve(1)) || (st = L->err.reserve(1)) ||
       (st = L->item_off.reserve((size_t)E + 1)) ||
+      (st = L->comb_cnt.reserve((size_t)S * (d.token_dim / 128))) ||
+      (st = L->done.reserve(2 * (size_t)L->items_max)) ||
       (st = L->xp.reserve(Rp * TD)) || (st = L->h.reserve(Rp * HD)) ||
       (st = L->yw.reserve(R * TD))) {
     moe_layer_destroy(L);
@@ -435,6 +438,7 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
     return st;
   }
   cudaMemset(L->xp.p, 0, Rp * TD * 2);
+  cudaMemset(L->comb_cnt.p, 0, sizeof(int32_t) * (size_t)S * (d.token_dim / 128));
   cudaMemset(L->h.p, 0, Rp * HD * 2);
   if ((st = encode_bf16(&L->tmWg, Wg, E, TD, moe::gate_box_rows(E))) ||
       (st = encode_bf16(&L->tmW1, W1, (uint64_t)E * HD, TD, 128)) ||
@@ -472,6 +476,8 @@ int moe_layer_destroy(moe_layer* L) {
   L->n_items.release();
   L->err.release();
   L->item_off.release();
+  L->comb_cnt.release();
+  L->done.release();
   L->dropped.release();
   L->n_dropped.release();
   L->logits.release();
@@ -501,12 +507,12 @@ int moe::capi::layer_front(moe_layer* L, const void* X, int S, const int32_t* id
   const float* w = idx_in ? w_in : L->w.p;
   // 1. gate
   mark(0);
+  if (X != L->tmX_ptr || S != L->tmX_rows) {
+    if ((st = encode_bf16(&L->tmX, X, (uint64_t)S, TD, 128))) return st;
+    L->tmX_ptr = X;
+    L->tmX_rows = S;
+  }
   if (!idx_in) {
-    if (X != L->tmX_ptr || S != L->tmX_rows) {
-      if ((st = encode_bf16(&L->tmX, X, (uint64_t)S, TD, 128))) return st;
-      L->tmX_ptr = X;
-      L->tmX_rows = S;
-    }
     GateArgs ga{S, TD, E, k, L->idx.p, L->w.p, d.keep_logits ? L->logits.p : nullptr};
     cudaError_t e = launch_gate(L->tmX, L->tmWg, ga, s);
     if (e != cudaSuccess) return cuda_fail(e, "gate launch");
@@ -540,7 +546,51 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
     if (ev) cudaEventRecord(ev[i], s);
   };
   const int32_t* off = e_lo >= 0 ? L->item_off.p : nullptr;
+  const bool fcomb = layer_fused_combine(L);
   mark(3);
+  // fused single launch in the weight-streaming regime (dynamic gating, many
+  // small items); compute-bound static batches and few-expert layers (cfg1)
+  // measured faster as two launches (profiles/r01_fused_ffn.md)
+  const bool one_launch = !L->d.split_ffn && !fcomb && L->d.mode == MOE_GATING_DYNAMIC &&
+                          L->tile_n == 128;
+  if (one_launch) {
+    // one persistent launch for both GEMMs, H kept in L2 (ffn_fused.cu)
+    MOE_CUDA(cudaMemsetAsync(L->done.p, 0, sizeof(int32_t) * 2 * (size_t)L->items_max, s));
+    FusedFfnArgs fa{};
+    fa.items = L->items.p;
+    fa.n_items = L->n_items.p;
+    fa.item_off = off;
+    fa.e_lo = e_lo;
+    fa.e_hi = e_hi;
+    fa.slot_of = L->slot_of;
+    fa.TD = TD;
+    fa.HD = HD;
+    fa.H = L->h.p;
+    fa.Yw = L->yw.p;
+    fa.wpos = L->wpos.p;
+    fa.done1 = L->done.p;
+    fa.done2 = L->done.p + L->items_max;
+    // an item's GEMM2 tiles trail its GEMM1 tiles by ~8 waves of CTAs
+    // (measured on the LM shape: 4 waves 1.49 ms, 8 waves 1.375 ms, 16 waves
+    // 1.43 ms FFN; profiles/r01_fused_ffn.md); MOE_FFN_LAG overrides (items)
+    static const int lag_env = [] {
+      const char* v = getenv("MOE_FFN_LAG");
+      return v ? atoi(v) : 0;
+    }();
+    const int per_item = HD / 128 + TD / 128;
+    const int lag = lag_env > 0 ? lag_env : std::max(2, (8 * L->ctx->sms + per_item - 1) / per_item);
+    static const int discard = [] {
+      const char* v = getenv("MOE_FFN_DISCARD");
+      return v ? atoi(v) : 1;
+    }();
+    fa.lag = lag;
+    fa.discard_h = discard;
+    cudaError_t e = launch_fused_ffn(L->tmW1, L->tmXp, L->tmW2, L->tmH, fa, L->tile_n,
+                                     L->ctx->sms, s);
+    if (e != cudaSuccess) return cuda_fail(e, "fused ffn launch");
+    mark(4);
+    return MOE_OK;
+  }
   GemmArgs g1{L->items.p, L->n_items.p, L->slot_of, HD, TD, kEpiReluBf16, L->h.p, nullptr, nullptr,
               off, e_lo, e_hi};
   cudaError_t e = launch_grouped_gemm(L->tmW1, L->tmXp, g1, L->tile_n, L->ctx->sms, s);
@@ -548,6 +598,18 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
   mark(4);
   GemmArgs g2{L->items.p, L->n_items.p, L->slot_of, TD, HD, kEpiScaleBf16, L->yw.p, L->wpos.p,
               nullptr, off, e_lo, e_hi};
+  if (fcomb && L->d.top_k == 1) {
+    // one contribution per token: write the layer output directly (row -> token)
+    g2.out = static_cast<__nv_bfloat16*>(L->fwd_out);
+    g2.out_rows = L->order.p;
+  } else if (fcomb) {
+    g2.mode = kEpiScaleCombine;
+    g2.top_k = L->d.top_k;
+    g2.comb_order = L->order.p;
+    g2.comb_pos = L->pos.p;
+    g2.comb_cnt = L->comb_cnt.p;
+    g2.comb_out = static_cast<__nv_bfloat16*>(L->fwd_out);
+  }
   e = launch_grouped_gemm(L->tmW2, L->tmH, g2, L->tile_n, L->ctx->sms, s);
   if (e != cudaSuccess) return cuda_fail(e, "grouped gemm 2 launch");
   return MOE_OK;
@@ -560,9 +622,11 @@ int moe::capi::layer_back(moe_layer* L, int S, void* out, cudaStream_t s, cudaEv
     if (ev) cudaEventRecord(ev[i], s);
   };
   mark(5);
-  cudaError_t e = launch_combine(L->yw.p, L->pos.p, S, L->d.top_k, L->d.token_dim,
-                                 (__nv_bfloat16*)out, s);
-  if (e != cudaSuccess) return cuda_fail(e, "combine launch");
+  if (!layer_fused_combine(L)) {
+    cudaError_t e = launch_combine(L->yw.p, L->pos.p, S, L->d.top_k, L->d.token_dim,
+                                   (__nv_bfloat16*)out, s);
+    if (e != cudaSuccess) return cuda_fail(e, "combine launch");
+  }
   mark(6);
   return MOE_OK;
 }
@@ -578,6 +642,7 @@ static int layer_forward_impl(moe_layer* L, const void* X, int S, void* out, cud
     ++L->t_calls;
   }
   int st;
+  L->fwd_out = out;
   if ((st = layer_front(L, X, S, idx_in, w_in, s, ev))) return st;
   if ((st = layer_ffn(L, s, -1, -1, ev))) return st;
   return layer_back(L, S, out, s, ev);

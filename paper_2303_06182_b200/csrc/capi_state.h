@@ -7,6 +7,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -149,9 +150,12 @@ struct moe_layer {
   int rows_max = 0;
   int items_max = 0;
   CUtensorMap tmWg, tmW1, tmW2, tmXp, tmH;
-  CUtensorMap tmX;
+  CUtensorMap tmX;  // X for the gate (box 64 x 128)
   const void* tmX_ptr = nullptr;
   int tmX_rows = 0;
+  DevBuf<int32_t> comb_cnt;  // fused-combine counters [S_max * TD/128], self-resetting
+  DevBuf<int32_t> done;      // fused-FFN per-item counters [2 * items_max]
+  void* fwd_out = nullptr;   // output of the forward in flight (fused combine target)
   // optional expert-cache weight pool
   const int32_t* slot_of = nullptr;
   DevBuf<int32_t> idx, pos, counts, splits, order, dropped, n_dropped, n_items, err, item_off;
@@ -195,5 +199,9 @@ int layer_front(moe_layer* L, const void* X, int S, const int32_t* idx_in, const
                 cudaStream_t s, cudaEvent_t* ev);
 int layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaEvent_t* ev);
 int layer_back(moe_layer* L, int S, void* out, cudaStream_t s, cudaEvent_t* ev);
+// dynamic gating with fuse_combine: the combine runs inside the GEMM2 epilogue
+inline bool layer_fused_combine(const moe_layer* L) {
+  return L->d.mode == MOE_GATING_DYNAMIC && L->d.fuse_combine;
+}
 }  // namespace capi
 }  // namespace moe

@@ -40,6 +40,58 @@ struct GemmCfg {
   static constexpr int kTmemCols = 2 * BN;
 };
 
+// Fused combine for one GEMM2 tile (128 output features x it.len rows), run
+// by the 4 epilogue warps (tid 0..127) after the tile's bf16 partials
+// (gate-weighted, Yw[row]) are stored.  Each row bumps its token's counter for
+// this 128-feature block; the k-th arrival is the finisher, which sums the k
+// partials of the token in slot order (j = 0..k-1) in fp32 and writes the
+// bf16 layer output -- the arithmetic of combine_kernel, so the result is
+// bitwise the same whatever order the contributions arrive in.  All rows of
+// the tile are handled together: one fence, one round of atomics, one round
+// of partial loads.
+__device__ __forceinline__ void combine_tile(const GemmArgs& g, const FfnItem& it, int m, int MT,
+                                             int tid, int* fin_tok, int* fin_cnt) {
+  const int k = g.top_k;
+  __threadfence();  // this thread's partial stores are visible device-wide
+  if (tid == 0) fin_cnt[0] = 0;
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  for (int r = tid; r < it.len; r += 128) {
+    const int tk = g.comb_order[it.row0 + r] / k;
+    int* cnt = g.comb_cnt + static_cast<size_t>(tk) * MT + m;
+    if (atomicAdd(cnt, 1) == k - 1) {
+      *cnt = 0;  // self-reset for the next forward
+      fin_tok[atomicAdd(fin_cnt, 1)] = tk;
+    }
+  }
+  __threadfence();
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  const int nfin = fin_cnt[0];
+  const int col = m * 128;
+  for (int w = tid; w < nfin * 16; w += 128) {
+    const int tk = fin_tok[w >> 4];
+    const int c = (w & 15) * 8;  // 8 bf16 = 16 bytes
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < k; ++j) {
+      const int p = g.comb_pos[static_cast<size_t>(tk) * k + j];
+      const uint4 v = __ldcg(reinterpret_cast<const uint4*>(g.out + static_cast<size_t>(p) * g.m_total +
+                                                             col + c));
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(h[i]);
+        acc[2 * i] += f.x;
+        acc[2 * i + 1] += f.y;
+      }
+    }
+    uint4 o;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+    *reinterpret_cast<uint4*>(g.comb_out + static_cast<size_t>(tk) * g.m_total + col + c) = o;
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");  // fin_tok is reused by the next tile
+}
+
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(256, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -89,6 +141,8 @@ __global__ void __launch_bounds__(256, 1)
 
   if (warp == 0 && lane == 0) {
     // ------------------------------------------------------------ producer
+    // (single thread: a warp-wide producer -- needed for per-lane TMA gather4 --
+    // measured 15% slower on the LM shape, profiles/r01_fusion_ab.md)
     const uint64_t pol_a = ptx::policy_evict_first();
     const uint64_t pol_b = ptx::policy_evict_last();
     int stage = 0;
@@ -151,6 +205,8 @@ __global__ void __launch_bounds__(256, 1)
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;  // TMEM lane quadrant owned by this warp
     __nv_bfloat16* stg = sEpi + q * 32 * 32;
+    __shared__ int fin_tok[256];  // tokens whose last contribution is in this tile
+    __shared__ int fin_cnt[1];
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -167,7 +223,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i)
             stg[i * 32 + lane] = __float2bfloat16_rn(fmaxf(__uint_as_float(r[i]), 0.f));
-        } else {
+        } else {  // kEpiScaleBf16 / kEpiScaleCombine: gate weight of the row
           const float wv = (c0 + lane < it.len) ? g.wpos[it.row0 + c0 + lane] : 0.f;
 #pragma unroll
           for (int i = 0; i < 32; ++i)
@@ -189,11 +245,13 @@ __global__ void __launch_bounds__(256, 1)
         }
         __syncwarp();
       }
+      // TMEM of this tile is no longer needed: release it before the combine
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
+      if (g.mode == kEpiScaleCombine) combine_tile(g, it, m, MT, threadIdx.x - 128, fin_tok, fin_cnt);
     }
   }
 

@@ -1,0 +1,323 @@
+// Fused expert FFN: GEMM1 (relu) and GEMM2 (gate-weighted) tiles in ONE
+// persistent tcgen05 kernel, with the hidden activations H kept in L2.
+//
+// In the two-launch form (ffn.cu) H makes a full HBM round trip: GEMM1 writes
+// rows * HD bf16 and GEMM2 reads them back (536 MB per LM layer call, ~82 us of
+// a 1.4 ms weight stream).  Here the tile sequence interleaves the two GEMMs:
+//
+//   group g = [ GEMM1 tiles of item g ] + [ GEMM2 tiles of item g - L ]
+//
+// so an item's GEMM2 tiles run about one wave of CTAs after its GEMM1 tiles,
+// while its H rows (n_e x HD bf16, ~0.5 MB) are still resident in L2.  The
+// GEMM2 producer waits on a per-item counter (all HD/128 GEMM1 tiles stored,
+// release/acquire + proxy fences) before TMA-loading H; when the last of the
+// item's TD/128 GEMM2 tiles has consumed H, its lines are dropped from L2
+// with discard.global.L2 so the dead activations are never written back.
+//
+// Deadlock freedom: every CTA walks its tiles in increasing sequence order and
+// a GEMM2 tile only depends on GEMM1 tiles earlier in the sequence, so the
+// earliest unfinished tile can always make progress (all CTAs are resident:
+// one per SM).
+//
+// Roles per CTA (256 threads) are those of grouped_gemm_kernel: warp 0 TMA
+// producer, warp 1 MMA issuer, warp 2 TMEM allocator, warps 4-7 epilogue.
+#include "moe_internal.h"
+#include "ptx.cuh"
+
+namespace moe {
+
+namespace {
+
+constexpr int kBlockM = 128;
+constexpr int kBlockK = 64;
+constexpr int kUmmaK = 16;
+constexpr int kABytes = kBlockM * kBlockK * 2;
+constexpr int kEpiBytes = 4 * 32 * 32 * 2;
+constexpr int kBoxRowsB = 16;
+
+template <int BN, int STAGES>
+struct FusedCfg {
+  static constexpr int kBBytes = BN * kBlockK * 2;
+  static constexpr int kSmem = 1024 + STAGES * (kABytes + kBBytes) + kEpiBytes +
+                               (2 * STAGES + 4) * 8 + 16;
+  static constexpr int kTmemCols = 2 * BN;
+};
+
+struct TileRef {
+  int item;
+  int gemm;  // 0: GEMM1 (W1 x Xp -> relu -> H), 1: GEMM2 (W2 x H -> scale -> Yw)
+  int m;     // 128-row block of the weight matrix
+};
+
+// Sequence position -> tile.  n items, lag L (<= n), MT1/MT2 m-blocks.
+__device__ __forceinline__ TileRef decode_tile(int t, int n, int L, int MT1, int MT2) {
+  const int head = L * MT1;
+  if (t < head) return {t / MT1, 0, t % MT1};
+  const int per = MT1 + MT2;
+  const int body = head + (n - L) * per;
+  if (t < body) {
+    const int u = t - head;
+    const int g = L + u / per;
+    const int r = u % per;
+    if (r < MT1) return {g, 0, r};
+    return {g - L, 1, r - MT1};
+  }
+  const int u = t - body;
+  return {n - L + u / MT2, 1, u % MT2};
+}
+
+__device__ __forceinline__ int ld_acquire(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __forceinline__ void discard_l2(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(256, 1)
+    fused_ffn_kernel(const __grid_constant__ CUtensorMap tmW1,
+                     const __grid_constant__ CUtensorMap tmXp,
+                     const __grid_constant__ CUtensorMap tmW2,
+                     const __grid_constant__ CUtensorMap tmH, FusedFfnArgs g) {
+  using Cfg = FusedCfg<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + STAGES * kABytes;
+  __nv_bfloat16* sEpi = reinterpret_cast<__nv_bfloat16*>(sB + STAGES * Cfg::kBBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sEpi) + kEpiBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ int last_consumer;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmW1);
+    ptx::prefetch_tmap(&tmXp);
+    ptx::prefetch_tmap(&tmW2);
+    ptx::prefetch_tmap(&tmH);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&tfull[s], 1);
+      ptx::mbar_init(&tempty[s], 4);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int item0 = g.item_off ? g.item_off[g.e_lo] : 0;
+  const int n = g.item_off ? g.item_off[g.e_hi] - item0 : *g.n_items;
+  const FfnItem* items = g.items + item0;
+  int32_t* done1 = g.done1 + item0;
+  int32_t* done2 = g.done2 + item0;
+  const int MT1 = g.HD / kBlockM, MT2 = g.TD / kBlockM;
+  const int KB1 = g.TD / kBlockK, KB2 = g.HD / kBlockK;
+  const int L = min(g.lag, n);
+  const int total = n * (MT1 + MT2);
+
+  if (warp == 0 && lane == 0) {
+    // ------------------------------------------------------------ producer
+    const uint64_t pol_w = ptx::policy_evict_first();
+    const uint64_t pol_x = ptx::policy_evict_last();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const TileRef tr = decode_tile(t, n, L, MT1, MT2);
+      const FfnItem it = items[tr.item];
+      const int nrows = (it.len + 15) & ~15;
+      const int wslot = g.slot_of ? g.slot_of[it.expert] : it.expert;
+      const CUtensorMap* tA = tr.gemm ? &tmW2 : &tmW1;
+      const CUtensorMap* tB = tr.gemm ? &tmH : &tmXp;
+      const int a_row = wslot * (tr.gemm ? g.TD : g.HD) + tr.m * kBlockM;
+      const int KB = tr.gemm ? KB2 : KB1;
+      if (tr.gemm) {
+        // H rows of this item: every GEMM1 tile stored (acquire), then make
+        // the generic-proxy stores visible to this thread's TMA reads
+        uint32_t polls = 0;
+        while (ld_acquire(done1 + tr.item) < MT1) {
+          __nanosleep(64);
+          if (++polls == (1u << 28)) __trap();
+        }
+        fence_proxy_async_global();
+      }
+      const uint32_t bytes = kABytes + nrows * kBlockK * 2;
+      for (int kb = 0; kb < KB; ++kb) {
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        ptx::mbar_arrive_expect_tx(&full[stage], bytes);
+        ptx::tma_load_2d(sA + stage * kABytes, tA, &full[stage], kb * kBlockK, a_row, pol_w);
+        uint8_t* b_dst = sB + stage * Cfg::kBBytes;
+        for (int r = 0; r < nrows; r += kBoxRowsB)
+          ptx::tma_load_2d(b_dst + r * kBlockK * 2, tB, &full[stage], kb * kBlockK, it.row0 + r,
+                           pol_x);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ------------------------------------------------------------ MMA issuer
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const TileRef tr = decode_tile(t, n, L, MT1, MT2);
+      const FfnItem it = items[tr.item];
+      const int nn = (it.len + 15) & ~15;
+      const uint32_t idesc = ptx::idesc_bf16(kBlockM, nn);
+      const int KB = tr.gemm ? KB2 : KB1;
+      ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t d = tmem_base + acc * BN;
+      for (int kb = 0; kb < KB; ++kb) {
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        const uint32_t a0 = ptx::smem_u32(sA + stage * kABytes);
+        const uint32_t b0 = ptx::smem_u32(sB + stage * Cfg::kBBytes);
+#pragma unroll
+        for (int kk = 0; kk < kBlockK / kUmmaK; ++kk)
+          ptx::mma_bf16(d, ptx::umma_desc_sw128(a0 + kk * kUmmaK * 2),
+                        ptx::umma_desc_sw128(b0 + kk * kUmmaK * 2), idesc,
+                        (kb | kk) != 0 ? 1u : 0u);
+        ptx::mma_commit(&empty[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      ptx::mma_commit(&tfull[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;
+    const int tid = threadIdx.x - 128;
+    __nv_bfloat16* stg = sEpi + q * 32 * 32;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const TileRef tr = decode_tile(t, n, L, MT1, MT2);
+      const FfnItem it = items[tr.item];
+      const int m_total = tr.gemm ? g.TD : g.HD;
+      __nv_bfloat16* out = tr.gemm ? g.Yw : g.H;
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int col0 = tr.m * kBlockM + q * 32;
+      for (int c0 = 0; c0 < it.len; c0 += 32) {
+        uint32_t r[32];
+        ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c0, r);
+        ptx::tmem_ld_wait();
+        if (tr.gemm == 0) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            stg[i * 32 + lane] = __float2bfloat16_rn(fmaxf(__uint_as_float(r[i]), 0.f));
+        } else {
+          const float wv = (c0 + lane < it.len) ? g.wpos[it.row0 + c0 + lane] : 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            stg[i * 32 + lane] =
+                __float2bfloat16_rn(__uint_as_float(r[i]) * __shfl_sync(0xffffffffu, wv, i));
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int tok = j * 8 + (lane >> 2);
+          const int ch = lane & 3;
+          if (c0 + tok < it.len) {
+            const uint4 v = *reinterpret_cast<const uint4*>(stg + tok * 32 + ch * 8);
+            *reinterpret_cast<uint4*>(out + static_cast<size_t>(it.row0 + c0 + tok) * m_total +
+                                      col0 + ch * 8) = v;
+          }
+        }
+        __syncwarp();
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+      if (tr.gemm == 0) {
+        // publish this GEMM1 tile's H rows
+        fence_proxy_async_global();
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (tid == 0) atomicAdd(done1 + tr.item, 1);
+      } else {
+        // this tile's MMAs (hence its H reads) are complete; the last consumer
+        // of the item drops the item's H lines from L2 without write-back
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (tid == 0) last_consumer = atomicAdd(done2 + tr.item, 1) == MT2 - 1;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (last_consumer && g.discard_h) {
+          const int lines_per_row = g.HD * 2 / 128;
+          const int lines = it.len * lines_per_row;
+          for (int l = tid; l < lines; l += 128)
+            discard_l2(g.H + static_cast<size_t>(it.row0 + l / lines_per_row) * g.HD +
+                       (l % lines_per_row) * 64);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+}
+
+template <int BN, int STAGES>
+cudaError_t prepare_fused() {
+  return cudaFuncSetAttribute(fused_ffn_kernel<BN, STAGES>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              FusedCfg<BN, STAGES>::kSmem);
+}
+
+template <int BN, int STAGES>
+cudaError_t launch_fused(const CUtensorMap& w1, const CUtensorMap& xp, const CUtensorMap& w2,
+                         const CUtensorMap& h, const FusedFfnArgs& g, int grid,
+                         cudaStream_t stream) {
+  fused_ffn_kernel<BN, STAGES>
+      <<<grid, 256, FusedCfg<BN, STAGES>::kSmem, stream>>>(w1, xp, w2, h, g);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t fused_ffn_prepare() {
+  cudaError_t e = prepare_fused<128, 6>();
+  if (e != cudaSuccess) return e;
+  return prepare_fused<256, 4>();
+}
+
+cudaError_t launch_fused_ffn(const CUtensorMap& tmW1, const CUtensorMap& tmXp,
+                             const CUtensorMap& tmW2, const CUtensorMap& tmH,
+                             const FusedFfnArgs& args, int tile_n, int grid,
+                             cudaStream_t stream) {
+  if (tile_n == 128) return launch_fused<128, 6>(tmW1, tmXp, tmW2, tmH, args, grid, stream);
+  if (tile_n == 256) return launch_fused<256, 4>(tmW1, tmXp, tmW2, tmH, args, grid, stream);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace moe

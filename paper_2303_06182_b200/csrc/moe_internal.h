@@ -48,7 +48,7 @@ cudaError_t route_prepare(int E, int* max_blocks);
 cudaError_t launch_route(RouteArgs a, int max_blocks, cudaStream_t stream);
 
 // ---- grouped expert FFN (tcgen05)
-enum EpilogueMode { kEpiReluBf16 = 0, kEpiScaleBf16 = 1 };
+enum EpilogueMode { kEpiReluBf16 = 0, kEpiScaleBf16 = 1, kEpiScaleCombine = 2 };
 
 struct GemmArgs {
   const FfnItem* items;
@@ -62,7 +62,36 @@ struct GemmArgs {
   const int32_t* out_rows; // optional row remap of the output (row r -> out_rows[r])
   const int32_t* item_off; // optional: run only the items of experts [e_lo, e_hi)
   int e_lo, e_hi;
+  // fused combine (kEpiScaleCombine): the last of the k contributions of a
+  // token (per 128-feature block) sums the bf16 partials in slot order and
+  // writes the layer output; counters [S * m_total/128] self-reset to 0.
+  int top_k;
+  const int32_t* comb_order;
+  const int32_t* comb_pos;
+  int32_t* comb_cnt;
+  __nv_bfloat16* comb_out;
 };
+
+// Fused GEMM1 + GEMM2 (ffn_fused.cu): one persistent launch, H kept in L2.
+struct FusedFfnArgs {
+  const FfnItem* items;
+  const int32_t* n_items;
+  const int32_t* item_off;  // optional expert range [e_lo, e_hi) (cache waves)
+  int e_lo, e_hi;
+  const int32_t* slot_of;   // optional expert -> weight slot
+  int TD, HD;
+  __nv_bfloat16* H;         // [rows, HD]
+  __nv_bfloat16* Yw;        // [rows, TD]
+  const float* wpos;        // gate weight per row
+  int32_t* done1;           // [items] GEMM1 tiles stored (zeroed before launch)
+  int32_t* done2;           // [items] GEMM2 tiles finished (zeroed before launch)
+  int lag;                  // items between an item's GEMM1 and GEMM2 tiles
+  int discard_h;            // drop consumed H lines from L2 (no write-back)
+};
+cudaError_t fused_ffn_prepare();
+cudaError_t launch_fused_ffn(const CUtensorMap& tmW1, const CUtensorMap& tmXp,
+                             const CUtensorMap& tmW2, const CUtensorMap& tmH,
+                             const FusedFfnArgs& args, int tile_n, int grid, cudaStream_t stream);
 
 cudaError_t gemm_prepare();
 // tmA: weights [slots*m_total, k_total]; tmB: activations [rows, k_total]
