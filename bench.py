@@ -129,13 +129,12 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(use), "samples_in_timed_region": len(inside)}
 
 
-def ffn_bytes(rows, active, TD, HD):
-    """Algorithmic HBM bytes of the grouped FFN (both launches), bf16:
-    each active expert's W1 and W2 read once, Xp read, H written then read,
-    Yw written."""
-    g1 = active * HD * TD * 2 + rows * TD * 2 + rows * HD * 2
-    g2 = active * TD * HD * 2 + rows * HD * 2 + rows * TD * 2
-    return g1, g2
+def ffn_bytes(rows, active, TD, HD, one_launch):
+    """Algorithmic HBM bytes of the grouped FFN, bf16: each active expert's W1
+    and W2 read once, Xp read, Yw written; the two-launch form also writes H
+    and reads it back (the fused launch keeps H in L2)."""
+    h = 0 if one_launch else 2 * rows * HD * 2
+    return active * 2 * HD * TD * 2 + rows * TD * 2 + rows * TD * 2 + h
 
 
 def layer_roofline(S, TD, HD, E, k, active, hbm_gbs, tflops):
@@ -461,13 +460,13 @@ def run_b200(args):
     weights = make_weights(shape, seed=2303061820)
     layer = MoeLayer(shape, S, mode=mode, capacity_factor=C if mode == "static" else 1.0, weights=weights,
                      tile_n=args.tile_n, fuse_combine=args.fuse_combine,
-                     split_ffn=args.split_ffn)
+                     split_ffn=args.split_ffn, fuse_front=args.fuse_front)
     x = make_tokens(S, TD, seed=seed)
     out = torch.empty_like(x)
     stream = torch.cuda.Stream()
     lib = layer.ctx.lib
     K, W = args.steps, args.warmup
-    _capi.check(lib.moe_layer_enable_timing(layer.h, K))
+    _capi.check(lib.moe_layer_enable_timing(layer.h, 0))
 
     with torch.cuda.stream(stream):
         for _ in range(W):
@@ -478,38 +477,52 @@ def run_b200(args):
     counts = v["counts"].cpu().numpy()
     active = int((counts > 0).sum()) if mode == "dynamic" else E
     rows = int(v["rows"])
-    # reset the timing ring so slot i <-> timed step i
-    _capi.check(lib.moe_layer_enable_timing(layer.h, K))
+    import ctypes
 
+    # ---- per-stage breakdown (CUDA events between the kernels of each step),
+    #      a separate pass: event records between kernels would break the
+    #      programmatic-dependent-launch overlap of the timed steps
+    Ks = min(K, 20)
+    _capi.check(lib.moe_layer_enable_timing(layer.h, Ks))
+    with torch.cuda.stream(stream):
+        for _ in range(Ks):
+            layer.forward(x, out, stream=stream)
+    stream.synchronize()
+    stage = np.zeros((Ks, len(STAGES)), np.float64)
+    buf = (ctypes.c_float * len(STAGES))()
+    for i in range(Ks):
+        _capi.check(lib.moe_layer_stage_times(layer.h, i, ctypes.cast(buf, ctypes.c_void_p)))
+        stage[i] = list(buf)
+    _capi.check(lib.moe_layer_enable_timing(layer.h, 0))
+
+    # ---- timed region: K steps (one CUDA-graph replay of the whole layer per
+    #      step unless --no-graph), events per step for the p50
+    use_graph = not args.no_graph
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            layer.forward(x, out, graph=use_graph, stream=stream)
+    stream.synchronize()
     sampler = ClockSampler(local) if not args.no_clocks else None
     if sampler:
         sampler.start()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
     barrier(world)
     torch.cuda.synchronize()
     if sampler:
         sampler.mark_start()
     with torch.cuda.stream(stream):
-        ev0.record(stream)
-        for _ in range(K):
-            layer.forward(x, out, stream=stream)
-        ev1.record(stream)
+        for i in range(K):
+            evs[i].record(stream)
+            layer.forward(x, out, graph=use_graph, stream=stream)
+        evs[K].record(stream)
     stream.synchronize()
     torch.cuda.synchronize()
     if sampler:
         sampler.mark_stop()
     barrier(world)
-    elapsed_ms = ev0.elapsed_time(ev1)
+    elapsed_ms = evs[0].elapsed_time(evs[K])
     layer.check_errors(stream)
-    stage = np.zeros((K, len(STAGES)), np.float64)
-    import ctypes
-
-    buf = (ctypes.c_float * len(STAGES))()
-    for i in range(K):
-        _capi.check(lib.moe_layer_stage_times(layer.h, i, ctypes.cast(buf, ctypes.c_void_p)))
-        stage[i] = list(buf)
-    step_ms = stage.sum(1)
+    step_ms = np.array([evs[i].elapsed_time(evs[i + 1]) for i in range(K)])
     elapsed_max = max_over_ranks(elapsed_ms, world)
     p50 = float(np.median(step_ms))
     p50_max = max_over_ranks(p50, world)
@@ -539,10 +552,11 @@ def run_b200(args):
     ms_per_step = elapsed_max / K
     value = world * S / (ms_per_step * 1e-3)
     mean_stage = stage.mean(0)
-    g1b, g2b = ffn_bytes(rows, active, TD, HD)
+    one_launch = mode == "dynamic" and int(v["tile_n"]) == 128 and not args.split_ffn
+    ffn_b = ffn_bytes(rows, active, TD, HD, one_launch)
     ffn_ms = mean_stage[3] + mean_stage[4]
-    achieved = (g1b + g2b) / (ffn_ms * 1e-3) / 1e9
-    traffic = load_traffic(args.workload)
+    achieved = ffn_b / (ffn_ms * 1e-3) / 1e9
+    traffic = load_traffic(args.workload) if one_launch else None
     t_roof, F, B = layer_roofline(S, TD, HD, E, k, active, hbm_gbs, tflops)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -566,13 +580,15 @@ def run_b200(args):
                    "parallelism": f"replicas x{world} (all experts on every GPU)" if world > 1 else "single GPU",
                    "l2": "no flush: per-step working set (expert weights, %.1f GB) >> 126 MB L2" % (
                        2 * active * TD * HD * 2 / 1e9)},
-        "roofline": {"kernel": "grouped_gemm_kernel (FFN GEMM1 + GEMM2)", "bound": "hbm",
+        "roofline": {"kernel": ("fused_ffn_kernel (GEMM1+GEMM2, one launch, H in L2)" if one_launch
+                                else "grouped_gemm_kernel (FFN GEMM1 + GEMM2)"), "bound": "hbm",
                      "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s", "frac": achieved / hbm_gbs,
-                     "peak_kind": peak_kind, "algorithmic_bytes_per_step": g1b + g2b,
+                     "peak_kind": peak_kind, "algorithmic_bytes_per_step": ffn_b,
                      "traffic": traffic},
         "layer_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms_per_step, "flops": F,
                            "bytes": B, "peaks": {"hbm_gbs": hbm_gbs, "bf16_tflops": tflops}},
         "stage_ms": {n: float(m) for n, m in zip(STAGES, mean_stage)},
+        "timed_path": "CUDA graph replay of moe_layer_forward (PDL edges)" if use_graph else "eager launches",
         "gpu_launches": 6 * K,
         "e2e": {"value": world * S / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": S * TD * 2, "d2h_bytes_per_step": S * TD * 2,
@@ -610,6 +626,8 @@ def main():
     ap.add_argument("--tokens", type=int, default=0, help="override tokens per step (mt-cache)")
     ap.add_argument("--fuse-combine", action="store_true", help="combine in the GEMM2 epilogue (A/B)")
     ap.add_argument("--split-ffn", action="store_true", help="GEMM1/GEMM2 as two launches (A/B)")
+    ap.add_argument("--fuse-front", action="store_true", help="gate+dispatch+gather in one launch (A/B)")
+    ap.add_argument("--no-graph", action="store_true", help="timed steps as eager launches")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -156,6 +156,10 @@ typedef struct moe_layer_desc {
   int split_ffn;          /* 1: GEMM1 and GEMM2 as two launches (H through HBM);
                              0 (default): one fused persistent launch with H
                              kept in L2 */
+  int fuse_front;         /* 1: gate + dispatch + gather in one cooperative
+                             launch (dynamic gating, batch <= one 128-token
+                             tile per SM); 0 (default): three launches --
+                             measured faster, profiles/r01_fusion_ab.md */
 } moe_layer_desc;
 
 /* Weights are caller-owned device buffers (bf16, row-major):

@@ -512,6 +512,31 @@ int moe::capi::layer_front(moe_layer* L, const void* X, int S, const int32_t* id
     L->tmX_ptr = X;
     L->tmX_rows = S;
   }
+  if (!idx_in && d.mode == MOE_GATING_DYNAMIC && d.fuse_front &&
+      gate_dispatch_supported(S, E, k, TD, L->ctx->sms)) {
+    // gate + dispatch + gather in one cooperative launch
+    GateArgs ga{S, TD, E, k, L->idx.p, L->w.p, d.keep_logits ? L->logits.p : nullptr};
+    DispatchArgs da{};
+    da.X = X;
+    da.Xp = L->xp.p;
+    da.counts = L->counts.p;
+    da.splits = L->splits.p;
+    da.order = L->order.p;
+    da.pos = L->pos.p;
+    da.wpos = L->wpos.p;
+    da.block_hist = L->ctx->block_hist.p;
+    da.items = L->items.p;
+    da.n_items = L->n_items.p;
+    da.item_off = L->item_off.p;
+    da.tile_n = L->tile_n;
+    L->last_rows = S * k;
+    L->last_cap = 0;
+    cudaError_t e = launch_gate_dispatch(L->tmX, L->tmWg, ga, da, s);
+    if (e != cudaSuccess) return cuda_fail(e, "gate+dispatch launch");
+    mark(1);
+    mark(2);
+    return MOE_OK;
+  }
   if (!idx_in) {
     GateArgs ga{S, TD, E, k, L->idx.p, L->w.p, d.keep_logits ? L->logits.p : nullptr};
     cudaError_t e = launch_gate(L->tmX, L->tmWg, ga, s);

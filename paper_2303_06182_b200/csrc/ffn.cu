@@ -130,6 +130,8 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // the work list and activations come from the previous kernel
 
   // optional expert range (expert-cache waves): items of experts [e_lo, e_hi)
   const int item0 = g.item_off ? g.item_off[g.e_lo] : 0;
@@ -271,9 +273,8 @@ cudaError_t prepare_one() {
 template <int BN, int STAGES>
 cudaError_t launch_one(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& g,
                        int grid, cudaStream_t stream) {
-  grouped_gemm_kernel<BN, STAGES>
-      <<<grid, 256, GemmCfg<BN, STAGES>::kSmem, stream>>>(tmA, tmB, g);
-  return cudaGetLastError();
+  return launch_chain(grouped_gemm_kernel<BN, STAGES>, dim3(grid), dim3(256),
+                      GemmCfg<BN, STAGES>::kSmem, stream, false, tmA, tmB, g);
 }
 
 }  // namespace

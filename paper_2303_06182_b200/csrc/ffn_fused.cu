@@ -123,6 +123,8 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // the work list and activations come from the previous kernel
 
   const int item0 = g.item_off ? g.item_off[g.e_lo] : 0;
   const int n = g.item_off ? g.item_off[g.e_hi] - item0 : *g.n_items;
@@ -298,9 +300,8 @@ template <int BN, int STAGES>
 cudaError_t launch_fused(const CUtensorMap& w1, const CUtensorMap& xp, const CUtensorMap& w2,
                          const CUtensorMap& h, const FusedFfnArgs& g, int grid,
                          cudaStream_t stream) {
-  fused_ffn_kernel<BN, STAGES>
-      <<<grid, 256, FusedCfg<BN, STAGES>::kSmem, stream>>>(w1, xp, w2, h, g);
-  return cudaGetLastError();
+  return launch_chain(fused_ffn_kernel<BN, STAGES>, dim3(grid), dim3(256),
+                      FusedCfg<BN, STAGES>::kSmem, stream, false, w1, xp, w2, h, g);
 }
 
 }  // namespace

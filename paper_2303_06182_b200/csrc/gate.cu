@@ -18,6 +18,7 @@
 // Warp 0 = TMA producer, warp 1 = MMA issuer, warp 2 = TMEM allocator,
 // warps 4-7 = epilogue, one thread per token: tcgen05.ld 32 logits at a time,
 // running top-k in registers, optional fp32 logits store for parity checks.
+#include <cooperative_groups.h>
 #include <float.h>
 
 #include <mutex>
@@ -75,15 +76,16 @@ __device__ __forceinline__ void topk_insert(float (&bv)[K], int (&bi)[K], float 
   }
 }
 
+// One 128-token tile of the gate: TMA + tcgen05 logits, top-K epilogue on all
+// 8 warps, idx / w written to global; with s_e/s_w the tile's routing is also
+// left in shared memory (slot t*k+j of the tile) for a fused dispatch.
+// Ends with a block barrier and the TMEM released.
 template <int K>
-__global__ void __launch_bounds__(256, 1)
-    gate_topk_kernel(const __grid_constant__ CUtensorMap tmX,
-                     const __grid_constant__ CUtensorMap tmWg, GateArgs a) {
+__device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensorMap& tmWg,
+                                          const GateArgs& a, uint8_t* smem, int* s_e,
+                                          float* s_w) {
   const GateLayout L = gate_layout(a.E);
   const int stage_bytes = kABytes + L.b_rows * kBlockK * 2;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.stages * stage_bytes);
   uint64_t* empty = full + L.stages;
   uint64_t* tfull = empty + L.stages;
@@ -115,6 +117,8 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // X and the routing buffers belong to the previous kernel until here
 
   if (warp == 0) {
     if (lane == 0) {
@@ -255,6 +259,10 @@ __global__ void __launch_bounds__(256, 1)
         acc += wj;
         a.idx[static_cast<size_t>(tok) * k + j] = bi[j];
         a.w[static_cast<size_t>(tok) * k + j] = wj;
+        if (s_e) {
+          s_e[tl * k + j] = bi[j];
+          s_w[tl * k + j] = wj;
+        }
       }
     }
   }
@@ -270,6 +278,229 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+__device__ __forceinline__ uint8_t* aligned_smem() {
+  extern __shared__ uint8_t smem_raw[];
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                    ~static_cast<uintptr_t>(1023));
+}
+
+template <int K>
+__global__ void __launch_bounds__(256, 1)
+    gate_topk_kernel(const __grid_constant__ CUtensorMap tmX,
+                     const __grid_constant__ CUtensorMap tmWg, GateArgs a) {
+  gate_tile<K>(tmX, tmWg, a, aligned_smem(), nullptr, nullptr);
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// peers holding the same key (one ballot per key bit; see route.cu)
+__device__ __forceinline__ uint32_t match_key(int key, int nbits) {
+  uint32_t m = __ballot_sync(0xffffffffu, key >= 0);
+  for (int bit = 0; bit < nbits; ++bit) {
+    const bool set = (key >> bit) & 1;
+    const uint32_t bm = __ballot_sync(0xffffffffu, set);
+    m &= set ? bm : ~bm;
+  }
+  return m;
+}
+
+// Exclusive scan of v[0..n) by the block (256 threads); returns the total.
+__device__ int scan_block(int* v, int n, int* scratch) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int lo = min(n, tid * per), hi = min(n, lo + per);
+  int s = 0;
+  for (int i = lo; i < hi; ++i) s += v[i];
+  int x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) scratch[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < nwarps ? scratch[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    scratch[lane] = w;
+  }
+  __syncthreads();
+  int run = (warp > 0 ? scratch[warp - 1] : 0) + x - s;
+  for (int i = lo; i < hi; ++i) {
+    const int t = v[i];
+    v[i] = run;
+    run += t;
+  }
+  const int total = scratch[nwarps - 1];
+  __syncthreads();
+  return total;
+}
+
+// Gate + dynamic dispatch + gather in one cooperative launch (one CTA per
+// 128-token tile, all resident): after the gate tile the CTA histograms its
+// 128*k slots, a grid barrier publishes every tile's histogram, each CTA
+// derives the global splits and its own stable bases (tiles in token order,
+// warps in slot order, ballot-ranked lanes -- the route kernel's order,
+// bit-exact to dynamic_dispatch, gating.cpp:58-86), scatters order/pos/wpos
+// and copies its tokens' rows into the expert-grouped Xp.  Saves the route
+// and gather launches and their HBM round trips of idx/order.
+template <int K>
+__global__ void __launch_bounds__(256, 1)
+    gate_dispatch_kernel(const __grid_constant__ CUtensorMap tmX,
+                         const __grid_constant__ CUtensorMap tmWg, GateArgs a, DispatchArgs d) {
+  namespace cg = cooperative_groups;
+  uint8_t* smem = aligned_smem();
+  const int k = a.k, E = a.E;
+  int* s_e = reinterpret_cast<int*>(smem + 8192);
+  float* s_w = reinterpret_cast<float*>(smem + 8192 + 4096);
+  gate_tile<K>(tmX, tmWg, a, smem, s_e, s_w);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x, nb = gridDim.x;
+  const int nb4 = (nb + 3) & ~3;
+  const int tok0 = b * kBlockM;
+  const int nslots = min(kBlockM, a.S - tok0) * k;  // slots of this tile
+  // smem after the gate: [0,8K) merge area | s_e | s_w | s_row (4 KB each) | counts
+  int* s_row = reinterpret_cast<int*>(smem + 16384);     // [128 * k] row of each slot
+  int* warp_cnt = reinterpret_cast<int*>(smem + 20480);  // [8][E]
+  int* tot = warp_cnt + 8 * E;                             // [E]
+  int* before = tot + E;                                   // [E]
+  int* scratch = before + E;                               // [33]
+  const int nbits = 32 - __clz(max(E - 1, 1));
+  const int per_warp = (((kBlockM * k + 7) / 8) + 31) & ~31;
+  const int w_lo = warp * per_warp, w_hi = min(nslots, w_lo + per_warp);
+  int* my_cnt = warp_cnt + warp * E;
+
+  // local histogram, per warp
+  for (int i = threadIdx.x; i < 8 * E; i += blockDim.x) warp_cnt[i] = 0;
+  __syncthreads();
+  for (int base = w_lo; base < w_hi; base += 32) {
+    const int e = base + lane < w_hi ? s_e[base + lane] : -1;
+    const uint32_t peers = match_key(e, nbits);
+    if (e >= 0 && (peers & lanemask_lt()) == 0) my_cnt[e] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  if (b == 0)
+    for (int i = threadIdx.x; i < E * (nb4 - nb); i += blockDim.x)
+      d.block_hist[(size_t)(i / (nb4 - nb)) * nb4 + nb + i % (nb4 - nb)] = 0;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int s = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += warp_cnt[w * E + e];
+    d.block_hist[(size_t)e * nb4 + b] = s;
+  }
+  cg::this_grid().sync();
+
+  // global splits and this tile's bases
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const int4* row = reinterpret_cast<const int4*>(d.block_hist + (size_t)e * nb4);
+    int s = 0, bf = 0;
+#pragma unroll 4
+    for (int j4 = 0; j4 < nb4 / 4; ++j4) {
+      const int4 x = row[j4];
+      const int j = 4 * j4;
+      s += x.x + x.y + x.z + x.w;
+      bf += (j < b ? x.x : 0) + (j + 1 < b ? x.y : 0) + (j + 2 < b ? x.z : 0) +
+            (j + 3 < b ? x.w : 0);
+    }
+    tot[e] = s;
+    before[e] = bf;
+  }
+  __syncthreads();
+  if (b == 0)
+    for (int e = threadIdx.x; e < E; e += blockDim.x) d.counts[e] = tot[e];
+  const int grand = scan_block(tot, E, scratch);  // tot -> splits
+  if (b == 0) {
+    for (int e = threadIdx.x; e < E; e += blockDim.x) d.splits[e] = tot[e];
+    if (threadIdx.x == 0) d.splits[E] = grand;
+  }
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int run = tot[e] + before[e];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const int x = warp_cnt[w * E + e];
+      warp_cnt[w * E + e] = run;
+      run += x;
+    }
+  }
+  __syncthreads();
+
+  // stable scatter of this tile's slots; remember each slot's row for the gather
+  for (int base = w_lo; base < w_hi; base += 32) {
+    const int sl = base + lane;
+    const int e = sl < w_hi ? s_e[sl] : -1;
+    const uint32_t peers = match_key(e, nbits);
+    if (e >= 0) {
+      const int p = my_cnt[e] + __popc(peers & lanemask_lt());
+      const int slot = tok0 * k + sl;
+      d.order[p] = slot;
+      d.pos[slot] = p;
+      d.wpos[p] = s_w[sl];
+      s_row[sl] = p;
+    }
+    __syncwarp();
+    if (e >= 0 && (peers & lanemask_lt()) == 0) my_cnt[e] += __popc(peers);
+    __syncwarp();
+  }
+
+  // FFN work items (block 0)
+  if (b == 0) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < E; e += blockDim.x)
+      before[e] = (d.counts[e] + d.tile_n - 1) / d.tile_n;
+    __syncthreads();
+    const int n_items = scan_block(before, E, scratch);
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+      const int rows = d.counts[e];
+      int it = before[e];
+      for (int c = 0; c < rows; c += d.tile_n, ++it) {
+        FfnItem item;
+        item.expert = e;
+        item.row0 = tot[e] + c;
+        item.len = min(d.tile_n, rows - c);
+        item.pad = 0;
+        d.items[it] = item;
+      }
+      if (d.item_off) d.item_off[e] = before[e];
+    }
+    if (threadIdx.x == 0) {
+      *d.n_items = n_items;
+      if (d.item_off) d.item_off[E] = n_items;
+    }
+  }
+  __syncthreads();
+
+  // gather: token rows of this tile -> their expert-grouped rows of Xp
+  const int vec = a.TD / 8;  // uint4 per row
+  const uint4* X = reinterpret_cast<const uint4*>(d.X);
+  uint4* Xp = reinterpret_cast<uint4*>(d.Xp);
+  // each warp moves two rows at a time with 4 independent 16-byte loads in
+  // flight per lane per row
+  for (int sl = warp; sl < nslots; sl += 8) {
+    const uint4* src = X + (size_t)(tok0 + sl / k) * vec;
+    uint4* dst = Xp + (size_t)s_row[sl] * vec;
+    int v = lane;
+    for (; v + 96 < vec; v += 128) {
+      const uint4 r0 = __ldg(src + v), r1 = __ldg(src + v + 32), r2 = __ldg(src + v + 64),
+                  r3 = __ldg(src + v + 96);
+      dst[v] = r0;
+      dst[v + 32] = r1;
+      dst[v + 64] = r2;
+      dst[v + 96] = r3;
+    }
+    for (; v < vec; v += 32) dst[v] = __ldg(src + v);
+  }
+}
+
 }  // namespace
 
 int gate_box_rows(int E) { return gate_layout(E).box_rows; }
@@ -281,7 +512,15 @@ cudaError_t gate_prepare(int E) {
   const GateLayout L = gate_layout(E);
   std::lock_guard<std::mutex> lock(mu);
   if (L.smem <= granted) return cudaSuccess;
-  for (auto fn : {gate_topk_kernel<1>, gate_topk_kernel<2>, gate_topk_kernel<4>, gate_topk_kernel<8>}) {
+  const void* fns[] = {reinterpret_cast<const void*>(gate_topk_kernel<1>),
+                       reinterpret_cast<const void*>(gate_topk_kernel<2>),
+                       reinterpret_cast<const void*>(gate_topk_kernel<4>),
+                       reinterpret_cast<const void*>(gate_topk_kernel<8>),
+                       reinterpret_cast<const void*>(gate_dispatch_kernel<1>),
+                       reinterpret_cast<const void*>(gate_dispatch_kernel<2>),
+                       reinterpret_cast<const void*>(gate_dispatch_kernel<4>),
+                       reinterpret_cast<const void*>(gate_dispatch_kernel<8>)};
+  for (const void* fn : fns) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem);
     if (e != cudaSuccess) return e;
   }
@@ -295,11 +534,45 @@ cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const G
     return cudaErrorInvalidValue;
   const GateLayout L = gate_layout(a.E);
   const int grid = (a.S + kBlockM - 1) / kBlockM;
-  if (a.k == 1) gate_topk_kernel<1><<<grid, 256, L.smem, stream>>>(tmX, tmWg, a);
-  else if (a.k == 2) gate_topk_kernel<2><<<grid, 256, L.smem, stream>>>(tmX, tmWg, a);
-  else if (a.k <= 4) gate_topk_kernel<4><<<grid, 256, L.smem, stream>>>(tmX, tmWg, a);
-  else gate_topk_kernel<8><<<grid, 256, L.smem, stream>>>(tmX, tmWg, a);
-  return cudaGetLastError();
+  auto kern = a.k == 1 ? gate_topk_kernel<1>
+              : a.k == 2 ? gate_topk_kernel<2>
+              : a.k <= 4 ? gate_topk_kernel<4> : gate_topk_kernel<8>;
+  return launch_chain(kern, dim3(grid), dim3(256), L.smem, stream, false, tmX, tmWg, a);
+}
+
+}  // namespace moe
+
+namespace moe {
+
+// Smem the fused kernel needs beyond the gate stages: merge area + tile
+// routing (16 KB) + per-warp histograms and scans.
+bool gate_dispatch_supported(int S, int E, int k, int TD, int sms) {
+  const GateLayout L = gate_layout(E);
+  const int tiles = (S + kBlockM - 1) / kBlockM;
+  const size_t need = 20480 + sizeof(int) * (10 * (size_t)E + 64);
+  return tiles <= sms && need <= (size_t)L.stages * (kABytes + L.b_rows * kBlockK * 2) &&
+         k * kBlockM <= 1024 && TD % 8 == 0;
+}
+
+cudaError_t launch_gate_dispatch(const CUtensorMap& tmX, const CUtensorMap& tmWg,
+                                 const GateArgs& a, const DispatchArgs& d, cudaStream_t stream) {
+  if (a.k < 1 || a.k > kMaxK || a.E > 512 || a.E < a.k || (a.TD % kBlockK) != 0)
+    return cudaErrorInvalidValue;
+  const GateLayout L = gate_layout(a.E);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((a.S + kBlockM - 1) / kBlockM);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = L.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (a.k == 1) return cudaLaunchKernelEx(&cfg, gate_dispatch_kernel<1>, tmX, tmWg, a, d);
+  if (a.k == 2) return cudaLaunchKernelEx(&cfg, gate_dispatch_kernel<2>, tmX, tmWg, a, d);
+  if (a.k <= 4) return cudaLaunchKernelEx(&cfg, gate_dispatch_kernel<4>, tmX, tmWg, a, d);
+  return cudaLaunchKernelEx(&cfg, gate_dispatch_kernel<8>, tmX, tmWg, a, d);
 }
 
 }  // namespace moe

@@ -6,7 +6,57 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+#include <utility>
+
 namespace moe {
+
+// ---- programmatic dependent launch (PDL)
+// Kernels of the layer chain are launched with programmatic stream
+// serialization: the next kernel's CTAs are scheduled while the previous one
+// drains, run their prologue (barrier init, TMEM alloc, descriptor prefetch)
+// and block in griddepcontrol.wait until the previous grid has completed and
+// its memory is visible.  MOE_PDL=0 disables it (A/B).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("MOE_PDL");
+    return !v || atoi(v) != 0;
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_chain(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                cudaStream_t stream, bool cooperative, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (cooperative) {
+    attr[n].id = cudaLaunchAttributeCooperative;
+    attr[n].val.cooperative = 1;
+    ++n;
+  } else if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+#ifdef __CUDACC__
+// wait for the previous kernel of the stream (no-op without PDL)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// allow the next kernel of the stream to be scheduled early
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#endif
 
 // One unit of grouped-FFN work: `len` (<= tile_n) consecutive rows of the
 // expert-grouped activation matrix, all routed to `expert`.
@@ -106,6 +156,24 @@ struct GateArgs {
   float* w;         // [S*k]
   float* logits;    // optional [S*E]
 };
+// Gate + dynamic dispatch + gather in one cooperative launch (gate.cu).
+struct DispatchArgs {
+  const void* X;       // [S, TD] bf16 (the gate's input)
+  void* Xp;            // [kS, TD] bf16, expert-grouped rows
+  int32_t* counts;     // [E]
+  int32_t* splits;     // [E+1]
+  int32_t* order;      // [kS]
+  int32_t* pos;        // [kS]
+  float* wpos;         // [kS]
+  int32_t* block_hist; // scratch [E * (tiles + 4)]
+  FfnItem* items;
+  int32_t* n_items;
+  int32_t* item_off;   // optional [E+1]
+  int tile_n;
+};
+bool gate_dispatch_supported(int S, int E, int k, int TD, int sms);
+cudaError_t launch_gate_dispatch(const CUtensorMap& tmX, const CUtensorMap& tmWg,
+                                 const GateArgs& a, const DispatchArgs& d, cudaStream_t stream);
 cudaError_t gate_prepare(int E);
 cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateArgs& a,
                         cudaStream_t stream);

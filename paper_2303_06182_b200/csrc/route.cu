@@ -132,6 +132,8 @@ __device__ __forceinline__ void load_keys(const RouteArgs& a, int base0, int hi,
 template <bool kSingle>
 __global__ void __launch_bounds__(kSingle ? kSingleThreads : kMultiThreads)
     route_kernel(RouteArgs a) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int kWarps = (kSingle ? kSingleThreads : kMultiThreads) / 32;
   extern __shared__ int smem[];
   __shared__ int warp_off[kWarps];
@@ -369,8 +371,8 @@ cudaError_t launch_route(RouteArgs a, int max_blocks, cudaStream_t stream) {
   if (total <= kSingleMaxSlots && single_smem <= 200 * 1024) {
     a.chunk = (total + kSingleThreads - 1) / kSingleThreads * kSingleThreads;
     if (a.chunk == 0) a.chunk = kSingleThreads;
-    route_kernel<true><<<1, kSingleThreads, single_smem, stream>>>(a);
-    return cudaGetLastError();
+    return launch_chain(route_kernel<true>, dim3(1), dim3(kSingleThreads), single_smem, stream,
+                        false, a);
   }
   const int unit = kMultiThreads;  // 32 slots per warp per step
   static const int chunk_units = [] {

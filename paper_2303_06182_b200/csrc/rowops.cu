@@ -21,6 +21,8 @@ namespace {
 __global__ void __launch_bounds__(256)
     gather_rows_kernel(const uint4* __restrict__ X, const int32_t* __restrict__ order, int rows,
                        int k, int vec_per_row, uint4* __restrict__ Xp) {
+  pdl_trigger();
+  pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -58,6 +60,8 @@ __device__ __forceinline__ void add_bf16x8(float (&acc)[8], const uint4& v) {
 __global__ void __launch_bounds__(256)
     combine_kernel(const uint4* __restrict__ Yw, const int32_t* __restrict__ pos, int S, int k,
                    int vec_per_row, uint4* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -103,6 +107,8 @@ __global__ void fill_uniform_bf16_kernel(__nv_bfloat16* dst, int64_t n, uint64_t
 // given lengths (one warp per segment).
 __global__ void fill_segments_kernel(const int32_t* __restrict__ counts, int n, int mod,
                                      int32_t* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   // exclusive offsets recomputed per segment: n is small (D * E_local)
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -138,17 +144,17 @@ int sm_count() {
 cudaError_t launch_gather_rows(const __nv_bfloat16* X, const int32_t* order, int rows, int k,
                                int TD, __nv_bfloat16* Xp, cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
-  gather_rows_kernel<<<grid_for(rows, sm_count()), 256, 0, stream>>>(
-      reinterpret_cast<const uint4*>(X), order, rows, k, TD / 8, reinterpret_cast<uint4*>(Xp));
-  return cudaGetLastError();
+  return launch_chain(gather_rows_kernel, dim3(grid_for(rows, sm_count())), dim3(256), 0, stream,
+                      false, reinterpret_cast<const uint4*>(X), order, rows, k, TD / 8,
+                      reinterpret_cast<uint4*>(Xp));
 }
 
 cudaError_t launch_combine(const __nv_bfloat16* Yw, const int32_t* pos, int S, int k, int TD,
                            __nv_bfloat16* out, cudaStream_t stream) {
   if (S <= 0) return cudaSuccess;
-  combine_kernel<<<grid_for(S, sm_count()), 256, 0, stream>>>(
-      reinterpret_cast<const uint4*>(Yw), pos, S, k, TD / 8, reinterpret_cast<uint4*>(out));
-  return cudaGetLastError();
+  return launch_chain(combine_kernel, dim3(grid_for(S, sm_count())), dim3(256), 0, stream, false,
+                      reinterpret_cast<const uint4*>(Yw), pos, S, k, TD / 8,
+                      reinterpret_cast<uint4*>(out));
 }
 
 cudaError_t launch_fill_segments(const int32_t* counts, int n_segments, int mod, int32_t* out,

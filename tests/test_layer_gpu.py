@@ -192,8 +192,8 @@ def test_static_mode_matches_oracle(S, TD, HD, E, k, C):
     assert err < TOL_OUT
 
 
-def test_graph_and_host_paths_bitwise_equal_to_eager():
-    S, TD, HD, E, k = 1024, 256, 512, 16, 2
+@pytest.mark.parametrize("S,TD,HD,E,k", [(1024, 256, 512, 16, 2), (16384, 1024, 4096, 512, 2)])
+def test_graph_and_host_paths_bitwise_equal_to_eager(S, TD, HD, E, k):
     shape = LayerShape(TD, HD, E, k)
     w = make_weights(shape, seed=SEED)
     layer = MoeLayer(shape, S, weights=w)
@@ -258,3 +258,24 @@ def test_fused_ffn_bitwise_equal_two_launch_ffn(S, TD, HD, E, k, mode, C):
     fused.check_errors()
     assert torch.equal(a, b)
     assert torch.equal(a, a2)
+
+
+@pytest.mark.parametrize("S,TD,HD,E,k", [(300, 256, 512, 8, 2), (2048, 1024, 4096, 8, 1), (257, 128, 256, 33, 3),
+                                         (16384, 1024, 4096, 512, 2), (6144, 2048, 8192, 128, 2),
+                                         (18944, 256, 256, 64, 2)])
+def test_fused_gate_dispatch_matches_three_launches(S, TD, HD, E, k):
+    """Gate + dispatch + gather in one cooperative launch == gate, route and
+    gather kernels: identical routing arrays, Xp rows and layer output."""
+    shape = LayerShape(TD, HD, E, k)
+    w = make_weights(shape, seed=SEED)
+    x = make_tokens(S, TD, seed=SEED)
+    fused = MoeLayer(shape, S, weights=w, split_ffn=True, fuse_front=True)
+    split = MoeLayer(shape, S, weights=w, split_ffn=True)
+    a = fused(x)
+    b = split(x)
+    torch.cuda.synchronize()
+    fused.check_errors()
+    va, vb = fused.view(), split.view()
+    for key in ("idx", "w", "counts", "splits", "order", "pos", "n_items", "xp"):
+        assert torch.equal(va[key], vb[key]), key
+    assert torch.equal(a, b)
