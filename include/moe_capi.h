@@ -79,6 +79,19 @@ int moe_ctx_destroy(moe_ctx* ctx);
 /* Number of SMs of the context's device. */
 int moe_ctx_sm_count(const moe_ctx* ctx);
 
+/* Device memory, pinned host memory, copies and streams for C/C++ hosts that
+ * do not link the CUDA runtime themselves (the C++ layer API,
+ * include/moesim/gpu_layer.hpp).  kind: 0 host->device, 1 device->host,
+ * 2 device->device.  stream NULL = legacy default stream. */
+int moe_device_alloc(moe_ctx* ctx, size_t bytes, void** out);
+int moe_device_free(moe_ctx* ctx, void* ptr);
+int moe_host_alloc(moe_ctx* ctx, size_t bytes, void** out); /* pinned */
+int moe_host_free(moe_ctx* ctx, void* ptr);
+int moe_memcpy(moe_ctx* ctx, void* dst, const void* src, size_t bytes, int kind, void* stream);
+int moe_stream_create(moe_ctx* ctx, void** out);
+int moe_stream_destroy(moe_ctx* ctx, void* stream);
+int moe_stream_synchronize(moe_ctx* ctx, void* stream);
+
 /* ---------------------------------------------------------------- routing */
 
 /* gating.cpp:22-28.  Pure host arithmetic; returns the capacity (>= 0). */

@@ -34,6 +34,8 @@ EXPORTED = [
     "moe_ffn_create", "moe_ffn_destroy", "moe_ffn_forward", "moe_route_dynamic_keyed",
     "moe_fill_segments", "moe_cache_create", "moe_cache_destroy", "moe_cache_forward",
     "moe_cache_forward_routed", "moe_cache_stats", "moe_cache_resident", "moe_layer_forward_routed",
+    "moe_device_alloc", "moe_device_free", "moe_host_alloc", "moe_host_free", "moe_memcpy",
+    "moe_stream_create", "moe_stream_destroy", "moe_stream_synchronize",
 ]
 
 

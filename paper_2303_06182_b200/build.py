@@ -65,9 +65,29 @@ def build_cxx(force: bool = False) -> str:
     return LIBCXX
 
 
+TOOLS = os.path.join(ROOT, "tools")
+BIN = os.path.join(ROOT, "build", "bin")
+
+
+def build_tools(force: bool = False) -> None:
+    """C++ host programs on the C++ API (no CUDA runtime linked directly)."""
+    os.makedirs(BIN, exist_ok=True)
+    for name in ("moesim_measure",):
+        src = os.path.join(TOOLS, name + ".cpp")
+        exe = os.path.join(BIN, name)
+        deps = [src, LIB, LIBCXX] + glob.glob(os.path.join(INCLUDE, "moesim", "*.hpp")) + [
+            os.path.join(INCLUDE, "moe_capi.h")]
+        if not force and not _stale(exe, deps):
+            continue
+        _run(["g++", "-std=c++20", "-O2", "-Wall", "-Wextra", f"-I{INCLUDE}", f"-I{EIGEN_MIN}", "-o", exe,
+              src, f"-L{HERE}", "-lmoesim_b200", "-lmoe_b200",
+              "-Wl,-rpath,$ORIGIN/../../paper_2303_06182_b200"])
+
+
 def build_all(force: bool = False) -> None:
     build_cuda(force)
     build_cxx(force)
+    build_tools(force)
 
 
 if __name__ == "__main__":

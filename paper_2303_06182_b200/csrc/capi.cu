@@ -91,6 +91,64 @@ int moe_ctx_destroy(moe_ctx* ctx) {
 
 int moe_ctx_sm_count(const moe_ctx* ctx) { return ctx ? ctx->sms : 0; }
 
+int moe_device_alloc(moe_ctx* ctx, size_t bytes, void** out) {
+  if (!ctx || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  MOE_CUDA(cudaSetDevice(ctx->device));
+  cudaError_t e = cudaMalloc(out, bytes ? bytes : 1);
+  if (e != cudaSuccess) return fail(MOE_ERR_OUT_OF_MEMORY, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  return MOE_OK;
+}
+
+int moe_device_free(moe_ctx* ctx, void* ptr) {
+  if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
+  MOE_CUDA(cudaFree(ptr));
+  return MOE_OK;
+}
+
+int moe_host_alloc(moe_ctx* ctx, size_t bytes, void** out) {
+  if (!ctx || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  cudaError_t e = cudaMallocHost(out, bytes ? bytes : 1);
+  if (e != cudaSuccess) return fail(MOE_ERR_OUT_OF_MEMORY, std::string("cudaMallocHost: ") + cudaGetErrorString(e));
+  return MOE_OK;
+}
+
+int moe_host_free(moe_ctx* ctx, void* ptr) {
+  if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
+  MOE_CUDA(cudaFreeHost(ptr));
+  return MOE_OK;
+}
+
+int moe_memcpy(moe_ctx* ctx, void* dst, const void* src, size_t bytes, int kind, void* stream) {
+  if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
+  const cudaMemcpyKind k = kind == 0   ? cudaMemcpyHostToDevice
+                           : kind == 1 ? cudaMemcpyDeviceToHost
+                                       : cudaMemcpyDeviceToDevice;
+  if (kind < 0 || kind > 2) return fail(MOE_ERR_INVALID_ARGUMENT, "bad copy kind");
+  MOE_CUDA(cudaMemcpyAsync(dst, src, bytes, k, (cudaStream_t)stream));
+  return MOE_OK;
+}
+
+int moe_stream_create(moe_ctx* ctx, void** out) {
+  if (!ctx || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  MOE_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s;
+  MOE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  *out = s;
+  return MOE_OK;
+}
+
+int moe_stream_destroy(moe_ctx* ctx, void* stream) {
+  if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
+  MOE_CUDA(cudaStreamDestroy((cudaStream_t)stream));
+  return MOE_OK;
+}
+
+int moe_stream_synchronize(moe_ctx* ctx, void* stream) {
+  if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
+  MOE_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  return MOE_OK;
+}
+
 int moe_expert_capacity(double capacity_factor, int seq_len) {
   // gating.cpp:22-28
   const double raw = capacity_factor * seq_len;
