@@ -858,11 +858,13 @@ int moe_ffn_create(moe_ctx* ctx, const moe_ffn_desc* desc, const void* W1, const
   }
   const size_t R = d.max_rows, Rp = R + 256, TD = d.token_dim, HD = d.hidden_dim;
   const size_t items_max = R / F->tile_n + d.num_experts + 1;
+  F->items_max = (int)items_max;
   int st;
   if ((st = F->counts.reserve(d.num_experts)) || (st = F->splits.reserve(d.num_experts + 1)) ||
       (st = F->order.reserve(R)) || (st = F->pos.reserve(R)) || (st = F->n_items.reserve(1)) ||
       (st = F->wpos.reserve(R)) || (st = F->ones.reserve(R)) ||
       (st = F->items.reserve(items_max)) || (st = F->xp.reserve(Rp * TD)) ||
+      (st = F->done.reserve(2 * items_max)) ||
       (st = F->h.reserve(Rp * HD)) || (st = ctx->prepare_route(d.num_experts))) {
     moe_ffn_destroy(F);
     return st;
@@ -891,6 +893,7 @@ int moe_ffn_destroy(moe_ffn* F) {
   F->order.release();
   F->pos.release();
   F->n_items.release();
+  F->done.release();
   F->wpos.release();
   F->ones.release();
   F->items.release();
@@ -914,6 +917,28 @@ int moe_ffn_forward(moe_ffn* F, const void* X_rows, const int32_t* keys, const f
   cudaError_t e = launch_gather_rows((const __nv_bfloat16*)X_rows, F->order.p, rows, 1, TD,
                                      F->xp.p, s);
   if (e != cudaSuccess) return cuda_fail(e, "gather launch");
+  if (F->tile_n == 128) {
+    // weight-streaming regime: one persistent launch, H kept in L2, the
+    // output rows written straight back to the received order
+    MOE_CUDA(cudaMemsetAsync(F->done.p, 0, sizeof(int32_t) * 2 * (size_t)F->items_max, s));
+    FusedFfnArgs fa{};
+    fa.items = F->items.p;
+    fa.n_items = F->n_items.p;
+    fa.TD = TD;
+    fa.HD = HD;
+    fa.H = F->h.p;
+    fa.Yw = (__nv_bfloat16*)Y_rows;
+    fa.out_rows = F->order.p;
+    fa.wpos = F->wpos.p;
+    fa.done1 = F->done.p;
+    fa.done2 = F->done.p + F->items_max;
+    const int per_item = HD / 128 + TD / 128;
+    fa.lag = std::max(2, (8 * F->ctx->sms + per_item - 1) / per_item);
+    fa.discard_h = 1;
+    e = launch_fused_ffn(F->tmW1, F->tmXp, F->tmW2, F->tmH, fa, F->tile_n, F->ctx->sms, s);
+    if (e != cudaSuccess) return cuda_fail(e, "fused ffn launch");
+    return MOE_OK;
+  }
   GemmArgs g1{F->items.p, F->n_items.p, nullptr, HD, TD, kEpiReluBf16, F->h.p, nullptr, nullptr};
   e = launch_grouped_gemm(F->tmW1, F->tmXp, g1, F->tile_n, F->ctx->sms, s);
   if (e != cudaSuccess) return cuda_fail(e, "grouped gemm 1 launch");

@@ -180,8 +180,9 @@ struct moe_ffn {
   moe_ctx* ctx = nullptr;
   moe_ffn_desc d{};
   int tile_n = 128;
+  int items_max = 0;
   CUtensorMap tmW1, tmW2, tmXp, tmH;
-  DevBuf<int32_t> counts, splits, order, pos, n_items;
+  DevBuf<int32_t> counts, splits, order, pos, n_items, done;
   DevBuf<float> wpos, ones;
   DevBuf<FfnItem> items;
   DevBuf<__nv_bfloat16> xp, h;

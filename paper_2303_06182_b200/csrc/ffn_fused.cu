@@ -248,8 +248,9 @@ __global__ void __launch_bounds__(256, 1)
           const int ch = lane & 3;
           if (c0 + tok < it.len) {
             const uint4 v = *reinterpret_cast<const uint4*>(stg + tok * 32 + ch * 8);
-            *reinterpret_cast<uint4*>(out + static_cast<size_t>(it.row0 + c0 + tok) * m_total +
-                                      col0 + ch * 8) = v;
+            int row = it.row0 + c0 + tok;
+            if (tr.gemm && g.out_rows) row = g.out_rows[row];
+            *reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * m_total + col0 + ch * 8) = v;
           }
         }
         __syncwarp();

@@ -132,6 +132,7 @@ struct FusedFfnArgs {
   int TD, HD;
   __nv_bfloat16* H;         // [rows, HD]
   __nv_bfloat16* Yw;        // [rows, TD]
+  const int32_t* out_rows;  // optional: GEMM2 row r is written to Yw row out_rows[r]
   const float* wpos;        // gate weight per row
   int32_t* done1;           // [items] GEMM1 tiles stored (zeroed before launch)
   int32_t* done2;           // [items] GEMM2 tiles finished (zeroed before launch)
