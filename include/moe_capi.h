@@ -194,6 +194,17 @@ int moe_layer_forward_graph(moe_layer* layer, const void* X, int S, void* out, v
 int moe_layer_forward_host(moe_layer* layer, const void* X_host, int S, void* out_host,
                            void* stream);
 
+/* End-to-end host path over a stream of n independent batches (a serving
+ * queue): batch i's H2D copy, its forward (graph replay on `stream`) and its
+ * D2H copy run on three streams with double-buffered device staging, so batch
+ * i+1's upload and batch i-1's read-back overlap batch i's compute.  Every
+ * byte of every batch crosses PCIe; synchronous (returns when all out_host[i]
+ * are written).  Output of batch i is bitwise equal to
+ * moe_layer_forward_host(X_host[i]).  Host buffers should be pinned; `stream`
+ * must be non-default. */
+int moe_layer_forward_host_batches(moe_layer* layer, const void* const* X_host, const int* S,
+                                   void* const* out_host, int n, void* stream);
+
 /* Per-stage CUDA-event timing of moe_layer_forward (eager path only).
  * Stages: 0 gate, 1 route, 2 gather, 3 FFN GEMM1, 4 FFN GEMM2, 5 combine.
  * enable: n_slots > 0 allocates a ring of n_slots event sets; call i records

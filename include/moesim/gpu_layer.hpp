@@ -170,6 +170,14 @@ class MoeLayer {
   void forward_host(const void* X_host, int S, void* out_host, void* stream = nullptr) {
     check(moe_layer_forward_host(h_, X_host, S, out_host, stream));
   }
+  // a queue of host batches, copies overlapped with neighbouring batches' compute
+  void forward_host_batches(const std::vector<const void*>& X_host, const std::vector<int>& S,
+                            const std::vector<void*>& out_host, void* stream) {
+    if (X_host.size() != S.size() || S.size() != out_host.size())
+      throw std::invalid_argument("one size and one output buffer per batch");
+    check(moe_layer_forward_host_batches(h_, X_host.data(), S.data(), out_host.data(),
+                                         static_cast<int>(S.size()), stream));
+  }
   void check_errors(void* stream = nullptr) { check(moe_check_errors(ctx_->get(), stream)); }
 
   void enable_timing(int slots) { check(moe_layer_enable_timing(h_, slots)); }

@@ -36,6 +36,7 @@ EXPORTED = [
     "moe_cache_forward_routed", "moe_cache_stats", "moe_cache_resident", "moe_layer_forward_routed",
     "moe_device_alloc", "moe_device_free", "moe_host_alloc", "moe_host_free", "moe_memcpy",
     "moe_stream_create", "moe_stream_destroy", "moe_stream_synchronize",
+    "moe_layer_forward_host_batches",
 ]
 
 
@@ -116,6 +117,7 @@ def load(path: str = LIB_PATH):
     _sig(lib.moe_layer_forward, I, P, P, I, P, P)
     _sig(lib.moe_layer_forward_graph, I, P, P, I, P, P)
     _sig(lib.moe_layer_forward_host, I, P, P, I, P, P)
+    _sig(lib.moe_layer_forward_host_batches, I, P, P, P, P, I, P)
     _sig(lib.moe_layer_get_view, I, P, C.POINTER(LayerView))
     _sig(lib.moe_layer_set_weight_pool, I, P, P, P, I, P)
     _sig(lib.moe_exchange_counts_host, I, P, P, I, I, I, P, I, P)

@@ -521,8 +521,17 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
 int moe_layer_destroy(moe_layer* L) {
   if (!L) return MOE_OK;
   cudaSetDevice(L->ctx->device);
-  if (L->gexec) cudaGraphExecDestroy(L->gexec);
+  L->drop_graphs();
   for (cudaEvent_t e : L->tev) cudaEventDestroy(e);
+  for (int b = 0; b < 2; ++b) {
+    if (L->ev_in[b]) cudaEventDestroy(L->ev_in[b]);
+    if (L->ev_comp[b]) cudaEventDestroy(L->ev_comp[b]);
+    if (L->ev_out[b]) cudaEventDestroy(L->ev_out[b]);
+    L->pin[b].release();
+    L->pout[b].release();
+  }
+  if (L->h2d) cudaStreamDestroy(L->h2d);
+  if (L->d2h) cudaStreamDestroy(L->d2h);
   L->idx.release();
   L->w.release();
   L->pos.release();
@@ -770,12 +779,16 @@ int moe_layer_stage_times(moe_layer* L, int slot, float* ms) {
 int moe_layer_forward_graph(moe_layer* L, const void* X, int S, void* out, void* stream) {
   if (!L || !X || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
-  if (!L->gexec || L->g_x != X || L->g_out != out || L->g_S != S || L->g_stream != s) {
-    if (L->gexec) {
-      cudaGraphExecDestroy(L->gexec);
-      L->gexec = nullptr;
-    }
+  moe_layer::GraphEntry* hit = nullptr;
+  for (moe_layer::GraphEntry& g : L->graphs)
+    if (g.exec && g.x == X && g.out == out && g.S == S && g.stream == s) hit = &g;
+  if (!hit) {
     if (s == nullptr) return fail(MOE_ERR_INVALID_ARGUMENT, "graph capture needs a non-default stream");
+    hit = &L->graphs[0];
+    for (moe_layer::GraphEntry& g : L->graphs)
+      if (g.used < hit->used) hit = &g;  // LRU (unused entries have used == 0)
+    if (hit->exec) cudaGraphExecDestroy(hit->exec);
+    *hit = moe_layer::GraphEntry{};
     MOE_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     int st = layer_forward_impl(L, X, S, out, s);
     cudaGraph_t graph = nullptr;
@@ -785,18 +798,19 @@ int moe_layer_forward_graph(moe_layer* L, const void* X, int S, void* out, void*
       return st;
     }
     if (e != cudaSuccess) return cuda_fail(e, "end capture");
-    e = cudaGraphInstantiate(&L->gexec, graph, 0);
+    e = cudaGraphInstantiate(&hit->exec, graph, 0);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) {
-      L->gexec = nullptr;
+      hit->exec = nullptr;
       return cuda_fail(e, "graph instantiate");
     }
-    L->g_x = X;
-    L->g_out = out;
-    L->g_S = S;
-    L->g_stream = s;
+    hit->x = X;
+    hit->out = out;
+    hit->S = S;
+    hit->stream = s;
   }
-  MOE_CUDA(cudaGraphLaunch(L->gexec, s));
+  hit->used = ++L->graph_clock;
+  MOE_CUDA(cudaGraphLaunch(hit->exec, s));
   return MOE_OK;
 }
 
@@ -811,6 +825,58 @@ int moe_layer_forward_host(moe_layer* L, const void* X_host, int S, void* out_ho
   st = layer_forward_impl(L, L->xin.p, S, L->yout.p, s);
   if (st) return st;
   MOE_CUDA(cudaMemcpyAsync(out_host, L->yout.p, nb, cudaMemcpyDeviceToHost, s));
+  MOE_CUDA(cudaStreamSynchronize(s));
+  return moe_check_errors(L->ctx, s);
+}
+
+int moe_layer_forward_host_batches(moe_layer* L, const void* const* X_host, const int* S,
+                                   void* const* out_host, int n, void* stream) {
+  if (!L || n < 0 || (n > 0 && (!X_host || !S || !out_host)))
+    return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (!stream) return fail(MOE_ERR_INVALID_ARGUMENT, "pipelined forward needs a non-default stream");
+  for (int i = 0; i < n; ++i) {
+    if (!X_host[i] || !out_host[i]) return fail(MOE_ERR_INVALID_ARGUMENT, "null batch buffer");
+    if (S[i] < 1 || S[i] > L->d.max_tokens)
+      return fail(MOE_ERR_INVALID_ARGUMENT, "batch size outside [1, max_tokens]");
+  }
+  cudaSetDevice(L->ctx->device);
+  const size_t elems = (size_t)L->d.max_tokens * L->d.token_dim;
+  int st;
+  for (int b = 0; b < 2; ++b)
+    if ((st = L->pin[b].reserve(elems)) || (st = L->pout[b].reserve(elems))) return st;
+  if (!L->h2d) {
+    MOE_CUDA(cudaStreamCreateWithFlags(&L->h2d, cudaStreamNonBlocking));
+    MOE_CUDA(cudaStreamCreateWithFlags(&L->d2h, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      MOE_CUDA(cudaEventCreateWithFlags(&L->ev_in[b], cudaEventDisableTiming));
+      MOE_CUDA(cudaEventCreateWithFlags(&L->ev_comp[b], cudaEventDisableTiming));
+      MOE_CUDA(cudaEventCreateWithFlags(&L->ev_out[b], cudaEventDisableTiming));
+    }
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  // the copy streams start after whatever the caller queued on `stream`
+  MOE_CUDA(cudaEventRecord(L->ev_comp[0], s));
+  MOE_CUDA(cudaStreamWaitEvent(L->h2d, L->ev_comp[0], 0));
+  MOE_CUDA(cudaStreamWaitEvent(L->d2h, L->ev_comp[0], 0));
+  MOE_CUDA(cudaEventRecord(L->ev_comp[1], s));
+  for (int i = 0; i < n; ++i) {
+    const int b = i & 1;
+    const size_t nb = (size_t)S[i] * L->d.token_dim * 2;
+    // batch i's input lands in pin[b] once batch i-2's compute has consumed it
+    MOE_CUDA(cudaStreamWaitEvent(L->h2d, L->ev_comp[b], 0));
+    MOE_CUDA(cudaMemcpyAsync(L->pin[b].p, X_host[i], nb, cudaMemcpyHostToDevice, L->h2d));
+    MOE_CUDA(cudaEventRecord(L->ev_in[b], L->h2d));
+    // compute waits for its input and for batch i-2's read-back of pout[b]
+    MOE_CUDA(cudaStreamWaitEvent(s, L->ev_in[b], 0));
+    if (i >= 2) MOE_CUDA(cudaStreamWaitEvent(s, L->ev_out[b], 0));
+    if ((st = moe_layer_forward_graph(L, L->pin[b].p, S[i], L->pout[b].p, s))) return st;
+    MOE_CUDA(cudaEventRecord(L->ev_comp[b], s));
+    MOE_CUDA(cudaStreamWaitEvent(L->d2h, L->ev_comp[b], 0));
+    MOE_CUDA(cudaMemcpyAsync(out_host[i], L->pout[b].p, nb, cudaMemcpyDeviceToHost, L->d2h));
+    MOE_CUDA(cudaEventRecord(L->ev_out[b], L->d2h));
+  }
+  MOE_CUDA(cudaStreamSynchronize(L->h2d));
+  MOE_CUDA(cudaStreamSynchronize(L->d2h));
   MOE_CUDA(cudaStreamSynchronize(s));
   return moe_check_errors(L->ctx, s);
 }
@@ -987,10 +1053,7 @@ int moe_layer_set_weight_pool(moe_layer* L, const void* W1_pool, const void* W2_
       return st;
     L->slot_of = slot_of;
   }
-  if (L->gexec) {
-    cudaGraphExecDestroy(L->gexec);
-    L->gexec = nullptr;
-  }
+  L->drop_graphs();
   return MOE_OK;
 }
 

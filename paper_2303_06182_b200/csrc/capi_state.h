@@ -168,12 +168,28 @@ struct moe_layer {
   std::vector<cudaEvent_t> tev;
   int t_slots = 0;
   long t_calls = 0;
-  // graph cache
-  cudaGraphExec_t gexec = nullptr;
-  const void* g_x = nullptr;
-  void* g_out = nullptr;
-  int g_S = -1;
-  cudaStream_t g_stream = nullptr;
+  // graph cache: one instantiated graph per (X, out, S, stream), LRU
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    const void* x = nullptr;
+    void* out = nullptr;
+    int S = -1;
+    cudaStream_t stream = nullptr;
+    uint64_t used = 0;
+  };
+  static constexpr int kGraphSlots = 4;
+  GraphEntry graphs[kGraphSlots];
+  uint64_t graph_clock = 0;
+  void drop_graphs() {
+    for (GraphEntry& g : graphs) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      g = GraphEntry{};
+    }
+  }
+  // pipelined host forward: double-buffered device staging + two copy streams
+  DevBuf<__nv_bfloat16> pin[2], pout[2];
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};
 };
 
 struct moe_ffn {

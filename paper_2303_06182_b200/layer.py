@@ -144,6 +144,20 @@ class MoeLayer:
                                                   _stream_ptr(stream)))
         return out_host
 
+    def forward_host_batches(self, xs_host, outs_host, stream):
+        """Pipelined end-to-end path over a queue of batches: pinned host bf16
+        in -> pinned host bf16 out for every batch, uploads and read-backs
+        overlapped with the neighbouring batches' compute (moe_capi.h)."""
+        n = len(xs_host)
+        if len(outs_host) != n:
+            raise ValueError("one output buffer per batch")
+        xp = (C.c_void_p * n)(*[x.data_ptr() for x in xs_host])
+        op = (C.c_void_p * n)(*[o.data_ptr() for o in outs_host])
+        sz = (C.c_int * n)(*[x.shape[0] for x in xs_host])
+        check(self.ctx.lib.moe_layer_forward_host_batches(self.h, xp, sz, op, n,
+                                                          _stream_ptr(stream)))
+        return outs_host
+
     def check_errors(self, stream=None):
         check(self.ctx.lib.moe_check_errors(self.ctx.h, _stream_ptr(stream)))
 

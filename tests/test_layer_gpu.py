@@ -212,6 +212,28 @@ def test_graph_and_host_paths_bitwise_equal_to_eager(S, TD, HD, E, k):
     assert torch.equal(oh, eager.cpu())
 
 
+@pytest.mark.parametrize("S,TD,HD,E,k", [(1024, 256, 512, 16, 2), (16384, 1024, 4096, 512, 2)])
+def test_pipelined_host_batches_bitwise_equal_per_call(S, TD, HD, E, k):
+    """moe_layer_forward_host_batches: every batch of the queue (different
+    tokens, different sizes, double-buffered staging reused) equals its own
+    synchronous moe_layer_forward_host call."""
+    shape = LayerShape(TD, HD, E, k)
+    layer = MoeLayer(shape, S, weights=make_weights(shape, seed=SEED))
+    sizes = [S, S // 2 + 3, S, 1, S - 7, S]
+    xs = [make_tokens(n, TD, seed=SEED + 10 + i).cpu().pin_memory() for i, n in enumerate(sizes)]
+    outs = [torch.empty_like(x).pin_memory() for x in xs]
+    s = torch.cuda.Stream()
+    layer.forward_host_batches(xs, outs, s)
+    for x, o in zip(xs, outs):
+        ref = torch.empty_like(x).pin_memory()
+        layer.forward_host(x, ref, stream=s)
+        assert torch.equal(o, ref)
+    # outputs written to a shared ring of buffers stay ordered
+    ring = [torch.empty_like(xs[0]).pin_memory() for _ in range(2)]
+    layer.forward_host_batches([xs[0], xs[2], xs[0], xs[2], xs[0]], [ring[0], ring[1]] * 2 + [ring[0]], s)
+    assert torch.equal(ring[0], outs[0]) and torch.equal(ring[1], outs[2])
+
+
 def test_repeat_forward_is_deterministic():
     layer, x, out, w, v = _run(4096, 256, 512, 64, 2)
     out2 = layer(x)
