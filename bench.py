@@ -278,6 +278,7 @@ def run_ep(args, world, rank, local):
     be = KernelBackend(ctx, shape, Wg, W1l, W2l, S, S * k * world, tile_n=args.tile_n)
     layer = ExpertParallelMoE(pl, k, be, Transport(), rank)
     stream = torch.cuda.Stream()
+    stream.wait_stream(torch.cuda.current_stream())  # inputs were written on the current stream
     K, W = args.steps, args.warmup
     with torch.cuda.stream(stream):
         for _ in range(W):
@@ -390,6 +391,7 @@ def run_cache(args):
     layer = MoeLayer(shape, S, weights=w)
     cache = ExpertCache(layer, slots, "lifo", W1h, W2h)
     stream = torch.cuda.Stream()
+    stream.wait_stream(torch.cuda.current_stream())  # inputs were written on the current stream
     out = torch.empty_like(x)
 
     def timed(fn):
@@ -464,6 +466,7 @@ def run_b200(args):
     x = make_tokens(S, TD, seed=seed)
     out = torch.empty_like(x)
     stream = torch.cuda.Stream()
+    stream.wait_stream(torch.cuda.current_stream())  # inputs were written on the current stream
     lib = layer.ctx.lib
     K, W = args.steps, args.warmup
     _capi.check(lib.moe_layer_enable_timing(layer.h, 0))

@@ -502,7 +502,8 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
       (st = encode_bf16(&L->tmW1, W1, (uint64_t)E * HD, TD, 128)) ||
       (st = encode_bf16(&L->tmW2, W2, (uint64_t)E * TD, HD, 128)) ||
       (st = encode_bf16(&L->tmXp, L->xp.p, Rp, TD, 16)) ||
-      (st = encode_bf16(&L->tmH, L->h.p, Rp, HD, 16))) {
+      (st = encode_bf16(&L->tmH, L->h.p, Rp, HD, 16)) ||
+      (st = encode_rows(&L->xpm, L->xp.p, Rp, TD)) || (st = encode_rows(&L->hm, L->h.p, Rp, HD))) {
     moe_layer_destroy(L);
     return st;
   }
@@ -677,7 +678,7 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
     }();
     fa.lag = lag;
     fa.discard_h = discard;
-    cudaError_t e = launch_fused_ffn(L->tmW1, L->tmXp, L->tmW2, L->tmH, fa, L->tile_n,
+    cudaError_t e = launch_fused_ffn(L->tmW1, L->xpm, L->tmW2, L->hm, fa, L->tile_n,
                                      L->ctx->sms, s);
     if (e != cudaSuccess) return cuda_fail(e, "fused ffn launch");
     mark(4);
@@ -944,7 +945,8 @@ int moe_ffn_create(moe_ctx* ctx, const moe_ffn_desc* desc, const void* W1, const
   if ((st = encode_bf16(&F->tmW1, W1, (uint64_t)d.num_experts * HD, TD, 128)) ||
       (st = encode_bf16(&F->tmW2, W2, (uint64_t)d.num_experts * TD, HD, 128)) ||
       (st = encode_bf16(&F->tmXp, F->xp.p, Rp, TD, 16)) ||
-      (st = encode_bf16(&F->tmH, F->h.p, Rp, HD, 16))) {
+      (st = encode_bf16(&F->tmH, F->h.p, Rp, HD, 16)) ||
+      (st = encode_rows(&F->xpm, F->xp.p, Rp, TD)) || (st = encode_rows(&F->hm, F->h.p, Rp, HD))) {
     moe_ffn_destroy(F);
     return st;
   }
@@ -1001,7 +1003,7 @@ int moe_ffn_forward(moe_ffn* F, const void* X_rows, const int32_t* keys, const f
     const int per_item = HD / 128 + TD / 128;
     fa.lag = std::max(2, (8 * F->ctx->sms + per_item - 1) / per_item);
     fa.discard_h = 1;
-    e = launch_fused_ffn(F->tmW1, F->tmXp, F->tmW2, F->tmH, fa, F->tile_n, F->ctx->sms, s);
+    e = launch_fused_ffn(F->tmW1, F->xpm, F->tmW2, F->hm, fa, F->tile_n, F->ctx->sms, s);
     if (e != cudaSuccess) return cuda_fail(e, "fused ffn launch");
     return MOE_OK;
   }

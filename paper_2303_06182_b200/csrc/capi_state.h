@@ -72,6 +72,15 @@ inline int encode_bf16(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t 
   return MOE_OK;
 }
 
+inline int encode_rows(moe::RowMaps* m, const void* ptr, uint64_t rows, uint64_t cols) {
+  int st;
+  if ((st = encode_bf16(&m->m16, ptr, rows, cols, 16)) ||
+      (st = encode_bf16(&m->m32, ptr, rows, cols, 32)) ||
+      (st = encode_bf16(&m->m64, ptr, rows, cols, 64)))
+    return st;
+  return MOE_OK;
+}
+
 // Reference check_batch (gating.cpp:12-18), verbatim messages.
 inline int check_batch(int S, int k, int E) {
   if (E < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "num_experts must be positive");
@@ -150,6 +159,7 @@ struct moe_layer {
   int rows_max = 0;
   int items_max = 0;
   CUtensorMap tmWg, tmW1, tmW2, tmXp, tmH;
+  moe::RowMaps xpm, hm;  // Xp / H at 16/32/64-row boxes (fused FFN)
   CUtensorMap tmX;  // X for the gate (box 64 x 128)
   const void* tmX_ptr = nullptr;
   int tmX_rows = 0;
@@ -198,6 +208,7 @@ struct moe_ffn {
   int tile_n = 128;
   int items_max = 0;
   CUtensorMap tmW1, tmW2, tmXp, tmH;
+  moe::RowMaps xpm, hm;
   DevBuf<int32_t> counts, splits, order, pos, n_items, done;
   DevBuf<float> wpos, ones;
   DevBuf<FfnItem> items;

@@ -33,7 +33,6 @@ constexpr int kBlockK = 64;
 constexpr int kUmmaK = 16;
 constexpr int kABytes = kBlockM * kBlockK * 2;
 constexpr int kEpiBytes = 4 * 32 * 32 * 2;
-constexpr int kBoxRowsB = 16;
 
 template <int BN, int STAGES>
 struct FusedCfg {
@@ -82,10 +81,9 @@ __device__ __forceinline__ void discard_l2(const void* p) {
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(256, 1)
-    fused_ffn_kernel(const __grid_constant__ CUtensorMap tmW1,
-                     const __grid_constant__ CUtensorMap tmXp,
-                     const __grid_constant__ CUtensorMap tmW2,
-                     const __grid_constant__ CUtensorMap tmH, FusedFfnArgs g) {
+    fused_ffn_kernel(const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ RowMaps xpm,
+                     const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ RowMaps hm,
+                     FusedFfnArgs g) {
   using Cfg = FusedCfg<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -105,9 +103,12 @@ __global__ void __launch_bounds__(256, 1)
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmW1);
-    ptx::prefetch_tmap(&tmXp);
     ptx::prefetch_tmap(&tmW2);
-    ptx::prefetch_tmap(&tmH);
+    for (const RowMaps* m : {&xpm, &hm}) {
+      ptx::prefetch_tmap(&m->m16);
+      ptx::prefetch_tmap(&m->m32);
+      ptx::prefetch_tmap(&m->m64);
+    }
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(256, 1)
       const int nrows = (it.len + 15) & ~15;
       const int wslot = g.slot_of ? g.slot_of[it.expert] : it.expert;
       const CUtensorMap* tA = tr.gemm ? &tmW2 : &tmW1;
-      const CUtensorMap* tB = tr.gemm ? &tmH : &tmXp;
+      const RowMaps* tB = tr.gemm ? &hm : &xpm;
       const int a_row = wslot * (tr.gemm ? g.TD : g.HD) + tr.m * kBlockM;
       const int KB = tr.gemm ? KB2 : KB1;
       if (tr.gemm) {
@@ -167,9 +168,18 @@ __global__ void __launch_bounds__(256, 1)
         ptx::mbar_arrive_expect_tx(&full[stage], bytes);
         ptx::tma_load_2d(sA + stage * kABytes, tA, &full[stage], kb * kBlockK, a_row, pol_w);
         uint8_t* b_dst = sB + stage * Cfg::kBBytes;
-        for (int r = 0; r < nrows; r += kBoxRowsB)
-          ptx::tma_load_2d(b_dst + r * kBlockK * 2, tB, &full[stage], kb * kBlockK, it.row0 + r,
-                           pol_x);
+        int r = 0;
+        for (; r + 64 <= nrows; r += 64)
+          ptx::tma_load_2d(b_dst + r * kBlockK * 2, &tB->m64, &full[stage], kb * kBlockK,
+                           it.row0 + r, pol_x);
+        if (r + 32 <= nrows) {
+          ptx::tma_load_2d(b_dst + r * kBlockK * 2, &tB->m32, &full[stage], kb * kBlockK,
+                           it.row0 + r, pol_x);
+          r += 32;
+        }
+        if (r < nrows)
+          ptx::tma_load_2d(b_dst + r * kBlockK * 2, &tB->m16, &full[stage], kb * kBlockK,
+                           it.row0 + r, pol_x);
         if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
@@ -298,8 +308,8 @@ cudaError_t prepare_fused() {
 }
 
 template <int BN, int STAGES>
-cudaError_t launch_fused(const CUtensorMap& w1, const CUtensorMap& xp, const CUtensorMap& w2,
-                         const CUtensorMap& h, const FusedFfnArgs& g, int grid,
+cudaError_t launch_fused(const CUtensorMap& w1, const RowMaps& xp, const CUtensorMap& w2,
+                         const RowMaps& h, const FusedFfnArgs& g, int grid,
                          cudaStream_t stream) {
   return launch_chain(fused_ffn_kernel<BN, STAGES>, dim3(grid), dim3(256),
                       FusedCfg<BN, STAGES>::kSmem, stream, false, w1, xp, w2, h, g);
@@ -313,12 +323,11 @@ cudaError_t fused_ffn_prepare() {
   return prepare_fused<256, 4>();
 }
 
-cudaError_t launch_fused_ffn(const CUtensorMap& tmW1, const CUtensorMap& tmXp,
-                             const CUtensorMap& tmW2, const CUtensorMap& tmH,
-                             const FusedFfnArgs& args, int tile_n, int grid,
+cudaError_t launch_fused_ffn(const CUtensorMap& tmW1, const RowMaps& xp, const CUtensorMap& tmW2,
+                             const RowMaps& h, const FusedFfnArgs& args, int tile_n, int grid,
                              cudaStream_t stream) {
-  if (tile_n == 128) return launch_fused<128, 6>(tmW1, tmXp, tmW2, tmH, args, grid, stream);
-  if (tile_n == 256) return launch_fused<256, 4>(tmW1, tmXp, tmW2, tmH, args, grid, stream);
+  if (tile_n == 128) return launch_fused<128, 6>(tmW1, xp, tmW2, h, args, grid, stream);
+  if (tile_n == 256) return launch_fused<256, 4>(tmW1, xp, tmW2, h, args, grid, stream);
   return cudaErrorInvalidValue;
 }
 

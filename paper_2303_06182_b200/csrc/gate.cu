@@ -21,7 +21,10 @@
 #include <cooperative_groups.h>
 #include <float.h>
 
+#include <cstdlib>
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "moe_internal.h"
 #include "ptx.cuh"
@@ -38,17 +41,26 @@ constexpr int kMaxSmem = 200 * 1024;
 
 struct GateLayout {
   int e_pad;      // E rounded up to 16
-  int b_rows;     // rows of Wg staged per k-block (multiple of the box height)
+  int b_rows;     // rows of Wg staged per k-block (n_box boxes)
   int box_rows;   // TMA box height for Wg
+  int n_box;      // 4 when E_pad >= 128 (one box per CTA of a 4-CTA cluster), else 1
   int stages;
   int smem;
 };
 
+// Wg k-block slab = n_box boxes; a cluster of C CTAs (C | n_box) splits the
+// boxes between its CTAs and multicasts each to all of them.
 __host__ __device__ inline GateLayout gate_layout(int E) {
   GateLayout L;
   L.e_pad = (E + 15) & ~15;
-  L.box_rows = L.e_pad <= 256 ? L.e_pad : 256;
-  L.b_rows = (L.e_pad + L.box_rows - 1) / L.box_rows * L.box_rows;
+  if (L.e_pad >= 128) {
+    L.b_rows = (L.e_pad + 31) & ~31;
+    L.n_box = 4;
+  } else {
+    L.b_rows = L.e_pad;
+    L.n_box = 1;
+  }
+  L.box_rows = L.b_rows / L.n_box;  // multiple of 8: every box starts on a swizzle atom
   const int stage = kABytes + L.b_rows * kBlockK * 2;
   int s = (kMaxSmem - 2048) / stage;
   L.stages = s > 8 ? 8 : s;
@@ -80,10 +92,11 @@ __device__ __forceinline__ void topk_insert(float (&bv)[K], int (&bi)[K], float 
 // 8 warps, idx / w written to global; with s_e/s_w the tile's routing is also
 // left in shared memory (slot t*k+j of the tile) for a fused dispatch.
 // Ends with a block barrier and the TMEM released.
-template <int K>
+template <int K, int C = 1>
 __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensorMap& tmWg,
                                           const GateArgs& a, uint8_t* smem, int* s_e,
                                           float* s_w) {
+  static_assert(C == 1 || C == 2 || C == 4, "cluster of 1, 2 or 4 CTAs");
   const GateLayout L = gate_layout(a.E);
   const int stage_bytes = kABytes + L.b_rows * kBlockK * 2;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.stages * stage_bytes);
@@ -101,7 +114,7 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
     ptx::prefetch_tmap(&tmWg);
     for (int s = 0; s < L.stages; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], C);  // one MMA commit from every CTA that reads the stage
     }
     ptx::mbar_init(tfull, 1);
     ptx::fence_barrier_init();
@@ -117,6 +130,7 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (C > 1) ptx::cluster_sync();  // peers' barriers exist before any multicast lands
   pdl_trigger();
   pdl_wait();  // X and the routing buffers belong to the previous kernel until here
 
@@ -125,16 +139,26 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
       // ---------------------------------------------------- TMA producer
       const uint64_t pol_x = ptx::policy_evict_first();
       const uint64_t pol_w = ptx::policy_evict_last();
+      // this CTA's share of the Wg boxes (all of them without a cluster)
+      const int per = L.n_box / C;
+      const int b_lo = C > 1 ? static_cast<int>(ptx::cluster_ctarank()) * per : 0;
       int stage = 0;
       uint32_t phase = 0;
       for (int kb = 0; kb < KB; ++kb) {
+        // free once every CTA of the cluster has consumed the stage
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         ptx::mbar_arrive_expect_tx(&full[stage], stage_bytes);
         uint8_t* st = smem + stage * stage_bytes;
         ptx::tma_load_2d(st, &tmX, &full[stage], kb * kBlockK, tok0, pol_x);
-        for (int r = 0; r < L.b_rows; r += L.box_rows)
-          ptx::tma_load_2d(st + kABytes + r * kBlockK * 2, &tmWg, &full[stage], kb * kBlockK, r,
-                           pol_w);
+        for (int b = b_lo; b < b_lo + per; ++b) {
+          const int r = b * L.box_rows;
+          if (C > 1)
+            ptx::tma_load_2d_mc(st + kABytes + r * kBlockK * 2, &tmWg, &full[stage], kb * kBlockK,
+                                r, static_cast<uint16_t>((1u << C) - 1), pol_w);
+          else
+            ptx::tma_load_2d(st + kABytes + r * kBlockK * 2, &tmWg, &full[stage], kb * kBlockK, r,
+                             pol_w);
+        }
         if (++stage == L.stages) {
           stage = 0;
           phase ^= 1;
@@ -165,7 +189,10 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
             ptx::mma_bf16(tmem_base + 256, ptx::umma_desc_sw128(a0 + kk * 32),
                           ptx::umma_desc_sw128(b0 + 256 * 128 + kk * 32), id1, acc);
         }
-        ptx::mma_commit(&empty[stage]);
+        if (C > 1)
+          ptx::mma_commit_mc(&empty[stage], static_cast<uint16_t>((1u << C) - 1));
+        else
+          ptx::mma_commit(&empty[stage]);
         if (++stage == L.stages) {
           stage = 0;
           phase ^= 1;
@@ -276,6 +303,8 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
     else if (L.e_pad <= 256) ptx::tmem_dealloc<256>(tmem_base);
     else ptx::tmem_dealloc<512>(tmem_base);
   }
+  // peers' last MMA commits arrive on this CTA's empty barriers: stay alive
+  if (C > 1) ptx::cluster_sync();
 }
 
 __device__ __forceinline__ uint8_t* aligned_smem() {
@@ -284,11 +313,11 @@ __device__ __forceinline__ uint8_t* aligned_smem() {
                                     ~static_cast<uintptr_t>(1023));
 }
 
-template <int K>
+template <int K, int C>
 __global__ void __launch_bounds__(256, 1)
     gate_topk_kernel(const __grid_constant__ CUtensorMap tmX,
                      const __grid_constant__ CUtensorMap tmWg, GateArgs a) {
-  gate_tile<K>(tmX, tmWg, a, aligned_smem(), nullptr, nullptr);
+  gate_tile<K, C>(tmX, tmWg, a, aligned_smem(), nullptr, nullptr);
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -505,6 +534,14 @@ __global__ void __launch_bounds__(256, 1)
 
 int gate_box_rows(int E) { return gate_layout(E).box_rows; }
 
+template <int C>
+const void* gate_fn(int k) {
+  return k == 1   ? reinterpret_cast<const void*>(gate_topk_kernel<1, C>)
+         : k == 2 ? reinterpret_cast<const void*>(gate_topk_kernel<2, C>)
+         : k <= 4 ? reinterpret_cast<const void*>(gate_topk_kernel<4, C>)
+                  : reinterpret_cast<const void*>(gate_topk_kernel<8, C>);
+}
+
 cudaError_t gate_prepare(int E) {
   // process-wide kernel attribute: only raise it (see route_prepare)
   static std::mutex mu;
@@ -512,11 +549,7 @@ cudaError_t gate_prepare(int E) {
   const GateLayout L = gate_layout(E);
   std::lock_guard<std::mutex> lock(mu);
   if (L.smem <= granted) return cudaSuccess;
-  const void* fns[] = {reinterpret_cast<const void*>(gate_topk_kernel<1>),
-                       reinterpret_cast<const void*>(gate_topk_kernel<2>),
-                       reinterpret_cast<const void*>(gate_topk_kernel<4>),
-                       reinterpret_cast<const void*>(gate_topk_kernel<8>),
-                       reinterpret_cast<const void*>(gate_dispatch_kernel<1>),
+  const void* fns[] = {reinterpret_cast<const void*>(gate_dispatch_kernel<1>),
                        reinterpret_cast<const void*>(gate_dispatch_kernel<2>),
                        reinterpret_cast<const void*>(gate_dispatch_kernel<4>),
                        reinterpret_cast<const void*>(gate_dispatch_kernel<8>)};
@@ -524,8 +557,73 @@ cudaError_t gate_prepare(int E) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem);
     if (e != cudaSuccess) return e;
   }
+  for (int k : {1, 2, 4, 8}) {
+    for (const void* fn : {gate_fn<1>(k), gate_fn<2>(k), gate_fn<4>(k)}) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem);
+      if (e != cudaSuccess) return e;
+    }
+  }
   granted = L.smem;
   return cudaSuccess;
+}
+
+// Cluster size for the gate: the largest C | n_box (<= MOE_GATE_CLUSTER, default
+// 4) for which every cluster of the grid is co-resident (one wave).
+int gate_cluster(const GateLayout& L, int tiles, int smem) {
+  static int env = -1;
+  if (env < 0) {
+    const char* v = getenv("MOE_GATE_CLUSTER");
+    env = v ? atoi(v) : 4;
+  }
+  for (int C = 4; C >= 2; C >>= 1) {
+    if (C > env || L.n_box % C != 0 || tiles < C) continue;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((tiles + C - 1) / C * C);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = C;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    const void* fn = C == 4 ? gate_fn<4>(2) : gate_fn<2>(2);
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (n * C >= tiles) return C;
+  }
+  return 1;
+}
+
+template <int K>
+cudaError_t launch_gate_k(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateArgs& a,
+                          int C, int tiles, int smem, cudaStream_t stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((tiles + C - 1) / C * C);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  attr[n].id = cudaLaunchAttributeClusterDimension;
+  attr[n].val.clusterDim.x = C;
+  attr[n].val.clusterDim.y = 1;
+  attr[n].val.clusterDim.z = 1;
+  ++n;
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  if (C == 4) return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 4>, tmX, tmWg, a);
+  if (C == 2) return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 2>, tmX, tmWg, a);
+  return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 1>, tmX, tmWg, a);
 }
 
 cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateArgs& a,
@@ -533,11 +631,21 @@ cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const G
   if (a.k < 1 || a.k > kMaxK || a.E > 512 || a.E < a.k || (a.TD % kBlockK) != 0)
     return cudaErrorInvalidValue;
   const GateLayout L = gate_layout(a.E);
-  const int grid = (a.S + kBlockM - 1) / kBlockM;
-  auto kern = a.k == 1 ? gate_topk_kernel<1>
-              : a.k == 2 ? gate_topk_kernel<2>
-              : a.k <= 4 ? gate_topk_kernel<4> : gate_topk_kernel<8>;
-  return launch_chain(kern, dim3(grid), dim3(256), L.smem, stream, false, tmX, tmWg, a);
+  const int tiles = (a.S + kBlockM - 1) / kBlockM;
+  // cached per (E, tiles): the occupancy query is not free
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, int> cache;
+  int C;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find({L.e_pad, tiles});
+    if (it == cache.end()) it = cache.emplace(std::make_pair(L.e_pad, tiles), gate_cluster(L, tiles, L.smem)).first;
+    C = it->second;
+  }
+  if (a.k == 1) return launch_gate_k<1>(tmX, tmWg, a, C, tiles, L.smem, stream);
+  if (a.k == 2) return launch_gate_k<2>(tmX, tmWg, a, C, tiles, L.smem, stream);
+  if (a.k <= 4) return launch_gate_k<4>(tmX, tmWg, a, C, tiles, L.smem, stream);
+  return launch_gate_k<8>(tmX, tmWg, a, C, tiles, L.smem, stream);
 }
 
 }  // namespace moe

@@ -139,10 +139,16 @@ struct FusedFfnArgs {
   int lag;                  // items between an item's GEMM1 and GEMM2 tiles
   int discard_h;            // drop consumed H lines from L2 (no write-back)
 };
+// One activation matrix (Xp or H) seen by TMA at three box heights: a B tile
+// of n rows (n % 16 == 0) is n/64 boxes of 64 rows plus at most one of 32 and
+// one of 16 -- 1-3 TMA issues per k-block instead of n/16.
+struct RowMaps {
+  CUtensorMap m16, m32, m64;
+};
 cudaError_t fused_ffn_prepare();
-cudaError_t launch_fused_ffn(const CUtensorMap& tmW1, const CUtensorMap& tmXp,
-                             const CUtensorMap& tmW2, const CUtensorMap& tmH,
-                             const FusedFfnArgs& args, int tile_n, int grid, cudaStream_t stream);
+cudaError_t launch_fused_ffn(const CUtensorMap& tmW1, const RowMaps& xp, const CUtensorMap& tmW2,
+                             const RowMaps& h, const FusedFfnArgs& args, int tile_n, int grid,
+                             cudaStream_t stream);
 
 cudaError_t gemm_prepare();
 // tmA: weights [slots*m_total, k_total]; tmB: activations [rows, k_total]

@@ -199,6 +199,7 @@ def test_graph_and_host_paths_bitwise_equal_to_eager(S, TD, HD, E, k):
     layer = MoeLayer(shape, S, weights=w)
     x = make_tokens(S, TD, seed=SEED)
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())  # inputs were written on the current stream
     with torch.cuda.stream(s):
         eager = layer(x, stream=s)
         out_g = torch.empty_like(x)
@@ -223,6 +224,7 @@ def test_pipelined_host_batches_bitwise_equal_per_call(S, TD, HD, E, k):
     xs = [make_tokens(n, TD, seed=SEED + 10 + i).cpu().pin_memory() for i, n in enumerate(sizes)]
     outs = [torch.empty_like(x).pin_memory() for x in xs]
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())  # inputs were written on the current stream
     layer.forward_host_batches(xs, outs, s)
     for x, o in zip(xs, outs):
         ref = torch.empty_like(x).pin_memory()

@@ -13,6 +13,7 @@ x = make_tokens(S, TD)
 layer = MoeLayer(shape, S, weights=w)
 out = torch.empty_like(x)
 s = torch.cuda.Stream()
+s.wait_stream(torch.cuda.current_stream())  # inputs were written on the current stream
 K = 100
 for graph in (False, True, False, True):
     with torch.cuda.stream(s):

@@ -17,6 +17,7 @@ x = make_tokens(S, TD)
 layer = MoeLayer(shape, S, weights=w)
 out = torch.empty_like(x)
 s = torch.cuda.Stream()
+s.wait_stream(torch.cuda.current_stream())  # inputs were written on the current stream
 with torch.cuda.stream(s):
     for _ in range(5):
         layer.forward(x, out, graph=graph, stream=s)
