@@ -173,6 +173,11 @@ typedef struct moe_layer_desc {
                              launch (dynamic gating, batch <= one 128-token
                              tile per SM); 0 (default): three launches --
                              measured faster, profiles/r01_fusion_ab.md */
+  int keep_layout;        /* 0 (default): when the fused FFN runs, the layer keeps
+                             a copy of W1/W2 repacked into contiguous 128x64
+                             tiles (+1x expert-weight memory; weights are
+                             snapshotted at create, see moe_layer_repack);
+                             1: stream the caller's row-major weights */
 } moe_layer_desc;
 
 /* Weights are caller-owned device buffers (bf16, row-major):
@@ -180,6 +185,10 @@ typedef struct moe_layer_desc {
 int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, const void* W1,
                      const void* W2, moe_layer** out);
 int moe_layer_destroy(moe_layer* layer);
+
+/* Refresh the layer's packed weight copy after the caller changed W1/W2 in
+ * place (no-op when the layer streams the caller's weights). */
+int moe_layer_repack(moe_layer* layer, void* stream);
 
 /* One forward pass on device buffers: X [S,TD] bf16 -> out [S,TD] bf16.
  * Stream-ordered, no host synchronisation (dynamic and static modes). */
@@ -249,7 +258,10 @@ int moe_layer_set_weight_pool(moe_layer* layer, const void* W1_pool, const void*
  * the building block of the layer): Y_rows[i] = row_w[i] * W2_e relu(W1_e x_i)
  * with e = keys[i] in [0, num_experts).  Rows are grouped by expert on the
  * device (stable counting sort), streamed through the tcgen05 grouped GEMM and
- * written back in input order.  W1 [E, HD, TD], W2 [E, TD, HD] bf16, device. */
+ * written back in input order.  W1 [E, HD, TD], W2 [E, TD, HD] bf16, device.
+ * At tile_n 128 the FFN keeps a tile-packed copy of W1/W2 made at create
+ * (weights snapshotted; MOE_PACK=0 in the environment streams the caller's
+ * buffers instead). */
 typedef struct moe_ffn moe_ffn;
 typedef struct moe_ffn_desc {
   int max_rows;

@@ -36,7 +36,7 @@ EXPORTED = [
     "moe_cache_forward_routed", "moe_cache_stats", "moe_cache_resident", "moe_layer_forward_routed",
     "moe_device_alloc", "moe_device_free", "moe_host_alloc", "moe_host_free", "moe_memcpy",
     "moe_stream_create", "moe_stream_destroy", "moe_stream_synchronize",
-    "moe_layer_forward_host_batches",
+    "moe_layer_forward_host_batches", "moe_layer_repack",
 ]
 
 
@@ -59,7 +59,7 @@ class LayerDesc(C.Structure):
         ("num_experts", C.c_int), ("top_k", C.c_int), ("mode", C.c_int),
         ("capacity_factor", C.c_double), ("tile_n", C.c_int), ("keep_logits", C.c_int),
         ("fuse_combine", C.c_int), ("split_ffn", C.c_int),
-        ("fuse_front", C.c_int),
+        ("fuse_front", C.c_int), ("keep_layout", C.c_int),
     ]
 
 
@@ -118,6 +118,7 @@ def load(path: str = LIB_PATH):
     _sig(lib.moe_layer_forward_graph, I, P, P, I, P, P)
     _sig(lib.moe_layer_forward_host, I, P, P, I, P, P)
     _sig(lib.moe_layer_forward_host_batches, I, P, P, P, P, I, P)
+    _sig(lib.moe_layer_repack, I, P, P)
     _sig(lib.moe_layer_get_view, I, P, C.POINTER(LayerView))
     _sig(lib.moe_layer_set_weight_pool, I, P, P, P, I, P)
     _sig(lib.moe_exchange_counts_host, I, P, P, I, I, I, P, I, P)

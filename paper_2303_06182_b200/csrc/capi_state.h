@@ -74,7 +74,8 @@ inline int encode_bf16(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t 
 
 inline int encode_rows(moe::RowMaps* m, const void* ptr, uint64_t rows, uint64_t cols) {
   int st;
-  if ((st = encode_bf16(&m->m16, ptr, rows, cols, 16)) ||
+  if ((st = encode_bf16(&m->m8, ptr, rows, cols, 8)) ||
+      (st = encode_bf16(&m->m16, ptr, rows, cols, 16)) ||
       (st = encode_bf16(&m->m32, ptr, rows, cols, 32)) ||
       (st = encode_bf16(&m->m64, ptr, rows, cols, 64)))
     return st;
@@ -159,7 +160,11 @@ struct moe_layer {
   int rows_max = 0;
   int items_max = 0;
   CUtensorMap tmWg, tmW1, tmW2, tmXp, tmH;
-  moe::RowMaps xpm, hm;  // Xp / H at 16/32/64-row boxes (fused FFN)
+  moe::RowMaps xpm, hm;  // Xp / H at 8/16/32/64-row boxes (fused FFN)
+  // prepacked weights: 128 x 64 tiles, 16 KB contiguous (launch_pack_tiles)
+  bool packed = false;
+  DevBuf<__nv_bfloat16> w1p, w2p;
+  CUtensorMap tmW1p, tmW2p;
   CUtensorMap tmX;  // X for the gate (box 64 x 128)
   const void* tmX_ptr = nullptr;
   int tmX_rows = 0;
@@ -209,6 +214,9 @@ struct moe_ffn {
   int items_max = 0;
   CUtensorMap tmW1, tmW2, tmXp, tmH;
   moe::RowMaps xpm, hm;
+  bool packed = false;
+  DevBuf<__nv_bfloat16> w1p, w2p;
+  CUtensorMap tmW1p, tmW2p;
   DevBuf<int32_t> counts, splits, order, pos, n_items, done;
   DevBuf<float> wpos, ones;
   DevBuf<FfnItem> items;

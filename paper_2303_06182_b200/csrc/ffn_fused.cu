@@ -21,6 +21,8 @@
 //
 // Roles per CTA (256 threads) are those of grouped_gemm_kernel: warp 0 TMA
 // producer, warp 1 MMA issuer, warp 2 TMEM allocator, warps 4-7 epilogue.
+#include <cstdlib>
+
 #include "moe_internal.h"
 #include "ptx.cuh"
 
@@ -29,14 +31,22 @@ namespace moe {
 namespace {
 
 constexpr int kBlockM = 128;
-constexpr int kBlockK = 64;
+constexpr int kChunkK = 64;  // one 128-byte swizzle atom row of bf16
 constexpr int kUmmaK = 16;
-constexpr int kABytes = kBlockM * kBlockK * 2;
 constexpr int kEpiBytes = 4 * 32 * 32 * 2;
 
-template <int BN, int STAGES>
+// A stage holds KCH k-chunks of 64 (KCH * 64 = the stage's K extent) for the
+// weight tile (128 rows) and the token tile (BN rows), chunk-major: chunk c of
+// A at c * 16 KB, chunk c of B at c * BN * 128 B, each a stack of 1024-byte
+// swizzle atoms.  Bigger stages amortise the barrier round trip and the MMA
+// issue overhead (8 MMAs per wait/commit at KCH = 2).
+template <int BN, int STAGES, int KCH>
 struct FusedCfg {
-  static constexpr int kBBytes = BN * kBlockK * 2;
+  static constexpr int kStageK = KCH * kChunkK;
+  static constexpr int kAChunk = kBlockM * kChunkK * 2;
+  static constexpr int kBChunk = BN * kChunkK * 2;
+  static constexpr int kABytes = KCH * kAChunk;
+  static constexpr int kBBytes = KCH * kBChunk;
   static constexpr int kSmem = 1024 + STAGES * (kABytes + kBBytes) + kEpiBytes +
                                (2 * STAGES + 4) * 8 + 16;
   static constexpr int kTmemCols = 2 * BN;
@@ -79,12 +89,13 @@ __device__ __forceinline__ void discard_l2(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int KCH>
 __global__ void __launch_bounds__(256, 1)
     fused_ffn_kernel(const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ RowMaps xpm,
                      const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ RowMaps hm,
                      FusedFfnArgs g) {
-  using Cfg = FusedCfg<BN, STAGES>;
+  using Cfg = FusedCfg<BN, STAGES, KCH>;
+  constexpr int kABytes = Cfg::kABytes;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -133,7 +144,7 @@ __global__ void __launch_bounds__(256, 1)
   int32_t* done1 = g.done1 + item0;
   int32_t* done2 = g.done2 + item0;
   const int MT1 = g.HD / kBlockM, MT2 = g.TD / kBlockM;
-  const int KB1 = g.TD / kBlockK, KB2 = g.HD / kBlockK;
+  const int KB1 = g.TD / Cfg::kStageK, KB2 = g.HD / Cfg::kStageK;
   const int L = min(g.lag, n);
   const int total = n * (MT1 + MT2);
 
@@ -151,6 +162,8 @@ __global__ void __launch_bounds__(256, 1)
       const CUtensorMap* tA = tr.gemm ? &tmW2 : &tmW1;
       const RowMaps* tB = tr.gemm ? &hm : &xpm;
       const int a_row = wslot * (tr.gemm ? g.TD : g.HD) + tr.m * kBlockM;
+      // prepacked: first 128 x 64 tile of this weight block
+      const int a_tile = (wslot * (tr.gemm ? MT2 : MT1) + tr.m) * ((tr.gemm ? g.HD : g.TD) / kChunkK);
       const int KB = tr.gemm ? KB2 : KB1;
       if (tr.gemm) {
         // H rows of this item: every GEMM1 tile stored (acquire), then make
@@ -162,24 +175,34 @@ __global__ void __launch_bounds__(256, 1)
         }
         fence_proxy_async_global();
       }
-      const uint32_t bytes = kABytes + nrows * kBlockK * 2;
+      const uint32_t bytes = kABytes + ((g.dbg & 1) ? 0 : KCH * nrows * kChunkK * 2);
       for (int kb = 0; kb < KB; ++kb) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         ptx::mbar_arrive_expect_tx(&full[stage], bytes);
-        ptx::tma_load_2d(sA + stage * kABytes, tA, &full[stage], kb * kBlockK, a_row, pol_w);
-        uint8_t* b_dst = sB + stage * Cfg::kBBytes;
-        int r = 0;
-        for (; r + 64 <= nrows; r += 64)
-          ptx::tma_load_2d(b_dst + r * kBlockK * 2, &tB->m64, &full[stage], kb * kBlockK,
-                           it.row0 + r, pol_x);
-        if (r + 32 <= nrows) {
-          ptx::tma_load_2d(b_dst + r * kBlockK * 2, &tB->m32, &full[stage], kb * kBlockK,
-                           it.row0 + r, pol_x);
-          r += 32;
+#pragma unroll
+        for (int c = 0; c < KCH; ++c) {
+          const int k0 = kb * Cfg::kStageK + c * kChunkK;
+          if (g.packed)
+            ptx::tma_load_2d(sA + stage * kABytes + c * Cfg::kAChunk, tA, &full[stage], 0,
+                             (a_tile + kb * KCH + c) * kBlockM, pol_w);
+          else
+            ptx::tma_load_2d(sA + stage * kABytes + c * Cfg::kAChunk, tA, &full[stage], k0, a_row,
+                             pol_w);
+          uint8_t* b_dst = sB + stage * Cfg::kBBytes + c * Cfg::kBChunk;
+          if (g.dbg & 1) continue;
+          int r = 0;
+          for (; r + 64 <= nrows; r += 64)
+            ptx::tma_load_2d(b_dst + r * kChunkK * 2, &tB->m64, &full[stage], k0, it.row0 + r,
+                             pol_x);
+          if (r + 32 <= nrows) {
+            ptx::tma_load_2d(b_dst + r * kChunkK * 2, &tB->m32, &full[stage], k0, it.row0 + r,
+                             pol_x);
+            r += 32;
+          }
+          if (r < nrows)
+            ptx::tma_load_2d(b_dst + r * kChunkK * 2, &tB->m16, &full[stage], k0, it.row0 + r,
+                             pol_x);
         }
-        if (r < nrows)
-          ptx::tma_load_2d(b_dst + r * kBlockK * 2, &tB->m16, &full[stage], kb * kBlockK,
-                           it.row0 + r, pol_x);
         if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
@@ -204,13 +227,18 @@ __global__ void __launch_bounds__(256, 1)
       for (int kb = 0; kb < KB; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
-        const uint32_t a0 = ptx::smem_u32(sA + stage * kABytes);
-        const uint32_t b0 = ptx::smem_u32(sB + stage * Cfg::kBBytes);
+        // descriptors of the stage's first chunk; the start-address field
+        // (addr >> 4) of later chunks / k-steps is a plain add (no carry:
+        // shared addresses stay below 256 KB)
+        const uint64_t da = ptx::umma_desc_sw128(ptx::smem_u32(sA + stage * kABytes));
+        const uint64_t db = ptx::umma_desc_sw128(ptx::smem_u32(sB + stage * Cfg::kBBytes));
 #pragma unroll
-        for (int kk = 0; kk < kBlockK / kUmmaK; ++kk)
-          ptx::mma_bf16(d, ptx::umma_desc_sw128(a0 + kk * kUmmaK * 2),
-                        ptx::umma_desc_sw128(b0 + kk * kUmmaK * 2), idesc,
-                        (kb | kk) != 0 ? 1u : 0u);
+        for (int c = 0; c < KCH; ++c)
+#pragma unroll
+          for (int kk = 0; kk < kChunkK / kUmmaK; ++kk)
+            ptx::mma_bf16(d, da + ((c * Cfg::kAChunk + kk * kUmmaK * 2) >> 4),
+                          db + ((c * Cfg::kBChunk + kk * kUmmaK * 2) >> 4), idesc,
+                          (kb | c | kk) != 0 ? 1u : 0u);
         ptx::mma_commit(&empty[stage]);
         if (++stage == STAGES) {
           stage = 0;
@@ -256,7 +284,7 @@ __global__ void __launch_bounds__(256, 1)
         for (int j = 0; j < 4; ++j) {
           const int tok = j * 8 + (lane >> 2);
           const int ch = lane & 3;
-          if (c0 + tok < it.len) {
+          if (c0 + tok < it.len && !(g.dbg & 2)) {
             const uint4 v = *reinterpret_cast<const uint4*>(stg + tok * 32 + ch * 8);
             int row = it.row0 + c0 + tok;
             if (tr.gemm && g.out_rows) row = g.out_rows[row];
@@ -300,34 +328,61 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int KCH>
 cudaError_t prepare_fused() {
-  return cudaFuncSetAttribute(fused_ffn_kernel<BN, STAGES>,
+  return cudaFuncSetAttribute(fused_ffn_kernel<BN, STAGES, KCH>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              FusedCfg<BN, STAGES>::kSmem);
+                              FusedCfg<BN, STAGES, KCH>::kSmem);
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int KCH>
 cudaError_t launch_fused(const CUtensorMap& w1, const RowMaps& xp, const CUtensorMap& w2,
                          const RowMaps& h, const FusedFfnArgs& g, int grid,
                          cudaStream_t stream) {
-  return launch_chain(fused_ffn_kernel<BN, STAGES>, dim3(grid), dim3(256),
-                      FusedCfg<BN, STAGES>::kSmem, stream, false, w1, xp, w2, h, g);
+  return launch_chain(fused_ffn_kernel<BN, STAGES, KCH>, dim3(grid), dim3(256),
+                      FusedCfg<BN, STAGES, KCH>::kSmem, stream, false, w1, xp, w2, h, g);
 }
 
 }  // namespace
 
+// MOE_FFN_KCH=1 selects the 64-deep stages (6 x 32 KB) for A/B experiments.
+int fused_kch() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MOE_FFN_KCH");
+    v = (e && atoi(e) == 1) ? 1 : 2;
+  }
+  return v;
+}
+
+cudaError_t fused_ffn_pair_prepare();
+bool fused_ffn_pair_enabled();
+cudaError_t launch_fused_ffn_pair(const CUtensorMap& tmW1, const RowMaps& xp,
+                                  const CUtensorMap& tmW2, const RowMaps& h,
+                                  const FusedFfnArgs& args, int sms, cudaStream_t stream);
+
 cudaError_t fused_ffn_prepare() {
-  cudaError_t e = prepare_fused<128, 6>();
+  cudaError_t e = fused_ffn_pair_prepare();
   if (e != cudaSuccess) return e;
-  return prepare_fused<256, 4>();
+  e = prepare_fused<128, 6, 1>();
+  if (e != cudaSuccess) return e;
+  if ((e = prepare_fused<128, 3, 2>()) != cudaSuccess) return e;
+  return prepare_fused<256, 4, 1>();
 }
 
 cudaError_t launch_fused_ffn(const CUtensorMap& tmW1, const RowMaps& xp, const CUtensorMap& tmW2,
                              const RowMaps& h, const FusedFfnArgs& args, int tile_n, int grid,
                              cudaStream_t stream) {
-  if (tile_n == 128) return launch_fused<128, 6>(tmW1, xp, tmW2, h, args, grid, stream);
-  if (tile_n == 256) return launch_fused<256, 4>(tmW1, xp, tmW2, h, args, grid, stream);
+  // CTA pairs (M = 256 UMMA) when both GEMMs have an even number of 128-row
+  // weight blocks
+  if (tile_n == 128 && fused_ffn_pair_enabled() && args.HD % 256 == 0 && args.TD % 256 == 0) {
+    cudaError_t e = launch_fused_ffn_pair(tmW1, xp, tmW2, h, args, grid, stream);
+    if (e != cudaErrorNotSupported) return e;
+  }
+  if (tile_n == 128 && fused_kch() == 2)
+    return launch_fused<128, 3, 2>(tmW1, xp, tmW2, h, args, grid, stream);
+  if (tile_n == 128) return launch_fused<128, 6, 1>(tmW1, xp, tmW2, h, args, grid, stream);
+  if (tile_n == 256) return launch_fused<256, 4, 1>(tmW1, xp, tmW2, h, args, grid, stream);
   return cudaErrorInvalidValue;
 }
 

@@ -138,12 +138,14 @@ struct FusedFfnArgs {
   int32_t* done2;           // [items] GEMM2 tiles finished (zeroed before launch)
   int lag;                  // items between an item's GEMM1 and GEMM2 tiles
   int discard_h;            // drop consumed H lines from L2 (no write-back)
+  int dbg;                  // experiments only (MOE_FFN_DBG): 1 = skip B loads, 2 = skip stores
+  int packed;               // tmW1/tmW2 address prepacked 128 x 64 tiles (launch_pack_tiles)
 };
-// One activation matrix (Xp or H) seen by TMA at three box heights: a B tile
-// of n rows (n % 16 == 0) is n/64 boxes of 64 rows plus at most one of 32 and
-// one of 16 -- 1-3 TMA issues per k-block instead of n/16.
+// One activation matrix (Xp or H) seen by TMA at four box heights: a B tile
+// of n rows (n % 8 == 0) is n/64 boxes of 64 rows plus at most one each of 32,
+// 16 and 8 -- a few TMA issues per k-block instead of n/16.
 struct RowMaps {
-  CUtensorMap m16, m32, m64;
+  CUtensorMap m8, m16, m32, m64;
 };
 cudaError_t fused_ffn_prepare();
 cudaError_t launch_fused_ffn(const CUtensorMap& tmW1, const RowMaps& xp, const CUtensorMap& tmW2,
@@ -190,6 +192,9 @@ cudaError_t launch_gather_rows(const __nv_bfloat16* X, const int32_t* order, int
                                int TD, __nv_bfloat16* Xp, cudaStream_t stream);
 cudaError_t launch_combine(const __nv_bfloat16* Yw, const int32_t* pos, int S, int k, int TD,
                            __nv_bfloat16* out, cudaStream_t stream);
+// row-major [rows, K] bf16 -> 128 x 64 tiles, 16 KB each, contiguous
+cudaError_t launch_pack_tiles(const __nv_bfloat16* src, __nv_bfloat16* dst, long rows, int K,
+                              cudaStream_t stream);
 cudaError_t launch_fill_segments(const int32_t* counts, int n_segments, int mod, int32_t* out,
                                  cudaStream_t stream);
 cudaError_t launch_fill_uniform_bf16(__nv_bfloat16* dst, int64_t n, uint64_t seed,

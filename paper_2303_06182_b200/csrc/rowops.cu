@@ -175,4 +175,30 @@ cudaError_t launch_fill_uniform_bf16(__nv_bfloat16* dst, int64_t n, uint64_t see
   return cudaGetLastError();
 }
 
+// Weight prepack: row-major [mblocks * 128, K] -> tiles of 128 rows x 64
+// columns, each 16 KB contiguous, tile (mb, kc) at tile index mb * (K/64) + kc.
+// One CTA per tile: 128 rows x 8 x 16 B.
+__global__ void pack_tiles_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, int K) {
+  const long tile = blockIdx.x;
+  const int kc_n = K / 64;
+  const long mb = tile / kc_n;
+  const int kc = static_cast<int>(tile % kc_n);
+  const int vrow = K / 8;  // uint4 per source row
+  for (int i = threadIdx.x; i < 128 * 8; i += blockDim.x) {
+    const int r = i >> 3, c = i & 7;
+    dst[tile * 1024 + i] = src[(mb * 128 + r) * vrow + kc * 8 + c];
+  }
+}
+
+cudaError_t launch_pack_tiles(const __nv_bfloat16* src, __nv_bfloat16* dst, long rows, int K,
+                              cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  if (rows % 128 || K % 64) return cudaErrorInvalidValue;
+  const long tiles = rows / 128 * (K / 64);
+  if (tiles > 0x7fffffffL) return cudaErrorInvalidValue;
+  pack_tiles_kernel<<<static_cast<unsigned>(tiles), 256, 0, stream>>>(
+      reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst), K);
+  return cudaGetLastError();
+}
+
 }  // namespace moe

@@ -82,7 +82,7 @@ class MoeLayer:
     def __init__(self, shape: LayerShape, max_tokens: int, mode: str = "dynamic",
                  capacity_factor: float = 1.0, weights=None, keep_logits: bool = False,
                  tile_n: int = 0, device: int | None = None, seed: int = SEED, fuse_combine: bool = False,
-                 split_ffn: bool = False, fuse_front: bool = False):
+                 split_ffn: bool = False, fuse_front: bool = False, keep_layout: bool = False):
         self.ctx = Context.get(device)
         dev = torch.device("cuda", self.ctx.device)
         TD, HD, E, k = shape.token_dim, shape.hidden_dim, shape.num_experts, shape.top_k
@@ -99,11 +99,15 @@ class MoeLayer:
         d = _capi.LayerDesc(max_tokens, TD, HD, E, k,
                             _capi.MOE_GATING_DYNAMIC if mode == "dynamic" else _capi.MOE_GATING_STATIC,
                             float(capacity_factor), int(tile_n), int(bool(keep_logits)), int(bool(fuse_combine)),
-                            int(bool(split_ffn)), int(bool(fuse_front)))
+                            int(bool(split_ffn)), int(bool(fuse_front)), int(bool(keep_layout)))
         h = C.c_void_p()
         check(self.ctx.lib.moe_layer_create(self.ctx.h, C.byref(d), _p(self.Wg), _p(self.W1),
                                             _p(self.W2), C.byref(h)))
         self.h = h
+
+    def repack(self, stream=None):
+        """Refresh the layer's packed copy of W1/W2 after in-place weight updates."""
+        check(self.ctx.lib.moe_layer_repack(self.h, _stream_ptr(stream)))
 
     def close(self):
         if getattr(self, "h", None):

@@ -236,6 +236,27 @@ def test_pipelined_host_batches_bitwise_equal_per_call(S, TD, HD, E, k):
     assert torch.equal(ring[0], outs[0]) and torch.equal(ring[1], outs[2])
 
 
+@pytest.mark.parametrize("S,TD,HD,E,k", [(1024, 256, 512, 16, 2), (16384, 1024, 4096, 512, 2)])
+def test_packed_weights_bitwise_equal_row_major_and_repack(S, TD, HD, E, k):
+    """The fused FFN's prepacked weight copy (default) gives the same bits as
+    streaming the caller's row-major weights (keep_layout), and
+    moe_layer_repack picks up in-place weight updates."""
+    shape = LayerShape(TD, HD, E, k)
+    w = make_weights(shape, seed=SEED)
+    x = make_tokens(S, TD, seed=SEED)
+    packed = MoeLayer(shape, S, weights=w)
+    plain = MoeLayer(shape, S, weights=w, keep_layout=True)
+    a, b = packed(x), plain(x)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    w[1].mul_(-1.0)  # in place: the packed copy is stale until repack
+    torch.cuda.synchronize()
+    packed.repack()
+    a2, b2 = packed(x), plain(x)
+    torch.cuda.synchronize()
+    assert torch.equal(a2, b2) and not torch.equal(a2, a)
+
+
 def test_repeat_forward_is_deterministic():
     layer, x, out, w, v = _run(4096, 256, 512, 64, 2)
     out2 = layer(x)
