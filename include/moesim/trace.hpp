@@ -2,12 +2,15 @@
 // reference's proj/include/moesim/trace.hpp:15-45 (same names, field names and
 // field order -- tests aggregate-initialise them, e.g. TokenAssignment{{e},{1.0}}).
 //
-// Only the types the dispatch path consumes are provided.  The reference's
-// trace I/O, synthetic generator and statistics (trace.hpp:52-96) are
-// simulator tooling outside this library's scope.
+// Besides the types: the synthetic generator, the JSON Lines trace files and
+// the invariant checker / load matrix of the reference (trace.hpp:52-88), so
+// generated or recorded routing can be replayed through the GPU layer
+// (tools/moesim_measure --trace).  The reference's split/sparsity statistics
+// and CSV export are simulator reporting, not provided.
 #pragma once
 
 #include <cstdint>
+#include <filesystem>
 #include <vector>
 
 #include <Eigen/Core>
@@ -65,5 +68,21 @@ struct LoadMatrix {
   Eigen::Index num_experts() const { return share.rows(); }
   Eigen::Index num_batches() const { return share.cols(); }
 };
+
+/// Checks every trace invariant (k distinct ids in [0, E), weights >= 0
+/// summing to 1, strictly increasing batch ids, non-empty batches); throws
+/// std::invalid_argument naming the batch/token of the first violation, with
+/// the reference's message text (trace.cpp:47-87).
+void validate(const TokenTrace& trace);
+
+/// JSON Lines: header {"num_experts","top_k","version":1}, then one line per
+/// batch.  load throws std::runtime_error (I/O, parse) or std::invalid_argument
+/// (invariants) with file:line context; save is byte-deterministic and writes
+/// the same bytes as the reference for the same trace.
+TokenTrace load_token_trace(const std::filesystem::path& path);
+void save_token_trace(const TokenTrace& trace, const std::filesystem::path& path);
+
+/// share(e, b) = fraction of batch b's k * seq_len slots routed to expert e.
+LoadMatrix aggregate_loads(const TokenTrace& trace);
 
 }  // namespace moesim

@@ -57,6 +57,9 @@ def ref_lib():
         _sig(lib.ref_contiguous_place, _I, _I, _I, _P)
         _sig(lib.ref_plan_dynamic_exchange, _I, _P, _I, _I, _I, _I, _P, _I64, _P, _P)
         _sig(lib.ref_gen_synthetic_trace, _I, _I, _I, _I, _I, _D, _D, _D, C.c_uint64, _P, _P)
+        _sig(lib.ref_save_synthetic_trace, _I, _I, _I, _I, _I, _D, _D, _D, C.c_uint64, C.c_char_p)
+        _sig(lib.ref_trace_roundtrip, _I, C.c_char_p, C.c_char_p, _P)
+        _sig(lib.ref_trace_loads, _I, C.c_char_p, _P, _I)
         _ref = lib
     return _ref
 
@@ -239,6 +242,33 @@ def ref_gen_synthetic_trace(E, k, B, S, skew, persistence, active_fraction, seed
     if rc:
         raise OracleError(ref_lib().ref_last_error().decode())
     return experts.reshape(B, S, k), weights.reshape(B, S, k)
+
+
+def ref_save_synthetic_trace(path, E, k, B, S, skew, persistence, active_fraction, seed):
+    rc = ref_lib().ref_save_synthetic_trace(E, k, B, S, skew, persistence, active_fraction, seed,
+                                            str(path).encode())
+    if rc:
+        raise OracleError(ref_lib().ref_last_error().decode())
+
+
+def ref_trace_roundtrip(in_path, out_path=""):
+    """(E, k, batches) of a trace file loaded by the reference; re-saved to
+    out_path when given.  Raises ValueError (invalid_argument) or OracleError."""
+    dims = np.zeros(3, np.int32)
+    rc = ref_lib().ref_trace_roundtrip(str(in_path).encode(), str(out_path).encode(), _ptr(dims))
+    if rc == 1:
+        raise ValueError(ref_lib().ref_last_error().decode())
+    if rc:
+        raise OracleError(ref_lib().ref_last_error().decode())
+    return tuple(int(v) for v in dims)
+
+
+def ref_trace_loads(path, E, B):
+    share = np.zeros(E * B, np.float64)
+    rc = ref_lib().ref_trace_loads(str(path).encode(), _ptr(share), E * B)
+    if rc:
+        raise OracleError(ref_lib().ref_last_error().decode())
+    return share.reshape(B, E).T
 
 
 # --------------------------------------------------------------- C restatement

@@ -277,4 +277,41 @@ int ref_gen_synthetic_trace(int E, int k, int B, int S, double skew, double pers
   });
 }
 
+// ---- trace files (trace.cpp:89-157) and load matrix (:158-172) -----------
+int ref_save_synthetic_trace(int E, int k, int B, int S, double skew, double persistence,
+                             double active_fraction, uint64_t seed, const char* path) {
+  return guarded([&] {
+    moesim::SyntheticSpec spec;
+    spec.num_experts = E;
+    spec.top_k = k;
+    spec.num_batches = B;
+    spec.seq_len = S;
+    spec.zipf_skew = skew;
+    spec.persistence = persistence;
+    spec.active_fraction = active_fraction;
+    spec.seed = seed;
+    moesim::save_token_trace(moesim::gen_synthetic_trace(spec), path);
+  });
+}
+
+int ref_trace_roundtrip(const char* in_path, const char* out_path, int* dims) {
+  return guarded([&] {
+    const auto tr = moesim::load_token_trace(in_path);
+    dims[0] = tr.num_experts;
+    dims[1] = tr.top_k;
+    dims[2] = tr.num_batches();
+    if (out_path && *out_path) moesim::save_token_trace(tr, out_path);
+  });
+}
+
+int ref_trace_loads(const char* path, double* share, int cap) {
+  return guarded([&] {
+    const auto L = moesim::aggregate_loads(moesim::load_token_trace(path));
+    const long n = static_cast<long>(L.share.rows()) * L.share.cols();
+    if (n > cap) throw std::runtime_error("load buffer too small");
+    for (long j = 0; j < L.share.cols(); ++j)
+      for (long i = 0; i < L.share.rows(); ++i) share[j * L.share.rows() + i] = L.share(i, j);
+  });
+}
+
 }  // extern "C"

@@ -18,6 +18,17 @@ CSRC = os.path.join(HERE, "csrc")
 HOST = os.path.join(HERE, "host")
 INCLUDE = os.path.join(ROOT, "include")
 EIGEN_MIN = os.path.join(ROOT, "third_party", "eigen_min")
+
+
+def _json_dir() -> str:
+    """nlohmann json 3.11 header shipped in the image (the reference's JSON
+    dependency; used by the trace-file I/O)."""
+    import sys
+    for base in sys.path:
+        d = os.path.join(base or ".", "include", "cudnn_frontend", "thirdparty", "nlohmann")
+        if os.path.exists(os.path.join(d, "json.hpp")):
+            return d
+    raise RuntimeError("nlohmann json.hpp not found in the image")
 LIB = os.path.join(HERE, "libmoe_b200.so")
 LIBCXX = os.path.join(HERE, "libmoesim_b200.so")
 
@@ -59,7 +70,7 @@ def build_cxx(force: bool = False) -> str:
     if not force and not _stale(LIBCXX, deps):
         return LIBCXX
     cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", f"-I{INCLUDE}",
-           f"-I{EIGEN_MIN}", "-o", LIBCXX, *srcs, f"-L{HERE}", "-lmoe_b200",
+           f"-I{EIGEN_MIN}", f"-isystem{_json_dir()}", "-o", LIBCXX, *srcs, f"-L{HERE}", "-lmoe_b200",
            "-Wl,-rpath,$ORIGIN"]
     _run(cmd)
     return LIBCXX

@@ -1004,15 +1004,14 @@ int moe_ffn_create(moe_ctx* ctx, const moe_ffn_desc* desc, const void* W1, const
   }();
   if (pack_env && F->tile_n == 128) {
     const size_t n1 = (size_t)d.num_experts * HD * TD;
-    cudaError_t e = cudaSuccess;
     if (F->w1p.reserve(n1) == MOE_OK && F->w2p.reserve(n1) == MOE_OK &&
         encode_bf16(&F->tmW1p, F->w1p.p, n1 / 64, 64, 128) == MOE_OK &&
         encode_bf16(&F->tmW2p, F->w2p.p, n1 / 64, 64, 128) == MOE_OK &&
-        (e = launch_pack_tiles(static_cast<const __nv_bfloat16*>(W1), F->w1p.p,
-                               (long)d.num_experts * HD, TD, nullptr)) == cudaSuccess &&
-        (e = launch_pack_tiles(static_cast<const __nv_bfloat16*>(W2), F->w2p.p,
-                               (long)d.num_experts * TD, HD, nullptr)) == cudaSuccess &&
-        (e = cudaDeviceSynchronize()) == cudaSuccess) {
+        launch_pack_tiles(static_cast<const __nv_bfloat16*>(W1), F->w1p.p,
+                          (long)d.num_experts * HD, TD, nullptr) == cudaSuccess &&
+        launch_pack_tiles(static_cast<const __nv_bfloat16*>(W2), F->w2p.p,
+                          (long)d.num_experts * TD, HD, nullptr) == cudaSuccess &&
+        cudaDeviceSynchronize() == cudaSuccess) {
       F->packed = true;
     } else {
       F->w1p.release();

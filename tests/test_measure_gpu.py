@@ -61,3 +61,29 @@ def test_measure_with_expert_cache_and_gate(tmp_path):
     out2, _ = _run(tmp_path, "--experts", "8", "--topk", "1", "--tokens", "300", "--batches", "2",
                    "--token-dim", "128", "--hidden-dim", "256", "--mode", "dynamic", "--gate", "--verify", "4")
     assert _summary(out2)["verify_rel_fro"] < 1e-2
+
+
+def test_measure_replays_trace_file(tmp_path):
+    """--trace: a JSON Lines routing trace (reference format) with batches of
+    different lengths drives the GPU layer; --save-trace writes back the same
+    bytes; the fp32 check uses the replayed routing."""
+    rng = __import__("numpy").random.default_rng(3)
+    E, k, lens = 12, 2, [200, 37, 256]
+    lines = [json.dumps({"num_experts": E, "top_k": k, "version": 1}, separators=(",", ":"), sort_keys=True)]
+    for b, n in enumerate(lens):
+        toks = []
+        for _ in range(n):
+            e = rng.choice(E, size=k, replace=False).tolist()
+            toks.append({"e": e, "w": [0.75, 0.25]})
+        lines.append(json.dumps({"batch_id": b, "tokens": toks}, separators=(",", ":"), sort_keys=True))
+    trace = tmp_path / "t.jsonl"
+    trace.write_text("\n".join(lines) + "\n")
+    saved = tmp_path / "saved.jsonl"
+    out, text = _run(tmp_path, "--trace", str(trace), "--save-trace", str(saved), "--token-dim", "128",
+                     "--hidden-dim", "256", "--mode", "dynamic", "--verify", "5")
+    s = _summary(out)
+    assert s["num_batches"] == 3
+    assert s["verify_rel_fro"] < 1e-2
+    assert saved.read_bytes() == trace.read_bytes()
+    man = json.load(open(out / "manifest.json"))
+    assert "file:" in json.dumps(man)

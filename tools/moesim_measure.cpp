@@ -13,6 +13,9 @@
 //       --token-dim 2048 --hidden-dim 8192 --mode both --capacity-factor 1
 //       --zipf 1.2 --persist 0.9 --active-frac 0.75 --cache-size 0 --out out/
 //   --gate        route with the layer's gate instead of the trace
+//   --trace F     replay the routing of a JSON Lines trace file (reference
+//                 format, load_token_trace); E, k and the batches come from it
+//   --save-trace F  write the routing trace used (generated or loaded)
 //   --verify N    check N tokens of the first batch (dynamic mode) against an
 //                 fp32 host reference
 #include <algorithm>
@@ -46,6 +49,7 @@ struct Options {
   std::string out = "measure_out";
   bool gate = false;
   int verify = 0;
+  std::string trace, save_trace;
 };
 
 [[noreturn]] void usage(const std::string& msg) {
@@ -77,6 +81,8 @@ Options parse(int argc, char** argv) {
     else if (a == "--out") o.out = val();
     else if (a == "--gate") o.gate = true;
     else if (a == "--verify") o.verify = std::stoi(val());
+    else if (a == "--trace") o.trace = val();
+    else if (a == "--save-trace") o.save_trace = val();
     else usage("unknown option " + a);
   }
   if (o.mode != "static" && o.mode != "dynamic" && o.mode != "both")
@@ -124,8 +130,20 @@ struct ModeResult {
 }  // namespace
 
 int main(int argc, char** argv) {
-  const Options o = parse(argc, argv);
+  Options o = parse(argc, argv);
   try {
+    // a replayed trace fixes E, k, the batch count and the tokens per batch
+    TokenTrace trace;
+    std::vector<int> seq;
+    if (!o.trace.empty()) {
+      if (o.gate) usage("--trace and --gate are exclusive");
+      trace = load_token_trace(o.trace);
+      o.experts = trace.num_experts;
+      o.topk = trace.top_k;
+      o.batches = trace.num_batches();
+      o.tokens = 0;
+      for (const Batch& b : trace.batches) o.tokens = std::max(o.tokens, b.seq_len());
+    }
     const fs::path out_dir(o.out);
     fs::create_directories(out_dir);
     gpu::Context ctx(0);
@@ -144,9 +162,8 @@ int main(int argc, char** argv) {
                            r3 / std::sqrt(float(HD)));
     gpu::fill_uniform_bf16(ctx, X.get(), static_cast<std::int64_t>(S) * TD, o.seed, 1, r3);
 
-    // routing trace (reference generator) -> device idx / w per batch
-    TokenTrace trace;
-    if (!o.gate) {
+    // routing trace (reference generator or file) -> device idx / w per batch
+    if (!o.gate && o.trace.empty()) {
       SyntheticSpec spec;
       spec.num_experts = E;
       spec.top_k = k;
@@ -158,18 +175,22 @@ int main(int argc, char** argv) {
       spec.seed = o.seed;
       trace = gen_synthetic_trace(spec);
     }
+    for (int b = 0; b < o.batches; ++b)
+      seq.push_back(o.gate ? S : trace.batches[static_cast<std::size_t>(b)].seq_len());
+    if (!o.save_trace.empty() && !o.gate) save_token_trace(trace, o.save_trace);
     gpu::DeviceBuffer idx(ctx, static_cast<std::size_t>(o.batches) * S * k * 4);
     gpu::DeviceBuffer wts(ctx, static_cast<std::size_t>(o.batches) * S * k * 4);
     if (!o.gate) {
       std::vector<std::int32_t> hi(static_cast<std::size_t>(o.batches) * S * k);
       std::vector<float> hw(hi.size());
-      std::size_t i = 0;
-      for (const Batch& b : trace.batches)
-        for (const TokenAssignment& ta : b.tokens)
+      for (std::size_t b = 0; b < trace.batches.size(); ++b) {
+        std::size_t i = b * static_cast<std::size_t>(S) * k;  // batch b at a fixed stride
+        for (const TokenAssignment& ta : trace.batches[b].tokens)
           for (int j = 0; j < k; ++j, ++i) {
             hi[i] = ta.experts[static_cast<std::size_t>(j)];
             hw[i] = static_cast<float>(ta.weights[static_cast<std::size_t>(j)]);
           }
+      }
       gpu::copy(ctx, idx.get(), hi.data(), hi.size() * 4, gpu::CopyKind::kHostToDevice);
       gpu::copy(ctx, wts.get(), hw.data(), hw.size() * 4, gpu::CopyKind::kHostToDevice);
     }
@@ -195,7 +216,8 @@ int main(int argc, char** argv) {
       layer.enable_timing(o.batches);
       auto run = [&](int b) {
         if (o.gate) layer.forward(X.get(), S, Y.get(), stream.get());
-        else layer.forward_routed(X.get(), batch_idx(b), batch_w(b), S, Y.get(), stream.get());
+        else layer.forward_routed(X.get(), batch_idx(b), batch_w(b), seq[static_cast<std::size_t>(b)], Y.get(),
+                                  stream.get());
       };
       run(0);  // warm-up
       stream.synchronize();
@@ -221,7 +243,7 @@ int main(int argc, char** argv) {
         run(0);
         stream.synchronize();
         const moe_layer_view vv = layer.view();
-        const int n = std::min(o.verify, S);
+        const int n = std::min(o.verify, seq[0]);
         std::vector<std::int32_t> hidx(static_cast<std::size_t>(n) * k);
         std::vector<float> hw(hidx.size());
         gpu::copy(ctx, hidx.data(), o.gate ? vv.idx : batch_idx(0), hidx.size() * 4,
@@ -275,7 +297,8 @@ int main(int argc, char** argv) {
         for (int b = 0; b < o.batches; ++b) {
           const auto t0 = std::chrono::steady_clock::now();
           if (o.gate) cache.forward(X.get(), S, Y.get(), stream.get());
-          else cache.forward_routed(X.get(), batch_idx(b), batch_w(b), S, Y.get(), stream.get());
+          else cache.forward_routed(X.get(), batch_idx(b), batch_w(b), seq[static_cast<std::size_t>(b)], Y.get(),
+                                    stream.get());
           stream.synchronize();
           cached_total += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
           const auto st = cache.stats();
@@ -337,7 +360,8 @@ int main(int argc, char** argv) {
       csv.row(std::string("global"), acc, hit, mis, rate, worst, res["dynamic"].transfer);
       outputs.push_back("cache.csv");
     }
-    const std::int64_t total_tokens = static_cast<std::int64_t>(S) * o.batches;
+    std::int64_t total_tokens = 0;
+    for (int n : seq) total_tokens += n;
     {
       Csv csv(out_dir / "summary.csv");
       csv.row("metric", "value");
@@ -362,7 +386,7 @@ int main(int argc, char** argv) {
         << ", \"hidden_dim\": " << HD << ", \"mode\": \"" << o.mode << "\", \"capacity_factor\": "
         << num(o.capacity_factor) << ", \"zipf\": " << num(o.zipf) << ", \"persist\": " << num(o.persist)
         << ", \"active_frac\": " << num(o.active_frac) << ", \"cache_size\": " << o.cache_size
-        << ", \"routing\": \"" << (o.gate ? "gate" : "trace") << "\"},\n  \"outputs\": [";
+        << ", \"routing\": \"" << (o.gate ? "gate" : o.trace.empty() ? "synthetic" : "file:" + o.trace) << "\"},\n  \"outputs\": [";
       for (std::size_t i = 0; i < outputs.size(); ++i) m << (i ? ", " : "") << '"' << outputs[i] << '"';
       m << "]\n}\n";
     }
