@@ -203,23 +203,23 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle.cpu_layer import cpu_layer_sample
+    from oracle.cpu_layer import CpuLayer, cpu_layer_bench
 
     S, TD, HD, E, k, mode, C, desc = WORKLOADS[args.workload]
+    L = CpuLayer(S, TD, HD, E, k)
     for _ in range(max(0, min(args.warmup, 1))):
-        cpu_layer_sample(S, TD, HD, E, k, n_sample_experts=2)
+        L.run()
+    # each step: full layer passes until >= 10 s of CPU work, median pass
     vals, secs = [], []
     r = None
     for _ in range(max(1, min(args.steps, 3))):
-        r = cpu_layer_sample(S, TD, HD, E, k)
+        r = cpu_layer_bench(S, TD, HD, E, k, min_seconds=10.0, layer=L)
         vals.append(r["tokens_per_s"])
         secs.append(r["seconds_per_layer"])
     vals.sort()
     v = vals[len(vals) // 2]
     secs.sort()
-    sample = (f"full-batch gate/top-k/dispatch/combine + expert FFN for experts 0..7 "
-              f"({r['sampled_slots']}/{r['total_slots']} slots) scaled to all slots; "
-              f"dispatch = {r['dispatch_impl']}; numpy/OpenBLAS fp32")
+    sample = r["sample"]
     line = {
         "metric": "MoE-layer tokens/s (dynamic gating)", "value": v, "unit": "tokens/s",
         "impl": "reference", "n_gpus": world, "steps": len(vals), "warmup": min(args.warmup, 1),
@@ -585,14 +585,11 @@ def run_b200(args):
     t_roof, F, B = layer_roofline(S, TD, HD, E, k, active, hbm_gbs, tflops)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        from oracle.cpu_layer import cpu_layer_sample
+        from oracle.cpu_layer import cpu_layer_bench
 
-        r = cpu_layer_sample(S, TD, HD, E, k)
+        r = cpu_layer_bench(S, TD, HD, E, k, min_seconds=10.0)
         cpu = {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": r["cores"], "kind": "port",
-               "sample": (f"full-batch gate/top-k/dispatch/combine + expert FFN for experts 0..7 "
-                          f"({r['sampled_slots']}/{r['total_slots']} slots) scaled to all slots; dispatch = "
-                          f"{r['dispatch_impl']}; numpy/OpenBLAS fp32; {r['measured_cpu_seconds']:.1f} s measured"),
-               "breakdown_s": r["breakdown_s"]}
+               "sample": r["sample"], "breakdown_s": r["breakdown_s"]}
     line = {
         "metric": "MoE-layer tokens/s (dynamic gating)" if mode == "dynamic" else "MoE-layer tokens/s (static gating)",
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
