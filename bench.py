@@ -238,12 +238,18 @@ def run_reference(args):
 def run_ep(args, world, rank, local):
     """N > 1: expert parallelism.  E/N experts per GPU (placement: the
     reference's greedy policy on a calibration routing histogram, or
-    contiguous), S tokens per GPU (weak scaling), NCCL all-to-all over NVLink
-    for the count exchange and the variable payload exchange."""
+    contiguous), S tokens per GPU (weak scaling).  Exchange (--ep-transport):
+      p2p   (default) the layer's own kernels over NVLink peer memory
+            (moe_ep_*): counts published into every peer's window, token rows
+            gathered straight into the owner's receive buffer, outputs read
+            back by the combine -- no host sync, the step is one CUDA graph
+      nccl  count all-to-all + host sync + variable payload all-to-all over
+            NCCL (torch.distributed), the comparison path"""
     import numpy as np
     import torch
 
-    from paper_2303_06182_b200.ep import ExpertParallelMoE, KernelBackend, Placement, Transport
+    from paper_2303_06182_b200.ep import (ExpertParallelMoE, KernelBackend, PeerExpertParallelMoE,
+                                          Placement, Transport)
     from paper_2303_06182_b200.layer import Context, LayerShape, make_tokens, make_weights
 
     S, TD, HD, E, k, mode, C, desc = WORKLOADS[args.workload]
@@ -275,16 +281,30 @@ def run_ep(args, world, rank, local):
     W1l, W2l = W1[loc].contiguous(), W2[loc].contiguous()
     del W1, W2
     torch.cuda.empty_cache()
-    be = KernelBackend(ctx, shape, Wg, W1l, W2l, S, S * k * world, tile_n=args.tile_n)
-    layer = ExpertParallelMoE(pl, k, be, Transport(), rank)
+    p2p = args.ep_transport == "p2p"
+    if p2p:
+        layer = PeerExpertParallelMoE(ctx, pl, shape, Wg, W1l, W2l, S, rank)
+        del W1l, W2l  # the layer keeps its own tile-packed copy
+        torch.cuda.empty_cache()
+        be = None
+        fwd = lambda xx, st, out=None: layer.forward(xx, st, out=out, graph=not args.no_graph)  # noqa: E731
+        check = layer.check_errors
+        n_launch = 8  # gate, route, publish, dispatch, recv, FFN, done, combine
+    else:
+        be = KernelBackend(ctx, shape, Wg, W1l, W2l, S, S * k * world, tile_n=args.tile_n)
+        layer = ExpertParallelMoE(pl, k, be, Transport(), rank)
+        fwd = lambda xx, st, out=None: layer.forward(xx, st)  # noqa: E731
+        check = be.check_errors
+        n_launch = 9
     stream = torch.cuda.Stream()
     stream.wait_stream(torch.cuda.current_stream())  # inputs were written on the current stream
+    out_buf = torch.empty_like(x)
     K, W = args.steps, args.warmup
     with torch.cuda.stream(stream):
         for _ in range(W):
-            out = layer.forward(x, stream)
+            out = fwd(x, stream, out_buf)
     stream.synchronize()
-    be.check_errors(stream)
+    check(stream)
     sampler = ClockSampler(local) if not args.no_clocks else None
     if sampler:
         sampler.start()
@@ -299,7 +319,7 @@ def run_ep(args, world, rank, local):
         ev0.record(stream)
         for i in range(K):
             step_ev[i].record(stream)
-            out = layer.forward(x, stream)
+            out = fwd(x, stream, out_buf)
         step_ev[K].record(stream)
         ev1.record(stream)
     stream.synchronize()
@@ -311,11 +331,20 @@ def run_ep(args, world, rank, local):
     p50 = max_over_ranks(float(np.median(steps)), world)
     if sampler:
         sampler.stop()
-    recv_rows = layer.last["recv_rows"]
-    sent_off = int(layer.last["send_counts"].sum()) - int(layer.last["send_counts"][rank].sum())
+    check(stream)
+    if p2p:
+        v = layer.view(S)
+        cnt = v["counts"].cpu().numpy().reshape(world, E // world).sum(1)
+        recv_rows = v["recv_rows"]
+        sent_off = int(cnt.sum() - cnt[rank])
+    else:
+        recv_rows = layer.last["recv_rows"]
+        sent_off = int(layer.last["send_counts"].sum()) - int(layer.last["send_counts"][rank].sum())
     # e2e: pinned host tokens in, host output out, copies inside the timed region
     xh = x.cpu().pin_memory()
     oh = torch.empty_like(xh).pin_memory()
+    xd = torch.empty_like(x)
+    od = torch.empty_like(x)
     Ke = max(3, min(K, args.e2e_steps))
     barrier(world)
     torch.cuda.synchronize()
@@ -324,20 +353,24 @@ def run_ep(args, world, rank, local):
     with torch.cuda.stream(stream):
         e0.record(stream)
         for _ in range(Ke):
-            xd = xh.to("cuda", non_blocking=True)
-            o = layer.forward(xd, stream)
+            xd.copy_(xh, non_blocking=True)
+            o = fwd(xd, stream, od)
             oh.copy_(o, non_blocking=True)
         e1.record(stream)
     stream.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / Ke, world)
-    be.check_errors(stream)
+    check(stream)
     if rank != 0:
-        be.close()
+        (layer if p2p else be).close()
         return
     ms = elapsed / K
     El = E // world
     wbytes = El * 2 * TD * HD * 2
     achieved = wbytes / (ms * 1e-3) / 1e9
+    xbytes = 2 * sent_off * TD * 2  # token rows out + expert outputs back, off-GPU
+    transport = ("NVLink peer memory: count publish + gather fused with the payload all-to-all + "
+                 "return fused with the combine, one CUDA graph per step" if p2p else
+                 "NCCL all-to-all over NVLink, count exchange + host sync + payload")
     line = {
         "metric": "MoE-layer tokens/s (dynamic gating)", "value": world * S / (ms * 1e-3), "unit": "tokens/s",
         "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms, "p50_ms": p50,
@@ -345,23 +378,27 @@ def run_ep(args, world, rank, local):
         "data": "synthetic (counter-hash uniform tokens; random-init experts, std 1/sqrt(fan-in))",
         "config": {"workload": desc + " -- expert parallel", "S_per_gpu": S, "TD": TD, "HD": HD, "E": E,
                    "top_k": k, "gating": mode, "experts_per_gpu": El, "placement": args.placement,
-                   "parallelism": f"ep{world} (NCCL all-to-all over NVLink, count exchange + payload)",
+                   "parallelism": f"ep{world} ({transport})", "ep_transport": args.ep_transport,
                    "l2": "no flush: per-step local expert weights %.2f GB >> 126 MB L2" % (wbytes / 1e9)},
         "roofline": {"kernel": "whole EP step: local expert weights streamed once per step", "bound": "hbm",
                      "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s", "frac": achieved / hbm_gbs,
                      "peak_kind": peak_kind, "traffic": None},
         "a2a": {"rows_received_rank0": recv_rows, "rows_sent_offrank_rank0": sent_off,
-                "payload_bytes_offrank_per_direction": sent_off * TD * 2},
-        "gpu_launches": 9 * K,
+                "payload_bytes_offrank_per_direction": sent_off * TD * 2,
+                "exchange_bytes_offrank_per_step": xbytes,
+                "exchange_gbs_over_whole_step": xbytes / (ms * 1e-3) / 1e9,
+                "nvlink_peak_gbs_per_direction": 900.0},
+        "gpu_launches": n_launch * K,
         "e2e": {"value": world * S / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": S * TD * 2, "d2h_bytes_per_step": S * TD * 2,
-                "api": "ExpertParallelMoE.forward over the C ABI (pinned host in/out)"},
+                "api": ("PeerExpertParallelMoE.forward (moe_ep_forward_graph)" if p2p else
+                        "ExpertParallelMoE.forward over the C ABI") + " (pinned host in/out)"},
         "cpu_baseline": None,
         "clocks": sampler.summary() if sampler else None,
         "gpu": torch.cuda.get_device_name(local),
     }
     print(json.dumps(line), flush=True)
-    be.close()
+    (layer if p2p else be).close()
 
 
 def run_cache(args):
@@ -648,6 +685,8 @@ def main():
     ap.add_argument("--json-out", default="")
     ap.add_argument("--replicas", action="store_true", help="N>1: full replicas instead of EP")
     ap.add_argument("--placement", default="greedy", choices=["greedy", "contiguous"])
+    ap.add_argument("--ep-transport", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1 exchange: NVLink peer memory (fused kernels) or NCCL all-to-all")
     ap.add_argument("--cache-slots", type=int, default=0, help="mt-cache: GPU slots (default E/4)")
     ap.add_argument("--tokens", type=int, default=0, help="override tokens per step (mt-cache)")
     ap.add_argument("--fuse-combine", action="store_true", help="combine in the GEMM2 epilogue (A/B)")

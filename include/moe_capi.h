@@ -58,7 +58,8 @@ typedef enum moe_status {
   MOE_ERR_CUDA = 2,             /* CUDA runtime / driver failure */
   MOE_ERR_UNSUPPORTED = 3,      /* shape outside what the kernels handle */
   MOE_ERR_OUT_OF_MEMORY = 4,
-  MOE_ERR_EXPERT_RANGE = 5      /* an expert id outside [0, E) (UB in the reference) */
+  MOE_ERR_EXPERT_RANGE = 5,     /* an expert id outside [0, E) (UB in the reference) */
+  MOE_ERR_PEER_TIMEOUT = 6      /* expert parallelism: a peer rank never signalled */
 } moe_status;
 
 typedef enum moe_gating_mode {
@@ -321,6 +322,86 @@ int moe_route_dynamic_keyed(moe_ctx* ctx, const int32_t* expert_idx, int S, int 
 int moe_fill_segments(moe_ctx* ctx, const int32_t* counts, int n_segments, int mod, int32_t* out,
                       void* stream);
 
+/* ---------------------------------------------------------------- EP over peer memory
+ *
+ * The expert-parallel layer with the exchange done by the layer's own kernels
+ * through NVLink peer memory (CUDA IPC mappings of one "window" per rank)
+ * instead of NCCL: one object per rank (one process per GPU).  Per forward:
+ *
+ *   gate -> route keyed by (device, local expert)            (local)
+ *   publish: my per-key slot counts -> every peer's window    (size phase,
+ *            exchange.cpp:100-104), then a release flag per peer
+ *   dispatch: wait for every rank's counts, compute each row's destination
+ *            row at its device (rows land grouped by local expert, then by
+ *            source rank, then by slot -- the single-GPU order), gather the
+ *            token row and store it straight into the peer's receive buffer
+ *            (payload phase, exchange.cpp:106-114) -- gather and all-to-all
+ *            fused, no staging copy
+ *   recv:    wait for every sender, build the FFN work list from the count
+ *            matrix (no host round trip)
+ *   FFN:     the fused tcgen05 FFN over the received rows (gate weight applied)
+ *   done:    release flag to every peer
+ *   combine: wait for every peer's FFN, each token sums its k expert outputs
+ *            read straight from the peers' output buffers (return all-to-all
+ *            and combine fused), in slot order j
+ *
+ * No host synchronisation: the whole forward is stream-ordered and can be
+ * captured in a CUDA graph (moe_ep_forward_graph).  Every rank must call
+ * forward the same number of times (a collective).  Waits time out after
+ * ~20 s (MOE_EP_TIMEOUT_MS) and report MOE_ERR_PEER_TIMEOUT through
+ * moe_ep_check_errors instead of hanging the device.
+ *
+ * Setup: moe_ep_create on every rank, exchange the MOE_EP_HANDLE_BYTES
+ * handles (any host transport: torch.distributed all_gather_object, MPI, a
+ * file), then moe_ep_connect with all handles in rank order. */
+#define MOE_EP_MAX_RANKS 8
+#define MOE_EP_HANDLE_BYTES 64
+
+typedef struct moe_ep moe_ep;
+typedef struct moe_ep_desc {
+  int rank;          /* this process's rank, 0 <= rank < world_size */
+  int world_size;    /* D <= MOE_EP_MAX_RANKS; E % D == 0 */
+  int max_tokens;    /* S upper bound per rank per forward */
+  int token_dim;     /* TD: multiple of 128 */
+  int hidden_dim;    /* HD: multiple of 128 */
+  int num_experts;   /* global E <= 512 */
+  int top_k;         /* k <= 8 */
+  int max_recv_rows; /* receive capacity; 0 = world_size * max_tokens * top_k (worst case) */
+} moe_ep_desc;
+
+/* Wg [E, TD] (all experts, replicated), W1_local [E/D, HD, TD], W2_local
+ * [E/D, TD, HD]: this rank's experts in increasing global id (bf16, device;
+ * snapshotted into the FFN's tile-packed copy).  device_of: HOST int32 [E],
+ * expert -> rank, exactly E/D per rank (the reference's Placement,
+ * include/moesim/balance.hpp:12-21). */
+int moe_ep_create(moe_ctx* ctx, const moe_ep_desc* desc, const void* Wg, const void* W1_local,
+                  const void* W2_local, const int32_t* device_of, moe_ep** out);
+int moe_ep_destroy(moe_ep* ep);
+/* This rank's window handle (MOE_EP_HANDLE_BYTES bytes). */
+int moe_ep_get_handle(moe_ep* ep, void* handle);
+/* handles: world_size * MOE_EP_HANDLE_BYTES, in rank order. */
+int moe_ep_connect(moe_ep* ep, const void* handles);
+/* X [S, TD] bf16 (this rank's tokens) -> out [S, TD] bf16. */
+int moe_ep_forward(moe_ep* ep, const void* X, int S, void* out, void* stream);
+int moe_ep_forward_graph(moe_ep* ep, const void* X, int S, void* out, void* stream);
+/* Synchronises `stream`; MOE_ERR_PEER_TIMEOUT / MOE_ERR_EXPERT_RANGE /
+ * MOE_ERR_UNSUPPORTED (receive capacity exceeded) from the device flags. */
+int moe_ep_check_errors(moe_ep* ep, void* stream);
+
+typedef struct moe_ep_view {
+  int32_t* idx;        /* [S*k] top-k expert ids (global) */
+  float* w;            /* [S*k] */
+  int32_t* counts;     /* [E] slots per key (key = device * E/D + local index) */
+  int32_t* counts_all; /* [D, E] every rank's counts (this rank's window) */
+  int32_t* dest;       /* [S*k] sorted row -> (device << 28) | row at that device */
+  int32_t* order;      /* [S*k] sorted row -> slot */
+  void* recv_x;        /* bf16 [max_recv_rows, TD] */
+  void* recv_y;        /* bf16 [max_recv_rows, TD] */
+  float* recv_w;       /* [max_recv_rows] */
+  int32_t* n_items;    /* [1] */
+  int max_recv_rows;
+} moe_ep_view;
+int moe_ep_get_view(moe_ep* ep, moe_ep_view* view);
 
 /* exchange.cpp:95-120, payload phase, as slot counts: counts[src*D + dst] =
  * number of assignment slots whose token lives on src (token t on t % D,

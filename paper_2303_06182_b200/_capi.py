@@ -18,6 +18,9 @@ MOE_ERR_CUDA = 2
 MOE_ERR_UNSUPPORTED = 3
 MOE_ERR_OUT_OF_MEMORY = 4
 MOE_ERR_EXPERT_RANGE = 5
+MOE_ERR_PEER_TIMEOUT = 6
+MOE_EP_MAX_RANKS = 8
+MOE_EP_HANDLE_BYTES = 64
 
 MOE_GATING_STATIC = 0
 MOE_GATING_DYNAMIC = 1
@@ -37,6 +40,8 @@ EXPORTED = [
     "moe_device_alloc", "moe_device_free", "moe_host_alloc", "moe_host_free", "moe_memcpy",
     "moe_stream_create", "moe_stream_destroy", "moe_stream_synchronize",
     "moe_layer_forward_host_batches", "moe_layer_repack",
+    "moe_ep_create", "moe_ep_destroy", "moe_ep_get_handle", "moe_ep_connect", "moe_ep_forward",
+    "moe_ep_forward_graph", "moe_ep_check_errors", "moe_ep_get_view",
 ]
 
 
@@ -75,6 +80,20 @@ class LayerView(C.Structure):
         ("dropped", C.c_void_p), ("n_dropped", C.c_void_p), ("xp", C.c_void_p),
         ("h", C.c_void_p), ("yw", C.c_void_p), ("n_items", C.c_void_p), ("rows", C.c_int),
         ("capacity", C.c_int), ("tile_n", C.c_int),
+    ]
+
+
+class EpDesc(C.Structure):
+    _fields_ = [("rank", C.c_int), ("world_size", C.c_int), ("max_tokens", C.c_int),
+                ("token_dim", C.c_int), ("hidden_dim", C.c_int), ("num_experts", C.c_int),
+                ("top_k", C.c_int), ("max_recv_rows", C.c_int)]
+
+
+class EpView(C.Structure):
+    _fields_ = [
+        ("idx", C.c_void_p), ("w", C.c_void_p), ("counts", C.c_void_p), ("counts_all", C.c_void_p),
+        ("dest", C.c_void_p), ("order", C.c_void_p), ("recv_x", C.c_void_p), ("recv_y", C.c_void_p),
+        ("recv_w", C.c_void_p), ("n_items", C.c_void_p), ("max_recv_rows", C.c_int),
     ]
 
 
@@ -136,6 +155,14 @@ def load(path: str = LIB_PATH):
     _sig(lib.moe_cache_stats, I, P, P, P)
     _sig(lib.moe_cache_resident, I, P, P, P)
     _sig(lib.moe_layer_forward_routed, I, P, P, P, P, I, P, P)
+    _sig(lib.moe_ep_create, I, P, C.POINTER(EpDesc), P, P, P, P, C.POINTER(P))
+    _sig(lib.moe_ep_destroy, I, P)
+    _sig(lib.moe_ep_get_handle, I, P, P)
+    _sig(lib.moe_ep_connect, I, P, P)
+    _sig(lib.moe_ep_forward, I, P, P, I, P, P)
+    _sig(lib.moe_ep_forward_graph, I, P, P, I, P, P)
+    _sig(lib.moe_ep_check_errors, I, P, P)
+    _sig(lib.moe_ep_get_view, I, P, C.POINTER(EpView))
     _lib = lib
     return lib
 

@@ -49,16 +49,31 @@ def _run(cmd, cwd=None):
 
 
 def build_cuda(force: bool = False, verbose_ptxas: bool = False) -> str:
+    """Each .cu compiles to its own object (in parallel, only the stale ones),
+    then one nvcc link into the shared library."""
+    from concurrent.futures import ThreadPoolExecutor
+
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    deps = srcs + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + [
+    common = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + [
         os.path.join(INCLUDE, "moe_capi.h"), __file__]
-    if not force and not _stale(LIB, deps):
-        return LIB
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           "-cudart", "static", f"-I{INCLUDE}", "-o", LIB, *srcs]
+    obj_dir = os.path.join(ROOT, "build", "obj")
+    os.makedirs(obj_dir, exist_ok=True)
+    objs = [os.path.join(obj_dir, os.path.basename(s)[:-3] + ".o") for s in srcs]
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{INCLUDE}"]
     if verbose_ptxas:
-        cmd.insert(1, "-Xptxas=-v")
-    _run(cmd)
+        flags.insert(0, "-Xptxas=-v")
+    todo = [(s, o) for s, o in zip(srcs, objs) if force or _stale(o, [s] + common)]
+
+    def compile_one(so):
+        s, o = so
+        _run([NVCC, *flags, "-c", s, "-o", o])
+
+    if todo:
+        with ThreadPoolExecutor(max_workers=min(len(todo), os.cpu_count() or 4)) as ex:
+            list(ex.map(compile_one, todo))
+    if not force and not todo and not _stale(LIB, objs):
+        return LIB
+    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs])
     return LIB
 
 

@@ -44,6 +44,7 @@ const char* moe_status_string(int s) {
     case MOE_ERR_UNSUPPORTED: return "unsupported shape";
     case MOE_ERR_OUT_OF_MEMORY: return "out of memory";
     case MOE_ERR_EXPERT_RANGE: return "expert id out of range";
+    case MOE_ERR_PEER_TIMEOUT: return "peer timeout";
     default: return "unknown status";
   }
 }

@@ -267,3 +267,118 @@ class ExpertParallelMoE:
         out = B.combine(yb, pos, S, k, stream)
         self.last = {"idx": idx, "w": w, "send_counts": sc, "recv_counts": rc, "recv_rows": R}
         return out
+
+
+# ------------------------------------------------------------------ exchange over peer memory
+class PeerExpertParallelMoE:
+    """One rank's share of the expert-parallel layer with the exchange done by
+    the layer's own kernels through NVLink peer memory (C ABI ``moe_ep_*``,
+    csrc/ep_p2p.cu): the count exchange, the gather fused with the payload
+    all-to-all, and the return all-to-all fused with the combine.  No NCCL and
+    no host synchronisation on the data path, so a forward is one stream-ordered
+    call that can be captured in a CUDA graph.
+
+    Same placement and routing as ``ExpertParallelMoE`` (keys = (device, local
+    expert), exchange.cpp:95-120 as slot counts); the receive layout is grouped
+    by local expert, then source rank, then slot -- the single-GPU order, so
+    each row's FFN is the same computation as in ``MoeLayer``.
+
+    ``torch.distributed`` is used only at construction to exchange the
+    64-byte CUDA IPC handles of the ranks' windows (any backend).
+    """
+
+    def __init__(self, ctx, placement: Placement, shape, Wg, W1_local, W2_local, max_tokens: int,
+                 rank: int, group=None, max_recv_rows: int = 0):
+        placement.validate()
+        self.ctx, self.lib = ctx, ctx.lib
+        self.placement, self.shape, self.rank = placement, shape, rank
+        self.D = placement.num_devices
+        self.max_tokens = max_tokens
+        d = _capi.EpDesc(rank, self.D, max_tokens, shape.token_dim, shape.hidden_dim,
+                         shape.num_experts, shape.top_k, max_recv_rows)
+        dev_of = np.ascontiguousarray(placement.device_of, dtype=np.int32)
+        h = C.c_void_p()
+        check(self.lib.moe_ep_create(ctx.h, C.byref(d), _p(Wg), _p(W1_local), _p(W2_local),
+                                     dev_of.ctypes.data_as(C.c_void_p), C.byref(h)))
+        self.h = h
+        self.Wg = Wg  # the gate's TMA descriptor holds Wg's raw pointer
+        buf = C.create_string_buffer(_capi.MOE_EP_HANDLE_BYTES)
+        check(self.lib.moe_ep_get_handle(self.h, buf))
+        mine = bytes(buf.raw)
+        if self.D > 1:
+            handles = [None] * self.D
+            dist.all_gather_object(handles, mine, group=group)
+        else:
+            handles = [mine]
+        check(self.lib.moe_ep_connect(self.h, b"".join(handles)))
+        if self.D > 1:
+            dist.barrier(group=group)
+        self.group = group
+
+    def forward(self, x: torch.Tensor, stream=None, out: torch.Tensor | None = None,
+                graph: bool = False) -> torch.Tensor:
+        """Collective: every rank calls forward the same number of times."""
+        S = x.shape[0]
+        if out is None:
+            out = torch.empty_like(x)
+        fn = self.lib.moe_ep_forward_graph if graph else self.lib.moe_ep_forward
+        check(fn(self.h, _p(x), S, _p(out), _s(stream)))
+        return out
+
+    def check_errors(self, stream=None):
+        check(self.lib.moe_ep_check_errors(self.h, _s(stream)))
+
+    def view(self, S: int) -> dict:
+        """Device buffers of the last forward (copies), for parity tests."""
+        from .layer import _from_ptr
+
+        v = _capi.EpView()
+        check(self.lib.moe_ep_get_view(self.h, C.byref(v)))
+        E, k, TD = self.shape.num_experts, self.shape.top_k, self.shape.token_dim
+        dev = torch.device("cuda", self.ctx.device)
+        ca = _from_ptr(v.counts_all, self.D * E, torch.int32, dev).view(self.D, E)
+        El = E // self.D
+        R = int(ca[:, self.rank * El:(self.rank + 1) * El].sum())
+        out = {
+            "idx": _from_ptr(v.idx, S * k, torch.int32, dev).view(S, k),
+            "w": _from_ptr(v.w, S * k, torch.float32, dev).view(S, k),
+            "counts": _from_ptr(v.counts, E, torch.int32, dev),
+            "counts_all": ca,
+            "dest": _from_ptr(v.dest, S * k, torch.int32, dev),
+            "order": _from_ptr(v.order, S * k, torch.int32, dev),
+            "n_items": int(_from_ptr(v.n_items, 1, torch.int32, dev)[0]),
+            "recv_rows": R,
+        }
+        if R:
+            out["recv_x"] = _from_ptr(v.recv_x, R * TD, torch.bfloat16, dev).view(R, TD)
+            out["recv_y"] = _from_ptr(v.recv_y, R * TD, torch.bfloat16, dev).view(R, TD)
+            out["recv_w"] = _from_ptr(v.recv_w, R, torch.float32, dev)
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            if self.D > 1 and dist.is_initialized():
+                dist.barrier(group=self.group)  # no peer still maps our window
+            self.lib.moe_ep_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.lib.moe_ep_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def recv_layout(counts_all: np.ndarray, rank: int, El: int):
+    """Receive-side row layout of device ``rank`` (host restatement of
+    ep_dispatch_kernel's destination rows, for tests): returns
+    start[src, local_expert] -- rows are grouped by local expert, then by
+    source rank, then in the source's slot order."""
+    D = counts_all.shape[0]
+    c = counts_all[:, rank * El:(rank + 1) * El].astype(np.int64)  # [src, e]
+    col = c.sum(0)
+    base = np.concatenate([[0], np.cumsum(col)[:-1]])
+    below = np.cumsum(c, axis=0) - c
+    return base[None, :] + below

@@ -184,3 +184,29 @@ def test_placement_key_map_groups_devices():
     assert km.tolist() == [3, 0, 4, 1, 2, 5]
     with pytest.raises(ValueError):
         Placement(np.array([0, 0, 0, 1], np.int32), 2).validate()
+
+
+def test_peer_recv_layout_partitions_rows():
+    """ep.recv_layout (the host restatement of ep_dispatch_kernel's destination
+    rows): at every device the (source, local expert) segments tile [0, R)
+    without gaps, ordered by local expert, then source rank -- the order the
+    single-GPU layer gives the same rows (stable sort by expert of slots, and
+    global slot order interleaves sources only within an expert)."""
+    from paper_2303_06182_b200.ep import recv_layout
+
+    rng = np.random.default_rng(3)
+    for D, El in [(1, 4), (2, 8), (4, 16), (8, 64)]:
+        ca = rng.integers(0, 50, size=(D, D * El))
+        ca[:, rng.integers(0, D * El, 3)] = 0  # empty segments
+        for p in range(D):
+            st = recv_layout(ca, p, El)
+            c = ca[:, p * El:(p + 1) * El]
+            seg = sorted((int(st[s, e]), int(c[s, e]), e, s) for s in range(D) for e in range(El))
+            pos = 0
+            for start, n, e, s in seg:
+                assert start == pos
+                pos += n
+            assert pos == c.sum()
+            order = [(e, s) for _, n, e, s in sorted((int(st[s, e]), int(c[s, e]), e, s)
+                                                      for s in range(D) for e in range(El)) if n]
+            assert order == sorted(order)
