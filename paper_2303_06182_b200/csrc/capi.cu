@@ -481,7 +481,7 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
       (st = L->n_items.reserve(1)) || (st = L->err.reserve(1)) ||
       (st = L->item_off.reserve((size_t)E + 1)) ||
       (st = L->comb_cnt.reserve((size_t)S * (d.token_dim / 128))) ||
-      (st = L->done.reserve(2 * (size_t)L->items_max)) ||
+      (st = L->done.reserve(2 * (size_t)L->items_max + 1)) ||
       (st = L->xp.reserve(Rp * TD)) || (st = L->h.reserve(Rp * HD)) ||
       (st = L->yw.reserve(R * TD))) {
     moe_layer_destroy(L);
@@ -692,7 +692,7 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
                           L->tile_n == 128;
   if (one_launch) {
     // one persistent launch for both GEMMs, H kept in L2 (ffn_fused.cu)
-    MOE_CUDA(cudaMemsetAsync(L->done.p, 0, sizeof(int32_t) * 2 * (size_t)L->items_max, s));
+    MOE_CUDA(cudaMemsetAsync(L->done.p, 0, sizeof(int32_t) * (2 * (size_t)L->items_max + 1), s));
     FusedFfnArgs fa{};
     fa.items = L->items.p;
     fa.n_items = L->n_items.p;
@@ -707,6 +707,7 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
     fa.wpos = L->wpos.p;
     fa.done1 = L->done.p;
     fa.done2 = L->done.p + L->items_max;
+    fa.tile_ctr = L->done.p + 2 * L->items_max;
     // an item's GEMM2 tiles trail its GEMM1 tiles by ~8 waves of CTAs
     // (measured on the LM shape: 4 waves 1.49 ms, 8 waves 1.375 ms, 16 waves
     // 1.43 ms FFN; profiles/r01_fused_ffn.md); MOE_FFN_LAG overrides (items)
@@ -979,7 +980,7 @@ int moe_ffn_create(moe_ctx* ctx, const moe_ffn_desc* desc, const void* W1, const
       (st = F->order.reserve(R)) || (st = F->pos.reserve(R)) || (st = F->n_items.reserve(1)) ||
       (st = F->wpos.reserve(R)) || (st = F->ones.reserve(R)) ||
       (st = F->items.reserve(items_max)) || (st = F->xp.reserve(Rp * TD)) ||
-      (st = F->done.reserve(2 * items_max)) ||
+      (st = F->done.reserve(2 * items_max + 1)) ||
       (st = F->h.reserve(Rp * HD)) || (st = ctx->prepare_route(d.num_experts))) {
     moe_ffn_destroy(F);
     return st;
@@ -1061,7 +1062,7 @@ int moe_ffn_forward(moe_ffn* F, const void* X_rows, const int32_t* keys, const f
   if (F->tile_n == 128) {
     // weight-streaming regime: one persistent launch, H kept in L2, the
     // output rows written straight back to the received order
-    MOE_CUDA(cudaMemsetAsync(F->done.p, 0, sizeof(int32_t) * 2 * (size_t)F->items_max, s));
+    MOE_CUDA(cudaMemsetAsync(F->done.p, 0, sizeof(int32_t) * (2 * (size_t)F->items_max + 1), s));
     FusedFfnArgs fa{};
     fa.items = F->items.p;
     fa.n_items = F->n_items.p;
@@ -1073,6 +1074,7 @@ int moe_ffn_forward(moe_ffn* F, const void* X_rows, const int32_t* keys, const f
     fa.wpos = F->wpos.p;
     fa.done1 = F->done.p;
     fa.done2 = F->done.p + F->items_max;
+    fa.tile_ctr = F->done.p + 2 * F->items_max;
     const int per_item = HD / 128 + TD / 128;
     fa.lag = std::max(2, (8 * F->ctx->sms + per_item - 1) / per_item);
     fa.discard_h = 1;

@@ -474,7 +474,7 @@ int moe_ep_create(moe_ctx* ctx, const moe_ep_desc* desc, const void* Wg, const v
       (st = P->order.reserve(S * k)) || (st = P->pos.reserve(S * k)) ||
       (st = P->wpos.reserve(S * k)) || (st = P->dest.reserve(S * k)) ||
       (st = P->n_items.reserve(1)) || (st = P->err.reserve(2)) ||
-      (st = P->done.reserve(2 * (size_t)P->items_max)) || (st = P->items.reserve(P->items_max)) ||
+      (st = P->done.reserve(2 * (size_t)P->items_max + 1)) || (st = P->items.reserve(P->items_max)) ||
       (st = P->h.reserve((R + 256) * HD)) || (st = P->w1p.reserve(n1)) || (st = P->w2p.reserve(n1)) ||
       (st = ctx->prepare_route(E)))
     return bail(st);
@@ -617,7 +617,7 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   ra.items = P->items.p;
   ra.n_items = P->n_items.p;
   ra.done = P->done.p;
-  ra.done_n = 2 * P->items_max;
+  ra.done_n = 2 * P->items_max + 1;
   ra.err = P->err.p;
   ra.timeout_ns = P->timeout_ns;
   ce = launch_chain(ep_recv_kernel, dim3(1), dim3(512), 0, s, false, ra);
@@ -633,6 +633,7 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   fa.wpos = reinterpret_cast<const float*>(P->window + P->lay.recv_w);
   fa.done1 = P->done.p;
   fa.done2 = P->done.p + P->items_max;
+  fa.tile_ctr = P->done.p + 2 * P->items_max;
   const int per_item = HD / 128 + TD / 128;
   fa.lag = std::max(2, (8 * P->ctx->sms + per_item - 1) / per_item);
   fa.discard_h = 1;

@@ -138,8 +138,13 @@ struct FusedFfnArgs {
   int32_t* done2;           // [items] GEMM2 tiles finished (zeroed before launch)
   int lag;                  // items between an item's GEMM1 and GEMM2 tiles
   int discard_h;            // drop consumed H lines from L2 (no write-back)
-  int dbg;                  // experiments only (MOE_FFN_DBG): 1 = skip B loads, 2 = skip stores
+  int dbg;                  // experiments only (MOE_FFN_DBG): 1 = skip B loads, 2 = skip stores,
+                            // 4 = skip MMAs, 8 = skip the epilogue
   int packed;               // tmW1/tmW2 address prepacked 128 x 64 tiles (launch_pack_tiles)
+  int full_fence;           // A/B: per-thread fence.sc before publishing an H tile
+  int32_t* tile_ctr;        // zeroed tile counter (dynamic scheduling); null = round robin
+  unsigned long long* prof;  // experiments (MOE_FFN_PROF): per-CTA start/end globaltimer
+  int spread;               // tile-order window (items), see ffn_fused.cu TileSeq; <= 1 item-major
 };
 // One activation matrix (Xp or H) seen by TMA at four box heights: a B tile
 // of n rows (n % 8 == 0) is n/64 boxes of 64 rows plus at most one each of 32,
