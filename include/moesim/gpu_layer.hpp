@@ -16,6 +16,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -238,6 +239,72 @@ class ExpertCache {
 
  private:
   moe_cache* h_ = nullptr;
+};
+
+// One rank's share of the expert-parallel layer with the exchange over NVLink
+// peer memory (moe_ep_*, one process per GPU).  The only host-side collective
+// is the exchange of the ranks' window handles at construction, done by the
+// caller's transport (`all_gather`: my MOE_EP_HANDLE_BYTES-byte handle in,
+// every rank's handle in rank order out -- MPI_Allgather, a file rendezvous,
+// torch.distributed, ...).  forward() is then a collective: every rank calls
+// it the same number of times; no host synchronisation inside.
+class ExpertParallelLayer {
+ public:
+  using AllGather = std::function<std::vector<std::string>(const std::string& mine)>;
+
+  ExpertParallelLayer(Context& ctx, const LayerShape& shape, int rank, int world_size,
+                      int max_tokens, const std::vector<std::int32_t>& device_of, const void* Wg,
+                      const void* W1_local, const void* W2_local, const AllGather& all_gather,
+                      int max_recv_rows = 0)
+      : ctx_(&ctx), shape_(shape), world_(world_size) {
+    if (static_cast<int>(device_of.size()) != shape.num_experts)
+      throw std::invalid_argument("device_of must have one entry per expert");
+    moe_ep_desc d{};
+    d.rank = rank;
+    d.world_size = world_size;
+    d.max_tokens = max_tokens;
+    d.token_dim = shape.token_dim;
+    d.hidden_dim = shape.hidden_dim;
+    d.num_experts = shape.num_experts;
+    d.top_k = shape.top_k;
+    d.max_recv_rows = max_recv_rows;
+    check(moe_ep_create(ctx.get(), &d, Wg, W1_local, W2_local, device_of.data(), &h_));
+    std::string mine(MOE_EP_HANDLE_BYTES, '\0');
+    check(moe_ep_get_handle(h_, mine.data()));
+    std::vector<std::string> all = world_size > 1 ? all_gather(mine) : std::vector<std::string>{mine};
+    if (static_cast<int>(all.size()) != world_size)
+      throw std::invalid_argument("all_gather must return one handle per rank");
+    std::string joined;
+    for (const std::string& h : all) {
+      if (h.size() != MOE_EP_HANDLE_BYTES) throw std::invalid_argument("bad handle size");
+      joined += h;
+    }
+    check(moe_ep_connect(h_, joined.data()));
+  }
+  // Callers must make sure no peer still runs a forward (a host barrier)
+  // before destroying: the peers map this rank's window.
+  ~ExpertParallelLayer() { moe_ep_destroy(h_); }
+  ExpertParallelLayer(const ExpertParallelLayer&) = delete;
+  ExpertParallelLayer& operator=(const ExpertParallelLayer&) = delete;
+
+  void forward(const void* X, int S, void* out, void* stream = nullptr) {
+    check(moe_ep_forward(h_, X, S, out, stream));
+  }
+  void forward_graph(const void* X, int S, void* out, void* stream) {
+    check(moe_ep_forward_graph(h_, X, S, out, stream));
+  }
+  void check_errors(void* stream = nullptr) { check(moe_ep_check_errors(h_, stream)); }
+  moe_ep_view view() {
+    moe_ep_view v{};
+    check(moe_ep_get_view(h_, &v));
+    return v;
+  }
+
+ private:
+  Context* ctx_;
+  LayerShape shape_;
+  int world_;
+  moe_ep* h_ = nullptr;
 };
 
 }  // namespace gpu

@@ -98,7 +98,7 @@ BIN = os.path.join(ROOT, "build", "bin")
 def build_tools(force: bool = False) -> None:
     """C++ host programs on the C++ API (no CUDA runtime linked directly)."""
     os.makedirs(BIN, exist_ok=True)
-    for name in ("moesim_measure",):
+    for name in ("moesim_measure", "ep_p2p_demo"):
         src = os.path.join(TOOLS, name + ".cpp")
         exe = os.path.join(BIN, name)
         deps = [src, LIB, LIBCXX] + glob.glob(os.path.join(INCLUDE, "moesim", "*.hpp")) + [

@@ -182,3 +182,61 @@ def test_peer_ep_two_ranks_bitwise_equals_single_gpu(S, TD, HD, E, k):
             row = starts[p][src, e] + (i - splits[qk])
             assert d == (p << 28) | row
             assert (res[p]["recv_x"][row] == r["x_local"][slot // k]).all()
+
+
+def _timeout_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), MOE_EP_TIMEOUT_MS="1500")
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2303_06182_b200._capi import MOE_ERR_PEER_TIMEOUT, MoeError
+    from paper_2303_06182_b200.ep import Placement
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        S, TD, HD, E, k = 256, 256, 512, 8, 2
+        ep, x, xl, mine = _build(rank, world, S, TD, HD, E, k, Placement.contiguous(E, world))
+        status = 0
+        if rank == 0:  # rank 1 never calls forward: rank 0's waits must time out, not hang
+            ep.forward(xl)
+            try:
+                ep.check_errors()
+            except MoeError as e:
+                status = e.status
+        dist.barrier()
+        q.put((rank, status))
+        ep.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_ep_missing_peer_times_out_instead_of_hanging():
+    from paper_2303_06182_b200._capi import MOE_ERR_PEER_TIMEOUT
+    from test_ep_gpu import collect
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_timeout_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(collect(procs, q, 2, 300))
+    for p in procs:
+        p.join(120)
+    assert res[0] == MOE_ERR_PEER_TIMEOUT
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_cxx_host_expert_parallel_demo(world, tmp_path):
+    """Pure C++ host (include/moesim/gpu_layer.hpp ExpertParallelLayer), ranks
+    forked by tools/ep_p2p_demo.cpp, handles exchanged through files; every
+    rank's rows bitwise equal to the single-GPU layer."""
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "build", "bin",
+                       "ep_p2p_demo")
+    r = subprocess.run([exe, "--world", str(world), "--tokens", "1024", "--experts", "32",
+                        "--dir", str(tmp_path / "ep")], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 rows differ" in r.stdout
