@@ -17,6 +17,7 @@
 
 namespace moe {
 int gate_box_rows(int E);
+int gate_box_cols();  // inner (K) extent of the gate's X / Wg TMA boxes
 
 namespace capi {
 
@@ -52,16 +53,19 @@ inline int get_encoder() {
 
 // Row-major bf16 matrix [rows, cols] viewed by TMA in boxes of 64 x box_rows
 // with the 128-byte swizzle the UMMA descriptors expect.
-inline int encode_bf16(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+inline int encode_bf16(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                       uint32_t box_cols = 64) {
   int st = get_encoder();
   if (st) return st;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
+  // rows of box_cols bf16: 128 B -> 128-byte swizzle, 64 B -> 64-byte swizzle
+  const CUtensorMapSwizzle sw = box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     char buf[160];

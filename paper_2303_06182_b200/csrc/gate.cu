@@ -34,10 +34,14 @@ namespace moe {
 namespace {
 
 constexpr int kBlockM = 128;
-constexpr int kBlockK = 64;
+// 32-deep k-blocks (64-byte rows, 64-byte swizzle): a stage is 8 KB of X +
+// b_rows x 64 B of Wg (40 KB at E = 512), so five stages fit and the loads of
+// four k-blocks are in flight while one is multiplied (at 64-deep stages only
+// two 80 KB stages fit and the MMA waited on every load).
+constexpr int kBlockK = 32;
 constexpr int kABytes = kBlockM * kBlockK * 2;
 constexpr int kMaxK = 8;
-constexpr int kMaxSmem = 200 * 1024;
+constexpr int kMaxSmem = 220 * 1024;
 
 struct GateLayout {
   int e_pad;      // E rounded up to 16
@@ -181,13 +185,13 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
         const uint32_t a0 = ptx::smem_u32(smem + stage * stage_bytes);
         const uint32_t b0 = a0 + kABytes;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
+        for (int kk = 0; kk < kBlockK / 16; ++kk) {
           const uint32_t acc = (kb | kk) != 0 ? 1u : 0u;
-          ptx::mma_bf16(tmem_base, ptx::umma_desc_sw128(a0 + kk * 32),
-                        ptx::umma_desc_sw128(b0 + kk * 32), id0, acc);
+          ptx::mma_bf16(tmem_base, ptx::umma_desc_sw64(a0 + kk * 32),
+                        ptx::umma_desc_sw64(b0 + kk * 32), id0, acc);
           if (n1 > 0)
-            ptx::mma_bf16(tmem_base + 256, ptx::umma_desc_sw128(a0 + kk * 32),
-                          ptx::umma_desc_sw128(b0 + 256 * 128 + kk * 32), id1, acc);
+            ptx::mma_bf16(tmem_base + 256, ptx::umma_desc_sw64(a0 + kk * 32),
+                          ptx::umma_desc_sw64(b0 + 256 * kBlockK * 2 + kk * 32), id1, acc);
         }
         if (C > 1)
           ptx::mma_commit_mc(&empty[stage], static_cast<uint16_t>((1u << C) - 1));
@@ -533,6 +537,7 @@ __global__ void __launch_bounds__(256, 1)
 }  // namespace
 
 int gate_box_rows(int E) { return gate_layout(E).box_rows; }
+int gate_box_cols() { return kBlockK; }
 
 template <int C>
 const void* gate_fn(int k) {

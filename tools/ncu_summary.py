@@ -43,11 +43,12 @@ def launches(path):
             order.append(name)
         v = float(r[iv].replace(",", ""))
         agg[name].append(v / 1000.0 if r[iu] == "ns" else v)
-    tot = sum(sum(v) for n, v in agg.items() if "fill_uniform" not in n)
+    SETUP = ("fill_uniform", "pack_tiles")  # one-time data / weight setup, not part of a step
+    tot = sum(sum(v) for n, v in agg.items() if not any(x in n for x in SETUP))
     out = ["| kernel | launches | mean us | min us | max us | share of step |", "|---|---|---|---|---|---|"]
     for n in order:
         v = agg[n]
-        share = "" if "fill_uniform" in n else f"{100 * sum(v) / tot:.1f}%"
+        share = "" if any(x in n for x in SETUP) else f"{100 * sum(v) / tot:.1f}%"
         out.append(f"| `{n}` | {len(v)} | {sum(v) / len(v):.1f} | {min(v):.1f} | {max(v):.1f} | {share} |")
     return "\n".join(out)
 
