@@ -29,7 +29,7 @@
 //               every peer
 //   dispatch(e) waits sig_counts[s] >= e for all s; stores rows + weights to
 //               peers; fence.sys; red.release.sys sig_data += 1 at every peer
-//   recv(e)     waits sig_data >= e * D * kDispatchCtas; builds the FFN work list
+//   recv(e)     waits sig_data >= e * D * dispatch_ctas; builds the FFN work list
 //   FFN(e)      local
 //   done(e)     st.release.sys sig_ydone[me] = e at every peer
 //   combine(e)  waits sig_ydone[p] >= e for all p; reads recv_y remotely
@@ -46,7 +46,6 @@ namespace moe {
 namespace {
 
 constexpr int kMaxRanks = MOE_EP_MAX_RANKS;
-constexpr int kDispatchCtas = 592;  // 4 x 148 (one wave of 512-thread CTAs); fixed: receivers count D * kDispatchCtas arrivals per step
 constexpr int kRowBits = 28;
 
 struct EpHdr {
@@ -80,6 +79,12 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
 __device__ __forceinline__ void red_add_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// Publish the CTA's prior global writes at system scope: the CTA barrier
+// orders every thread's stores before thread `t`'s fence + release, which is
+// cumulative, so the peers' acquire sees all of them (one fence per CTA
+// instead of one per thread; MOE_EP_FENCE=1 adds the per-thread fences back).
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -128,9 +133,11 @@ __global__ void __launch_bounds__(512)
     int32_t* dst = reinterpret_cast<int32_t*>(peers.base[p] + lay.counts_all) + rank * E;
     for (int i = threadIdx.x; i < E; i += blockDim.x) dst[i] = counts[i];
   }
-  __threadfence_system();
   __syncthreads();
-  if (threadIdx.x < D) st_release_sys(&hdr(peers.base[threadIdx.x])->sig_counts[rank], e);
+  if (threadIdx.x < D) {
+    fence_acq_rel_sys();
+    st_release_sys(&hdr(peers.base[threadIdx.x])->sig_counts[rank], e);
+  }
   if (threadIdx.x == 0) me->epoch = e;
 }
 
@@ -146,6 +153,7 @@ struct EpDispatchArgs {
   int32_t* dest;           // [rows] -> (device << 28) | row at that device
   int32_t* err;            // [0] timeout, [1] receive capacity exceeded
   unsigned long long timeout_ns;
+  int full_fence;          // A/B: per-thread fence.sc.sys before the arrival
 };
 
 __global__ void __launch_bounds__(512) ep_dispatch_kernel(EpDispatchArgs a) {
@@ -227,17 +235,20 @@ __global__ void __launch_bounds__(512) ep_dispatch_kernel(EpDispatchArgs a) {
       }
     }
   }
-  __threadfence_system();
+  if (a.full_fence) __threadfence_system();
   __syncthreads();
   // every CTA arrives (even on a timeout) so no receiver waits on a dead step
-  if (threadIdx.x < a.D) red_add_release_sys(&hdr(a.peers.base[threadIdx.x])->sig_data, 1ull);
+  if (threadIdx.x < a.D) {
+    fence_acq_rel_sys();
+    red_add_release_sys(&hdr(a.peers.base[threadIdx.x])->sig_data, 1ull);
+  }
 }
 
 // ---------------------------------------------------------------- receive side
 struct EpRecvArgs {
   char* mine;
   EpLayout lay;
-  int rank, D, E, El, tile_n, max_recv;
+  int rank, D, E, El, tile_n, max_recv, dispatch_ctas;
   FfnItem* items;
   int32_t* n_items;
   int32_t* done;  // fused-FFN counters, zeroed here
@@ -255,7 +266,7 @@ __global__ void __launch_bounds__(512) ep_recv_kernel(EpRecvArgs a) {
   EpHdr* h = hdr(a.mine);
   const unsigned long long e = h->epoch;
   if (threadIdx.x == 0)
-    s_ok = wait_geq(&h->sig_data, e * static_cast<unsigned long long>(a.D) * kDispatchCtas, a.err,
+    s_ok = wait_geq(&h->sig_data, e * static_cast<unsigned long long>(a.D) * a.dispatch_ctas, a.err,
                     a.timeout_ns);
   for (int i = threadIdx.x; i < a.done_n; i += blockDim.x) a.done[i] = 0;
   __syncthreads();
@@ -400,6 +411,10 @@ struct moe_ep {
   DevBuf<FfnItem> items;
   DevBuf<__nv_bfloat16> h, w1p, w2p;
   unsigned long long timeout_ns = 20ull * 1000 * 1000 * 1000;
+  // CTAs of the dispatch kernel: every rank must use the same count (the
+  // receivers wait for D * dispatch_ctas arrivals); MOE_EP_DISPATCH_CTAS
+  int dispatch_ctas = 256;
+  int full_fence = 0;
   cudaGraphExec_t graph = nullptr;
   const void* g_x = nullptr;
   void* g_out = nullptr;
@@ -495,6 +510,8 @@ int moe_ep_create(moe_ctx* ctx, const moe_ep_desc* desc, const void* Wg, const v
       (ce = cudaDeviceSynchronize()) != cudaSuccess)
     return bail(cuda_fail(ce, "EP weight prepack"));
   if (const char* v = getenv("MOE_EP_TIMEOUT_MS")) P->timeout_ns = (unsigned long long)atoll(v) * 1000000ull;
+  if (const char* v = getenv("MOE_EP_DISPATCH_CTAS")) P->dispatch_ctas = std::max(1, atoi(v));
+  if (const char* v = getenv("MOE_EP_FENCE")) P->full_fence = atoi(v);
   *out = P;
   return MOE_OK;
 }
@@ -602,7 +619,8 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   da.dest = P->dest.p;
   da.err = P->err.p;
   da.timeout_ns = P->timeout_ns;
-  ce = launch_chain(ep_dispatch_kernel, dim3(kDispatchCtas), dim3(512), 0, s, false, da);
+  da.full_fence = P->full_fence;
+  ce = launch_chain(ep_dispatch_kernel, dim3(P->dispatch_ctas), dim3(512), 0, s, false, da);
   if (ce != cudaSuccess) return cuda_fail(ce, "EP dispatch launch");
   // 4. receive side: work list from the count matrix
   EpRecvArgs ra{};
@@ -614,6 +632,7 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   ra.El = P->El;
   ra.tile_n = 128;
   ra.max_recv = P->max_recv;
+  ra.dispatch_ctas = P->dispatch_ctas;
   ra.items = P->items.p;
   ra.n_items = P->n_items.p;
   ra.done = P->done.p;
