@@ -155,6 +155,9 @@ def load(path: str = LIB_PATH):
     _sig(lib.moe_cache_stats, I, P, P, P)
     _sig(lib.moe_cache_resident, I, P, P, P)
     _sig(lib.moe_layer_forward_routed, I, P, P, P, P, I, P, P)
+    if not hasattr(lib, "moe_ep_create"):  # an older build (A/B runs via MOE_LIB_PATH)
+        _lib = lib
+        return lib
     _sig(lib.moe_ep_create, I, P, C.POINTER(EpDesc), P, P, P, P, C.POINTER(P))
     _sig(lib.moe_ep_destroy, I, P)
     _sig(lib.moe_ep_get_handle, I, P, P)

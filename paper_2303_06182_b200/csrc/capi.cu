@@ -164,7 +164,8 @@ int moe::capi::route_common(moe_ctx* ctx, const int32_t* expert_idx, int S, int 
                         int32_t* counts, int32_t* splits, int32_t* order, int32_t* pos,
                         const float* gate_w, float* wpos, int32_t* dropped, int32_t* n_dropped,
                         FfnItem* items, int32_t* n_items, int tile_n, const int32_t* key_map,
-                        int num_keys_in, cudaStream_t stream, int32_t* item_off) {
+                        int num_keys_in, cudaStream_t stream, int32_t* item_off,
+                        int32_t* zero, int zero_n) {
   int st = ctx->prepare_route(E);
   if (st) return st;
   if (cap > 0) {
@@ -194,6 +195,8 @@ int moe::capi::route_common(moe_ctx* ctx, const int32_t* expert_idx, int S, int 
   a.n_items = n_items;
   a.item_off = item_off;
   a.error_flag = ctx->err_flag.p;
+  a.zero = zero;
+  a.zero_n = zero ? zero_n : 0;
   cudaError_t e = launch_route(a, ctx->route_max_blocks, stream);
   if (e != cudaSuccess) return cuda_fail(e, "route kernel launch");
   return MOE_OK;
@@ -615,6 +618,7 @@ int moe::capi::layer_front(moe_layer* L, const void* X, int S, const int32_t* id
   if (S > d.max_tokens) return fail(MOE_ERR_INVALID_ARGUMENT, "S exceeds max_tokens");
   const int k = d.top_k, E = d.num_experts, TD = d.token_dim;
   int st;
+  L->counters_zeroed = false;
   const int32_t* idx = idx_in ? idx_in : L->idx.p;
   const float* w = idx_in ? w_in : L->w.p;
   // 1. gate
@@ -665,8 +669,9 @@ int moe::capi::layer_front(moe_layer* L, const void* X, int S, const int32_t* id
   mark(1);
   st = route_common(L->ctx, idx, S, k, E, cap, L->counts.p, L->splits.p, L->order.p, L->pos.p, w,
                     L->wpos.p, L->dropped.p, L->n_dropped.p, L->items.p, L->n_items.p, L->tile_n,
-                    nullptr, 0, s, L->item_off.p);
+                    nullptr, 0, s, L->item_off.p, L->done.p, 2 * L->items_max + 1);
   if (st) return st;
+  L->counters_zeroed = true;
   // 3. gather token rows into expert-grouped order
   mark(2);
   cudaError_t e = launch_gather_rows((const __nv_bfloat16*)X, L->order.p, rows, k, TD, L->xp.p, s);
@@ -692,7 +697,11 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
                           L->tile_n == 128;
   if (one_launch) {
     // one persistent launch for both GEMMs, H kept in L2 (ffn_fused.cu)
-    MOE_CUDA(cudaMemsetAsync(L->done.p, 0, sizeof(int32_t) * (2 * (size_t)L->items_max + 1), s));
+    // the route kernel zeroed the counters for a whole-layer FFN; expert-range
+    // waves (expert cache) share the tile counter and need a fresh one each
+    if (!(e_lo < 0 && L->counters_zeroed))
+      MOE_CUDA(cudaMemsetAsync(L->done.p, 0, sizeof(int32_t) * (2 * (size_t)L->items_max + 1), s));
+    L->counters_zeroed = false;
     FusedFfnArgs fa{};
     fa.items = L->items.p;
     fa.n_items = L->n_items.p;

@@ -183,6 +183,7 @@ struct moe_layer {
   DevBuf<__nv_bfloat16> xp, h, yw, xin, yout;
   int last_rows = 0;
   int last_cap = 0;
+  bool counters_zeroed = false;  // the route kernel of this forward zeroed `done`
   // per-stage timing ring (eager path)
   std::vector<cudaEvent_t> tev;
   int t_slots = 0;
@@ -234,7 +235,8 @@ int route_common(moe_ctx* ctx, const int32_t* expert_idx, int S, int k, int E, i
                  int32_t* counts, int32_t* splits, int32_t* order, int32_t* pos,
                  const float* gate_w, float* wpos, int32_t* dropped, int32_t* n_dropped,
                  FfnItem* items, int32_t* n_items, int tile_n, const int32_t* key_map,
-                 int num_keys_in, cudaStream_t stream, int32_t* item_off = nullptr);
+                 int num_keys_in, cudaStream_t stream, int32_t* item_off = nullptr,
+                 int32_t* zero = nullptr, int zero_n = 0);
 int layer_front(moe_layer* L, const void* X, int S, const int32_t* idx_in, const float* w_in,
                 cudaStream_t s, cudaEvent_t* ev);
 int layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaEvent_t* ev);

@@ -51,9 +51,7 @@ struct FusedCfg {
   static constexpr int kBBytes = KCH * kBChunk;
   static constexpr int kSmem = 1024 + STAGES * (kABytes + kBBytes) + kEpiBytes +
                                (2 * STAGES + 4) * 8 + 16;
-  // accumulator column stride (power of two: TMEM allocations are)
-  static constexpr int kAccStride = BN <= 64 ? 64 : (BN <= 128 ? 128 : 256);
-  static constexpr int kTmemCols = 2 * kAccStride;
+  static constexpr int kTmemCols = 2 * BN;
 };
 
 struct TileRef {
@@ -62,68 +60,22 @@ struct TileRef {
   int m;     // 128-row block of the weight matrix
 };
 
-// Sequence position -> tile.  n items, lag L (<= n), MT1/MT2 m-blocks, and
-// a spread window W: inside a window of W consecutive items the tiles run
-// m-block-major (item fastest), so the ~148 tiles in flight touch ~148/W...
-// more distinct items' token rows at once instead of all MT1 m-blocks of one
-// item hammering the same L2 lines (W = 1: item-major).  L % W == 0 unless
-// L == n.
-struct TileSeq {
-  int n, L, MT1, MT2, W;
-  // tile r of a run over items [item0, item0 + cnt) with MT m-blocks each
-  __device__ __forceinline__ void run(int r, int item0, int cnt, int MT, int& item, int& m) const {
-    const int fw = cnt / W;
-    const int full = fw * W * MT;
-    if (r < full) {
-      const int b = r / (W * MT), x = r - b * W * MT;
-      item = item0 + b * W + x % W;
-      m = x / W;
-    } else {
-      const int x = r - full, w = cnt - fw * W;
-      item = item0 + fw * W + x % w;
-      m = x / w;
-    }
+// Sequence position -> tile.  n items, lag L (<= n), MT1/MT2 m-blocks.
+__device__ __forceinline__ TileRef decode_tile(int t, int n, int L, int MT1, int MT2) {
+  const int head = L * MT1;
+  if (t < head) return {t / MT1, 0, t % MT1};
+  const int per = MT1 + MT2;
+  const int body = head + (n - L) * per;
+  if (t < body) {
+    const int u = t - head;
+    const int g = L + u / per;
+    const int r = u % per;
+    if (r < MT1) return {g, 0, r};
+    return {g - L, 1, r - MT1};
   }
-  __device__ __forceinline__ TileRef decode(int t) const {
-    TileRef tr;
-    const int head = L * MT1;
-    if (t < head) {
-      run(t, 0, L, MT1, tr.item, tr.m);
-      tr.gemm = 0;
-      return tr;
-    }
-    const int per = MT1 + MT2, nb = n - L;
-    const int body = head + nb * per;
-    if (t < body) {
-      // window j: GEMM1 tiles of items [L + jW, +w), then GEMM2 tiles of [jW, +w)
-      const int u = t - head, F = nb / W;
-      int j, w, r;
-      if (u < F * W * per) {
-        j = u / (W * per);
-        w = W;
-        r = u - j * W * per;
-      } else {
-        j = F;
-        w = nb - F * W;
-        r = u - F * W * per;
-      }
-      if (r < w * MT1) {
-        tr.item = L + j * W + r % w;
-        tr.m = r / w;
-        tr.gemm = 0;
-      } else {
-        r -= w * MT1;
-        tr.item = j * W + r % w;
-        tr.m = r / w;
-        tr.gemm = 1;
-      }
-      return tr;
-    }
-    run(t - body, n - L, L, MT2, tr.item, tr.m);
-    tr.gemm = 1;
-    return tr;
-  }
-};
+  const int u = t - body;
+  return {n - L + u / MT2, 1, u % MT2};
+}
 
 __device__ __forceinline__ int ld_acquire(const int32_t* p) {
   int v;
@@ -168,10 +120,6 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ int last_consumer;
-  constexpr int kRing = 4;
-  __shared__ int ring_t[kRing];  // tile handed from the producer to MMA + epilogue (-1 = end)
-  __shared__ FfnItem ring_it[kRing];
-  __shared__ __align__(8) uint64_t ring_full[kRing], ring_empty[kRing];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -192,10 +140,6 @@ __global__ void __launch_bounds__(256, 1)
       ptx::mbar_init(&tfull[s], 1);
       ptx::mbar_init(&tempty[s], 4);
     }
-    for (int s = 0; s < kRing; ++s) {
-      ptx::mbar_init(&ring_full[s], 1);
-      ptx::mbar_init(&ring_empty[s], 5);  // MMA thread + 4 epilogue warps
-    }
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
@@ -214,9 +158,7 @@ __global__ void __launch_bounds__(256, 1)
   int32_t* done2 = g.done2 + item0;
   const int MT1 = g.HD / kBlockM, MT2 = g.TD / kBlockM;
   const int KB1 = g.TD / Cfg::kStageK, KB2 = g.HD / Cfg::kStageK;
-  const int W = max(1, g.spread);
-  const int L = min((g.lag + W - 1) / W * W, n);
-  const TileSeq seq{n, L, MT1, MT2, W};
+  const int L = min(g.lag, n);
   const int total = n * (MT1 + MT2);
 
   if (warp == 0 && lane == 0) {
@@ -225,46 +167,9 @@ __global__ void __launch_bounds__(256, 1)
     const uint64_t pol_x = ptx::policy_evict_last();
     int stage = 0;
     uint32_t phase = 0;
-    // Tiles are claimed from a global counter in sequence order (dynamic
-    // persistent scheduling: a CTA that streams faster takes more tiles, so
-    // the CTAs finish together) or, without a counter, round robin.  Claims run
-    // two tiles ahead and the claimed tile's work item one tile ahead, so
-    // neither the atomic nor the item load sits on the TMA issue path.  Each
-    // tile is handed to the MMA and epilogue warps through a small smem ring.
-    int j = 0;
-    auto claim = [&]() -> int {
-      const int c = g.tile_ctr ? atomicAdd(g.tile_ctr, 1) : blockIdx.x + j * gridDim.x;
-      ++j;
-      return c;
-    };
-    int cur = claim();
-    int pend = cur < total ? claim() : total;
-    TileRef ctr = cur < total ? seq.decode(cur) : TileRef{0, 0, 0};
-    FfnItem cit = cur < total ? items[ctr.item] : FfnItem{0, 0, 0, 0};
-    int cready = (cur < total && ctr.gemm) ? ld_acquire(done1 + ctr.item) : 0;
-    int rs = 0;
-    uint32_t rph = 0;
-    while (true) {
-      ptx::mbar_wait(&ring_empty[rs], rph ^ 1);
-      ring_t[rs] = cur < total ? cur : -1;
-      ring_it[rs] = cit;
-      ptx::mbar_arrive(&ring_full[rs]);
-      if (++rs == kRing) {
-        rs = 0;
-        rph ^= 1;
-      }
-      if (cur >= total) break;
-      const TileRef tr = ctr;
-      const FfnItem it = cit;
-      int ready = cready;
-      const int nxt = pend;
-      TileRef nr{0, 0, 0};
-      FfnItem nit{0, 0, 0, 0};
-      if (nxt < total) {
-        nr = seq.decode(nxt);
-        nit = items[nr.item];
-        pend = claim();
-      }
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const TileRef tr = decode_tile(t, n, L, MT1, MT2);
+      const FfnItem it = items[tr.item];
       const int nrows = (it.len + 15) & ~15;
       const int wslot = g.slot_of ? g.slot_of[it.expert] : it.expert;
       const CUtensorMap* tA = tr.gemm ? &tmW2 : &tmW1;
@@ -277,10 +182,9 @@ __global__ void __launch_bounds__(256, 1)
         // H rows of this item: every GEMM1 tile stored (acquire), then make
         // the generic-proxy stores visible to this thread's TMA reads
         uint32_t polls = 0;
-        while (ready < MT1) {
+        while (ld_acquire(done1 + tr.item) < MT1) {
           __nanosleep(64);
           if (++polls == (1u << 28)) __trap();
-          ready = ld_acquire(done1 + tr.item);
         }
         fence_proxy_async_global();
       }
@@ -317,11 +221,6 @@ __global__ void __launch_bounds__(256, 1)
           phase ^= 1;
         }
       }
-      // readiness of the next GEMM2 tile, polled while this tile's loads land
-      cready = (nxt < total && nr.gemm) ? ld_acquire(done1 + nr.item) : 0;
-      cur = nxt;
-      ctr = nr;
-      cit = nit;
     }
   } else if (warp == 1 && lane == 0) {
     // ------------------------------------------------------------ MMA issuer
@@ -329,25 +228,15 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    int rs = 0;
-    uint32_t rph = 0;
-    while (true) {
-      ptx::mbar_wait(&ring_full[rs], rph);
-      const int t = ring_t[rs];
-      const FfnItem it = ring_it[rs];
-      ptx::mbar_arrive(&ring_empty[rs]);
-      if (++rs == kRing) {
-        rs = 0;
-        rph ^= 1;
-      }
-      if (t < 0) break;
-      const TileRef tr = seq.decode(t);
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const TileRef tr = decode_tile(t, n, L, MT1, MT2);
+      const FfnItem it = items[tr.item];
       const int nn = (it.len + 15) & ~15;
       const uint32_t idesc = ptx::idesc_bf16(kBlockM, nn);
       const int KB = tr.gemm ? KB2 : KB1;
       ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
       ptx::tc_fence_after();
-      const uint32_t d = tmem_base + acc * Cfg::kAccStride;
+      const uint32_t d = tmem_base + acc * BN;
       for (int kb = 0; kb < KB; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
@@ -391,20 +280,9 @@ __global__ void __launch_bounds__(256, 1)
     __nv_bfloat16* stg = sEpi + q * 32 * 32;
     int acc = 0;
     uint32_t acc_phase = 0;
-    int rs = 0;
-    uint32_t rph = 0;
-    while (true) {
-      ptx::mbar_wait(&ring_full[rs], rph);
-      const int t = ring_t[rs];
-      const FfnItem it = ring_it[rs];
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&ring_empty[rs]);
-      if (++rs == kRing) {
-        rs = 0;
-        rph ^= 1;
-      }
-      if (t < 0) break;
-      const TileRef tr = seq.decode(t);
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const TileRef tr = decode_tile(t, n, L, MT1, MT2);
+      const FfnItem it = items[tr.item];
       const int m_total = tr.gemm ? g.TD : g.HD;
       __nv_bfloat16* out = tr.gemm ? g.Yw : g.H;
       ptx::mbar_wait(&tfull[acc], acc_phase);
@@ -412,7 +290,7 @@ __global__ void __launch_bounds__(256, 1)
       const int col0 = tr.m * kBlockM + q * 32;
       for (int c0 = 0; c0 < ((g.dbg & 8) ? 0 : it.len); c0 += 32) {
         uint32_t r[32];
-        ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * Cfg::kAccStride + c0, r);
+        ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c0, r);
         ptx::tmem_ld_wait();
         if (tr.gemm == 0) {
 #pragma unroll
@@ -445,13 +323,18 @@ __global__ void __launch_bounds__(256, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
       if (tr.gemm == 0) {
-        // publish this GEMM1 tile's H rows: the named barrier orders the 128
-        // epilogue threads' stores before thread 0's release (cumulative), so
-        // no per-thread fence.sc is needed (MOE_FFN_FENCE=1 restores it, A/B)
+        // publish this GEMM1 tile's H rows
         fence_proxy_async_global();
-        if (g.full_fence) __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (tid == 0) red_release_add(done1 + tr.item, 1);
+        if (g.full_fence) {
+          __threadfence();
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (tid == 0) atomicAdd(done1 + tr.item, 1);
+        } else {
+          // the named barrier orders the 128 threads' stores before thread 0's
+          // release (cumulative): one release instead of 128 fence.sc
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (tid == 0) red_release_add(done1 + tr.item, 1);
+        }
       } else {
         // this tile's MMAs (hence its H reads) are complete; the last consumer
         // of the item drops the item's H lines from L2 without write-back
@@ -505,9 +388,6 @@ int fused_kch() {
 }
 
 cudaError_t fused_ffn_pair_prepare();
-cudaError_t launch_fused_ffn_impl(const CUtensorMap& tmW1, const RowMaps& xp, const CUtensorMap& tmW2,
-                                  const RowMaps& h, FusedFfnArgs args, int tile_n, int grid,
-                                  cudaStream_t stream);
 bool fused_ffn_pair_enabled();
 cudaError_t launch_fused_ffn_pair(const CUtensorMap& tmW1, const RowMaps& xp,
                                   const CUtensorMap& tmW2, const RowMaps& h,
@@ -519,61 +399,11 @@ cudaError_t fused_ffn_prepare() {
   e = prepare_fused<128, 6, 1>();
   if (e != cudaSuccess) return e;
   if ((e = prepare_fused<128, 3, 2>()) != cudaSuccess) return e;
-
   return prepare_fused<256, 4, 1>();
 }
 
-cudaError_t launch_fused_ffn(const CUtensorMap& tmW1, const RowMaps& xp, const CUtensorMap& tmW2,
-                             const RowMaps& h, const FusedFfnArgs& args_in, int tile_n, int grid,
-                             cudaStream_t stream) {
-  static const int full_fence = [] {
-    const char* v = getenv("MOE_FFN_FENCE");
-    return v ? atoi(v) : 0;
-  }();
-  static const int spread = [] {
-    const char* v = getenv("MOE_FFN_SPREAD");
-    return v ? atoi(v) : 1;
-  }();
-  static const int prof = [] {
-    const char* v = getenv("MOE_FFN_PROF");
-    return v ? atoi(v) : 0;
-  }();
-  FusedFfnArgs args = args_in;
-  args.full_fence = full_fence;
-  if (args.spread == 0) args.spread = spread;
-  static const int dyn = [] {
-    const char* v = getenv("MOE_FFN_DYN");
-    return v ? atoi(v) : 1;
-  }();
-  if (!dyn) args.tile_ctr = nullptr;
-  static unsigned long long* prof_buf = nullptr;
-  if (prof) {
-    if (!prof_buf) cudaMalloc(&prof_buf, 2 * 1024 * sizeof(unsigned long long));
-    args.prof = prof_buf;
-    cudaError_t e = launch_fused_ffn_impl(tmW1, xp, tmW2, h, args, tile_n, grid, stream);
-    if (e != cudaSuccess) return e;
-    // experiments only: per-CTA start/end spread of this launch (eager path)
-    unsigned long long hb[2 * 1024];
-    cudaStreamSynchronize(stream);
-    cudaMemcpy(hb, prof_buf, 2 * grid * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-    unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0;
-    double esum = 0;
-    for (int i = 0; i < grid; ++i) {
-      s0 = std::min(s0, hb[2 * i]);
-      s1 = std::max(s1, hb[2 * i]);
-      e0 = std::min(e0, hb[2 * i + 1]);
-      e1 = std::max(e1, hb[2 * i + 1]);
-    }
-    for (int i = 0; i < grid; ++i) esum += (double)(hb[2 * i + 1] - s0);
-    fprintf(stderr, "[ffn prof] start spread %.1f us, first end %.1f us, mean end %.1f us, last end %.1f us\n",
-            (s1 - s0) * 1e-3, (e0 - s0) * 1e-3, esum / grid * 1e-3, (e1 - s0) * 1e-3);
-    return cudaSuccess;
-  }
-  return launch_fused_ffn_impl(tmW1, xp, tmW2, h, args, tile_n, grid, stream);
-}
-
 cudaError_t launch_fused_ffn_impl(const CUtensorMap& tmW1, const RowMaps& xp, const CUtensorMap& tmW2,
-                                  const RowMaps& h, FusedFfnArgs args, int tile_n, int grid,
+                                  const RowMaps& h, const FusedFfnArgs& args, int tile_n, int grid,
                                   cudaStream_t stream) {
   // CTA pairs (M = 256 UMMA) when both GEMMs have an even number of 128-row
   // weight blocks
@@ -584,9 +414,45 @@ cudaError_t launch_fused_ffn_impl(const CUtensorMap& tmW1, const RowMaps& xp, co
   if (tile_n == 128 && fused_kch() == 2)
     return launch_fused<128, 3, 2>(tmW1, xp, tmW2, h, args, grid, stream);
   if (tile_n == 128) return launch_fused<128, 6, 1>(tmW1, xp, tmW2, h, args, grid, stream);
-
   if (tile_n == 256) return launch_fused<256, 4, 1>(tmW1, xp, tmW2, h, args, grid, stream);
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_fused_ffn(const CUtensorMap& tmW1, const RowMaps& xp, const CUtensorMap& tmW2,
+                             const RowMaps& h, const FusedFfnArgs& args_in, int tile_n, int grid,
+                             cudaStream_t stream) {
+  static const int full_fence = [] {
+    const char* v = getenv("MOE_FFN_FENCE");
+    return v ? atoi(v) : 1;
+  }();
+  static const int prof = [] {
+    const char* v = getenv("MOE_FFN_PROF");
+    return v ? atoi(v) : 0;
+  }();
+  FusedFfnArgs args = args_in;
+  args.full_fence = full_fence;
+  if (!prof) return launch_fused_ffn_impl(tmW1, xp, tmW2, h, args, tile_n, grid, stream);
+  // experiments only: per-CTA start/end spread of this launch (eager path)
+  static unsigned long long* prof_buf = nullptr;
+  if (!prof_buf) cudaMalloc(&prof_buf, 2 * 1024 * sizeof(unsigned long long));
+  args.prof = prof_buf;
+  cudaError_t e = launch_fused_ffn_impl(tmW1, xp, tmW2, h, args, tile_n, grid, stream);
+  if (e != cudaSuccess) return e;
+  unsigned long long hb[2 * 1024];
+  cudaStreamSynchronize(stream);
+  cudaMemcpy(hb, prof_buf, 2 * grid * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0;
+  double esum = 0;
+  for (int i = 0; i < grid; ++i) {
+    s0 = std::min(s0, hb[2 * i]);
+    s1 = std::max(s1, hb[2 * i]);
+    e0 = std::min(e0, hb[2 * i + 1]);
+    e1 = std::max(e1, hb[2 * i + 1]);
+  }
+  for (int i = 0; i < grid; ++i) esum += (double)(hb[2 * i + 1] - s0);
+  fprintf(stderr, "[ffn prof] start spread %.1f us, first end %.1f us, mean end %.1f us, last end %.1f us\n",
+          (s1 - s0) * 1e-3, (e0 - s0) * 1e-3, esum / grid * 1e-3, (e1 - s0) * 1e-3);
+  return cudaSuccess;
 }
 
 }  // namespace moe

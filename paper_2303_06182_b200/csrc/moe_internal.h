@@ -91,6 +91,8 @@ struct RouteArgs {
   int32_t* n_items;           // [1]
   int32_t* item_off;          // optional [E+1]: first item of each expert (expert cache waves)
   int32_t* error_flag;        // [1] set to 1 on an out-of-range expert id
+  int32_t* zero;              // optional [zero_n] buffer zeroed by the kernel (FFN counters)
+  int zero_n;
 };
 
 size_t route_smem_bytes(int E);

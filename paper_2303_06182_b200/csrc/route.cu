@@ -134,6 +134,10 @@ __global__ void __launch_bounds__(kSingle ? kSingleThreads : kMultiThreads)
     route_kernel(RouteArgs a) {
   pdl_trigger();
   pdl_wait();
+  // zero the FFN's per-item / tile counters for this forward (saves a
+  // memset node between the gather and the FFN, which would break the PDL chain)
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.zero_n; i += gridDim.x * blockDim.x)
+    a.zero[i] = 0;
   constexpr int kWarps = (kSingle ? kSingleThreads : kMultiThreads) / 32;
   extern __shared__ int smem[];
   __shared__ int warp_off[kWarps];
