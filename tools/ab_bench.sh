@@ -2,12 +2,12 @@
 # Same-box A/B of several builds of libmoe_b200.so: alternates bench.py runs
 # with MOE_LIB_PATH=<lib>, prints ms/step and per-stage times.
 #   tools/ab_bench.sh "libA.so libB.so [...]" [rounds] [bench args]
-# Env knobs for a variant: "libB.so@MOE_FFN_DYN=0" runs libB with that env.
+# Env knobs for a variant: "libB.so@A=1,B=2" runs libB with those env vars.
 LIBS=$1; R=${2:-3}; shift 2
 for i in $(seq 1 $R); do
   for spec in $LIBS; do
     lib=${spec%%@*}; envs=""
-    [ "$spec" != "$lib" ] && envs=${spec#*@}
+    [ "$spec" != "$lib" ] && envs=${spec#*@} && envs=${envs//,/ }
     env $envs MOE_LIB_PATH=$lib timeout 300 python bench.py --no-cpu-baseline --no-clocks "$@" > gpurun_out/ab.json 2>gpurun_out/ab.err
     python - "$spec" <<'PY'
 import json, os, sys
