@@ -282,10 +282,16 @@ def run_ep(args, world, rank, local):
     del W1, W2
     torch.cuda.empty_cache()
     p2p = args.ep_transport == "p2p"
+    transport_note = ""
     if p2p:
-        layer = PeerExpertParallelMoE(ctx, pl, shape, Wg, W1l, W2l, S, rank)
-        del W1l, W2l  # the layer keeps its own tile-packed copy
-        torch.cuda.empty_cache()
+        from paper_2303_06182_b200.ep import PeerMemoryUnavailable
+
+        try:
+            layer = PeerExpertParallelMoE(ctx, pl, shape, Wg, W1l, W2l, S, rank)
+        except PeerMemoryUnavailable as e:  # raised on every rank: fall back together
+            p2p = False
+            transport_note = f"p2p unavailable ({e}); NCCL fallback"
+    if p2p:
         be = None
         fwd = lambda xx, st, out=None: layer.forward(xx, st, out=out, graph=not args.no_graph)  # noqa: E731
         check = layer.check_errors
@@ -296,6 +302,8 @@ def run_ep(args, world, rank, local):
         fwd = lambda xx, st, out=None: layer.forward(xx, st)  # noqa: E731
         check = be.check_errors
         n_launch = 9
+    del W1l, W2l  # each EP form keeps what it needs (packed copy / tensor references)
+    torch.cuda.empty_cache()
     stream = torch.cuda.Stream()
     stream.wait_stream(torch.cuda.current_stream())  # inputs were written on the current stream
     out_buf = torch.empty_like(x)
@@ -378,7 +386,8 @@ def run_ep(args, world, rank, local):
         "data": "synthetic (counter-hash uniform tokens; random-init experts, std 1/sqrt(fan-in))",
         "config": {"workload": desc + " -- expert parallel", "S_per_gpu": S, "TD": TD, "HD": HD, "E": E,
                    "top_k": k, "gating": mode, "experts_per_gpu": El, "placement": args.placement,
-                   "parallelism": f"ep{world} ({transport})", "ep_transport": args.ep_transport,
+                   "parallelism": f"ep{world} ({transport})",
+                   "ep_transport": ("p2p" if p2p else "nccl") + (f" -- {transport_note}" if transport_note else ""),
                    "l2": "no flush: per-step local expert weights %.2f GB >> 126 MB L2" % (wbytes / 1e9)},
         "roofline": {"kernel": "whole EP step: local expert weights streamed once per step", "bound": "hbm",
                      "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s", "frac": achieved / hbm_gbs,

@@ -270,6 +270,11 @@ class ExpertParallelMoE:
 
 
 # ------------------------------------------------------------------ exchange over peer memory
+class PeerMemoryUnavailable(RuntimeError):
+    """Raised on EVERY rank when any rank cannot map its peers' windows (CUDA
+    IPC / peer access unavailable), so callers can fall back collectively."""
+
+
 class PeerExpertParallelMoE:
     """One rank's share of the expert-parallel layer with the exchange done by
     the layer's own kernels through NVLink peer memory (C ABI ``moe_ep_*``,
@@ -305,15 +310,26 @@ class PeerExpertParallelMoE:
         buf = C.create_string_buffer(_capi.MOE_EP_HANDLE_BYTES)
         check(self.lib.moe_ep_get_handle(self.h, buf))
         mine = bytes(buf.raw)
+        self.group = group
         if self.D > 1:
             handles = [None] * self.D
             dist.all_gather_object(handles, mine, group=group)
         else:
             handles = [mine]
-        check(self.lib.moe_ep_connect(self.h, b"".join(handles)))
+        st = self.lib.moe_ep_connect(self.h, b"".join(handles))
+        err = self.lib.moe_last_error().decode() if st else ""
         if self.D > 1:
+            # collective verdict: every rank mapped every peer window, or none proceeds
+            ok = torch.tensor([0 if st else 1], dtype=torch.int32,
+                              device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+            if int(ok.item()) == 0:
+                self.lib.moe_ep_destroy(self.h)
+                self.h = None
+                raise PeerMemoryUnavailable(err or "a peer rank could not map the windows")
             dist.barrier(group=group)
-        self.group = group
+        elif st:
+            check(st)
 
     def forward(self, x: torch.Tensor, stream=None, out: torch.Tensor | None = None,
                 graph: bool = False) -> torch.Tensor:
