@@ -340,11 +340,22 @@ def run_ep(args, world, rank, local):
     if sampler:
         sampler.stop()
     check(stream)
+    ep_stage = None
     if p2p:
         v = layer.view(S)
         cnt = v["counts"].cpu().numpy().reshape(world, E // world).sum(1)
         recv_rows = v["recv_rows"]
         sent_off = int(cnt.sum() - cnt[rank])
+        # per-stage events from a separate untimed pass of eager forwards
+        # (collective: every rank runs it); median per stage, max over ranks
+        layer.enable_timing(True)
+        per = []
+        with torch.cuda.stream(stream):
+            for _ in range(5):
+                layer.forward(x, stream, out=out_buf, graph=False)
+                per.append(layer.stage_times())
+        layer.enable_timing(False)
+        ep_stage = {kk: max_over_ranks(float(np.median([p_[kk] for p_ in per])), world) for kk in per[0]}
     else:
         recv_rows = layer.last["recv_rows"]
         sent_off = int(layer.last["send_counts"].sum()) - int(layer.last["send_counts"][rank].sum())
@@ -396,7 +407,14 @@ def run_ep(args, world, rank, local):
                 "payload_bytes_offrank_per_direction": sent_off * TD * 2,
                 "exchange_bytes_offrank_per_step": xbytes,
                 "exchange_gbs_over_whole_step": xbytes / (ms * 1e-3) / 1e9,
-                "nvlink_peak_gbs_per_direction": 900.0},
+                "nvlink_peak_gbs_per_direction": 900.0,
+                "nvlink_measured_peer_copy_gbs": 770.0,
+                **({"dispatch_ms": ep_stage["dispatch"], "combine_ms": ep_stage["combine"],
+                    "dispatch_gbs_offrank": sent_off * TD * 2 / (ep_stage["dispatch"] * 1e-3) / 1e9,
+                    "combine_gbs_offrank": sent_off * TD * 2 / (ep_stage["combine"] * 1e-3) / 1e9,
+                    "note": "dispatch / combine kernel times include the wait for the slowest peer"}
+                   if ep_stage else {})},
+        "stage_ms": ep_stage,
         "gpu_launches": n_launch * K,
         "e2e": {"value": world * S / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": S * TD * 2, "d2h_bytes_per_step": S * TD * 2,

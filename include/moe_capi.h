@@ -388,6 +388,15 @@ int moe_ep_forward_graph(moe_ep* ep, const void* X, int S, void* out, void* stre
  * MOE_ERR_UNSUPPORTED (receive capacity exceeded) from the device flags. */
 int moe_ep_check_errors(moe_ep* ep, void* stream);
 
+/* Per-stage CUDA-event timing of eager moe_ep_forward calls (not graph
+ * replays).  Stages: 0 gate + keyed route, 1 count publish, 2 dispatch
+ * (includes the wait for every rank's counts), 3 receive / work list,
+ * 4 FFN, 5 done flags, 6 combine (includes the wait for every peer's FFN).
+ * stage_times synchronises on the last forward's final event. */
+#define MOE_EP_NUM_STAGES 7
+int moe_ep_enable_timing(moe_ep* ep, int on);
+int moe_ep_stage_times(moe_ep* ep, float* ms);
+
 typedef struct moe_ep_view {
   int32_t* idx;        /* [S*k] top-k expert ids (global) */
   float* w;            /* [S*k] */

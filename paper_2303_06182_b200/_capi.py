@@ -21,6 +21,8 @@ MOE_ERR_EXPERT_RANGE = 5
 MOE_ERR_PEER_TIMEOUT = 6
 MOE_EP_MAX_RANKS = 8
 MOE_EP_HANDLE_BYTES = 64
+MOE_EP_NUM_STAGES = 7
+EP_STAGES = ["gate_route", "publish", "dispatch", "recv", "ffn", "done", "combine"]
 
 MOE_GATING_STATIC = 0
 MOE_GATING_DYNAMIC = 1
@@ -41,7 +43,8 @@ EXPORTED = [
     "moe_stream_create", "moe_stream_destroy", "moe_stream_synchronize",
     "moe_layer_forward_host_batches", "moe_layer_repack",
     "moe_ep_create", "moe_ep_destroy", "moe_ep_get_handle", "moe_ep_connect", "moe_ep_forward",
-    "moe_ep_forward_graph", "moe_ep_check_errors", "moe_ep_get_view",
+    "moe_ep_forward_graph", "moe_ep_check_errors", "moe_ep_get_view", "moe_ep_enable_timing",
+    "moe_ep_stage_times",
 ]
 
 
@@ -166,6 +169,8 @@ def load(path: str = LIB_PATH):
     _sig(lib.moe_ep_forward_graph, I, P, P, I, P, P)
     _sig(lib.moe_ep_check_errors, I, P, P)
     _sig(lib.moe_ep_get_view, I, P, C.POINTER(EpView))
+    _sig(lib.moe_ep_enable_timing, I, P, I)
+    _sig(lib.moe_ep_stage_times, I, P, P)
     _lib = lib
     return lib
 

@@ -415,6 +415,8 @@ struct moe_ep {
   // receivers wait for D * dispatch_ctas arrivals); MOE_EP_DISPATCH_CTAS
   int dispatch_ctas = 256;
   int full_fence = 0;
+  cudaEvent_t tev[MOE_EP_NUM_STAGES + 1] = {};  // per-stage timing (eager forwards)
+  bool timing = false;
   cudaGraphExec_t graph = nullptr;
   const void* g_x = nullptr;
   void* g_out = nullptr;
@@ -520,6 +522,8 @@ int moe_ep_destroy(moe_ep* P) {
   if (!P) return MOE_OK;
   cudaSetDevice(P->ctx->device);
   if (P->graph) cudaGraphExecDestroy(P->graph);
+  for (cudaEvent_t e : P->tev)
+    if (e) cudaEventDestroy(e);
   for (int r = 0; r < MOE_EP_MAX_RANKS; ++r)
     if (P->opened[r]) cudaIpcCloseMemHandle(P->peers.base[r]);
   if (P->window) cudaFree(P->window);
@@ -577,8 +581,12 @@ int moe_ep_connect(moe_ep* P, const void* handles) {
 }
 
 extern "C++" {
-static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStream_t s) {
+static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStream_t s,
+                           bool timed = false) {
   const moe_ep_desc& d = P->d;
+  auto mark = [&](int i) {
+    if (timed && P->timing) cudaEventRecord(P->tev[i], s);
+  };
   if (!P->connected) return fail(MOE_ERR_INVALID_ARGUMENT, "moe_ep_connect has not been called");
   if (S < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "empty batch");
   if (S > d.max_tokens) return fail(MOE_ERR_INVALID_ARGUMENT, "S exceeds max_tokens");
@@ -591,12 +599,14 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   }
   // 1. gate + keyed route (local)
   GateArgs ga{S, TD, E, k, P->idx.p, P->w.p, nullptr};
+  mark(0);
   cudaError_t ce = launch_gate(P->tmX, P->tmWg, ga, s);
   if (ce != cudaSuccess) return cuda_fail(ce, "gate launch");
   st = route_common(P->ctx, P->idx.p, S, k, E, 0, P->counts.p, P->splits.p, P->order.p, P->pos.p,
                     P->w.p, P->wpos.p, nullptr, nullptr, nullptr, nullptr, 128, P->key_map.p, E, s);
   if (st) return st;
   // 2. size phase
+  mark(1);
   ce = launch_chain(ep_publish_kernel, dim3(1), dim3(512), 0, s, false, P->peers, P->lay, d.rank, D,
                     E, (const int32_t*)P->counts.p);
   if (ce != cudaSuccess) return cuda_fail(ce, "EP publish launch");
@@ -620,6 +630,7 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   da.err = P->err.p;
   da.timeout_ns = P->timeout_ns;
   da.full_fence = P->full_fence;
+  mark(2);
   ce = launch_chain(ep_dispatch_kernel, dim3(P->dispatch_ctas), dim3(512), 0, s, false, da);
   if (ce != cudaSuccess) return cuda_fail(ce, "EP dispatch launch");
   // 4. receive side: work list from the count matrix
@@ -639,6 +650,7 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   ra.done_n = 2 * P->items_max + 1;
   ra.err = P->err.p;
   ra.timeout_ns = P->timeout_ns;
+  mark(3);
   ce = launch_chain(ep_recv_kernel, dim3(1), dim3(512), 0, s, false, ra);
   if (ce != cudaSuccess) return cuda_fail(ce, "EP receive launch");
   // 5. the fused FFN over the received rows (gate weight applied in GEMM2)
@@ -657,9 +669,11 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   fa.lag = std::max(2, (8 * P->ctx->sms + per_item - 1) / per_item);
   fa.discard_h = 1;
   fa.packed = 1;
+  mark(4);
   ce = launch_fused_ffn(P->tmW1p, P->xpm, P->tmW2p, P->hm, fa, 128, P->ctx->sms, s);
   if (ce != cudaSuccess) return cuda_fail(ce, "EP fused ffn launch");
   // 6. outputs ready -> every peer
+  mark(5);
   ce = launch_chain(ep_done_kernel, dim3(1), dim3(32), 0, s, false, P->peers, d.rank, D);
   if (ce != cudaSuccess) return cuda_fail(ce, "EP done launch");
   // 7. return leg fused with the combine
@@ -677,8 +691,10 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   ca.err = P->err.p;
   ca.timeout_ns = P->timeout_ns;
   const int grid = std::min(P->ctx->sms * 8, (S + 7) / 8);
+  mark(6);
   ce = launch_chain(ep_combine_kernel, dim3(std::max(grid, 1)), dim3(256), 0, s, false, ca);
   if (ce != cudaSuccess) return cuda_fail(ce, "EP combine launch");
+  mark(7);
   return MOE_OK;
 }
 }  // extern "C++"
@@ -686,7 +702,26 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
 int moe_ep_forward(moe_ep* P, const void* X, int S, void* out, void* stream) {
   if (!P || !X || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   cudaSetDevice(P->ctx->device);
-  return ep_forward_impl(P, X, S, out, (cudaStream_t)stream);
+  return ep_forward_impl(P, X, S, out, (cudaStream_t)stream, true);
+}
+
+int moe_ep_enable_timing(moe_ep* P, int on) {
+  if (!P) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  cudaSetDevice(P->ctx->device);
+  if (on && !P->tev[0])
+    for (cudaEvent_t& e : P->tev) MOE_CUDA(cudaEventCreate(&e));
+  P->timing = on != 0;
+  return MOE_OK;
+}
+
+int moe_ep_stage_times(moe_ep* P, float* ms) {
+  if (!P || !ms) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (!P->tev[0]) return fail(MOE_ERR_INVALID_ARGUMENT, "timing not enabled");
+  cudaSetDevice(P->ctx->device);
+  MOE_CUDA(cudaEventSynchronize(P->tev[MOE_EP_NUM_STAGES]));
+  for (int i = 0; i < MOE_EP_NUM_STAGES; ++i)
+    MOE_CUDA(cudaEventElapsedTime(&ms[i], P->tev[i], P->tev[i + 1]));
+  return MOE_OK;
 }
 
 int moe_ep_forward_graph(moe_ep* P, const void* X, int S, void* out, void* stream) {

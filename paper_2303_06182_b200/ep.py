@@ -344,6 +344,15 @@ class PeerExpertParallelMoE:
     def check_errors(self, stream=None):
         check(self.lib.moe_ep_check_errors(self.h, _s(stream)))
 
+    def enable_timing(self, on: bool = True):
+        check(self.lib.moe_ep_enable_timing(self.h, 1 if on else 0))
+
+    def stage_times(self) -> dict:
+        """ms per stage of the last eager forward (moe_ep_stage_times)."""
+        ms = (C.c_float * _capi.MOE_EP_NUM_STAGES)()
+        check(self.lib.moe_ep_stage_times(self.h, ms))
+        return dict(zip(_capi.EP_STAGES, [float(v) for v in ms]))
+
     def view(self, S: int) -> dict:
         """Device buffers of the last forward (copies), for parity tests."""
         from .layer import _from_ptr
