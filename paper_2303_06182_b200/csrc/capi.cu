@@ -426,6 +426,18 @@ int moe_fill_uniform_bf16(moe_ctx* ctx, void* dst, int64_t n, uint64_t seed, uin
 
 // ------------------------------------------------------------------ layer
 
+// 256-token work items (many tokens per expert, e.g. cfg1: 8 experts x 256
+// tokens) also go through the one-launch fused FFN: measured 0.0943 vs
+// 0.1167 ms per cfg1 layer against the two-launch form (same box, A/B);
+// MOE_FUSED_256=0 restores the two launches
+static bool fused256_enabled() {
+  static const int v = [] {
+    const char* e = getenv("MOE_FUSED_256");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
 int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, const void* W1,
                      const void* W2, moe_layer** out) {
   if (!ctx || !desc || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
@@ -523,7 +535,7 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
     return v ? atoi(v) : 1;
   }();
   if (!d.keep_layout && pack_env && !d.split_ffn && !d.fuse_combine &&
-      d.mode == MOE_GATING_DYNAMIC && L->tile_n == 128) {
+      d.mode == MOE_GATING_DYNAMIC && (L->tile_n == 128 || fused256_enabled())) {
     const size_t n1 = (size_t)E * HD * TD;
     if (L->w1p.reserve(n1) == MOE_OK && L->w2p.reserve(n1) == MOE_OK &&
         encode_bf16(&L->tmW1p, L->w1p.p, n1 / 64, 64, 128) == MOE_OK &&
@@ -694,7 +706,7 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
   // small items); compute-bound static batches and few-expert layers (cfg1)
   // measured faster as two launches (profiles/r01_fused_ffn.md)
   const bool one_launch = !L->d.split_ffn && !fcomb && L->d.mode == MOE_GATING_DYNAMIC &&
-                          L->tile_n == 128;
+                          (L->tile_n == 128 || fused256_enabled());
   if (one_launch) {
     // one persistent launch for both GEMMs, H kept in L2 (ffn_fused.cu)
     // the route kernel zeroed the counters for a whole-layer FFN; expert-range

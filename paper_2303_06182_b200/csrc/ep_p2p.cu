@@ -394,6 +394,7 @@ struct moe_ep {
   moe_ctx* ctx = nullptr;
   moe_ep_desc d{};
   int El = 0;
+  int tile_n = 128;
   int max_recv = 0;
   int items_max = 0;
   moe::EpLayout lay{};
@@ -463,7 +464,13 @@ int moe_ep_create(moe_ctx* ctx, const moe_ep_desc* desc, const void* Wg, const v
   P->El = El;
   P->max_recv = (int)R;
   P->Wg = Wg;
-  P->items_max = (int)(R / 128 + El + 1);
+  // work-item width: 256-token items (N = 256 MMAs, half the weight re-reads)
+  // once the expected rows per local expert (D * S * k / E) pass ~160, as the
+  // single-GPU layer picks; MOE_EP_TILE_N overrides
+  const double per_expert = (double)D * d.max_tokens * d.top_k / E;
+  P->tile_n = per_expert > 160.0 ? 256 : 128;
+  if (const char* v = getenv("MOE_EP_TILE_N")) P->tile_n = atoi(v) == 256 ? 256 : 128;
+  P->items_max = (int)(R / P->tile_n + El + 1);
   const size_t TD = d.token_dim, HD = d.hidden_dim, S = d.max_tokens, k = d.top_k;
   size_t off = align256(sizeof(EpHdr));
   P->lay.counts_all = off;
@@ -641,7 +648,7 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   ra.D = D;
   ra.E = E;
   ra.El = P->El;
-  ra.tile_n = 128;
+  ra.tile_n = P->tile_n;
   ra.max_recv = P->max_recv;
   ra.dispatch_ctas = P->dispatch_ctas;
   ra.items = P->items.p;
@@ -670,7 +677,7 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   fa.discard_h = 1;
   fa.packed = 1;
   mark(4);
-  ce = launch_fused_ffn(P->tmW1p, P->xpm, P->tmW2p, P->hm, fa, 128, P->ctx->sms, s);
+  ce = launch_fused_ffn(P->tmW1p, P->xpm, P->tmW2p, P->hm, fa, P->tile_n, P->ctx->sms, s);
   if (ce != cudaSuccess) return cuda_fail(ce, "EP fused ffn launch");
   // 6. outputs ready -> every peer
   mark(5);

@@ -62,10 +62,16 @@ def _build(rank, world, S, TD, HD, E, k, placement, max_recv_rows=0):
     return ep, x, xl, mine
 
 
-def test_peer_ep_one_rank_bitwise_equals_layer():
+@pytest.mark.parametrize("S,TD,HD,E,k,tile_n", [(1024, 256, 512, 16, 2, "128"),
+                                                (1024, 256, 512, 16, 2, "256"),
+                                                (4096, 1024, 4096, 8, 2, "")])
+def test_peer_ep_one_rank_bitwise_equals_layer(S, TD, HD, E, k, tile_n, monkeypatch):
+    """World size 1 (the exchange goes through the rank's own window); 128- and
+    256-token work items (the receive FFN's N), auto = 256 at 1024 rows/expert."""
     from paper_2303_06182_b200.ep import Placement
 
-    S, TD, HD, E, k = 1024, 256, 512, 16, 2
+    if tile_n:
+        monkeypatch.setenv("MOE_EP_TILE_N", tile_n)
     ref_bits, ref_idx = _single_gpu_reference(S, TD, HD, E, k)
     ep, x, xl, mine = _build(0, 1, S, TD, HD, E, k, Placement.contiguous(E, 1))
     s = torch.cuda.Stream()
