@@ -705,7 +705,15 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
   // fused single launch in the weight-streaming regime (dynamic gating, many
   // small items); compute-bound static batches and few-expert layers (cfg1)
   // measured faster as two launches (profiles/r01_fused_ffn.md)
-  const bool one_launch = !L->d.split_ffn && !fcomb && L->d.mode == MOE_GATING_DYNAMIC &&
+  // static gating too (capacity-padded items, zero placeholder rows): one
+  // launch measured 7.95 vs 8.65 ms (LM CF=0.05) and 46.8 vs 56.6 ms (MT CF=1)
+  // against two (same box); MOE_FUSED_STATIC=0 restores the two launches
+  static const int fused_static = [] {
+    const char* e = getenv("MOE_FUSED_STATIC");
+    return e ? atoi(e) : 1;
+  }();
+  const bool one_launch = !L->d.split_ffn && !fcomb &&
+                          (L->d.mode == MOE_GATING_DYNAMIC || fused_static) &&
                           (L->tile_n == 128 || fused256_enabled());
   if (one_launch) {
     // one persistent launch for both GEMMs, H kept in L2 (ffn_fused.cu)
