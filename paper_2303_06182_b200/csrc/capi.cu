@@ -1033,7 +1033,7 @@ int moe_ffn_create(moe_ctx* ctx, const moe_ffn_desc* desc, const void* W1, const
     const char* v = getenv("MOE_PACK");
     return v ? atoi(v) : 1;
   }();
-  if (pack_env && F->tile_n == 128) {
+  if (pack_env && (F->tile_n == 128 || fused256_enabled())) {
     const size_t n1 = (size_t)d.num_experts * HD * TD;
     if (F->w1p.reserve(n1) == MOE_OK && F->w2p.reserve(n1) == MOE_OK &&
         encode_bf16(&F->tmW1p, F->w1p.p, n1 / 64, 64, 128) == MOE_OK &&
@@ -1088,7 +1088,7 @@ int moe_ffn_forward(moe_ffn* F, const void* X_rows, const int32_t* keys, const f
   cudaError_t e = launch_gather_rows((const __nv_bfloat16*)X_rows, F->order.p, rows, 1, TD,
                                      F->xp.p, s);
   if (e != cudaSuccess) return cuda_fail(e, "gather launch");
-  if (F->tile_n == 128) {
+  if (F->tile_n == 128 || fused256_enabled()) {
     // weight-streaming regime: one persistent launch, H kept in L2, the
     // output rows written straight back to the received order
     MOE_CUDA(cudaMemsetAsync(F->done.p, 0, sizeof(int32_t) * (2 * (size_t)F->items_max + 1), s));
