@@ -324,3 +324,57 @@ def test_fused_gate_dispatch_matches_three_launches(S, TD, HD, E, k):
     for key in ("idx", "w", "counts", "splits", "order", "pos", "n_items", "xp"):
         assert torch.equal(va[key], vb[key]), key
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("S,TD,HD,E,k,mode,C", [
+    (1, 256, 256, 16, 2, "dynamic", 1.0),      # a single token
+    (127, 128, 256, 8, 8, "dynamic", 1.0),     # k == E: every expert gets every token
+    (129, 256, 512, 5, 1, "dynamic", 1.0),     # E not a power of two, S not a tile multiple
+    (4097, 256, 256, 64, 2, "dynamic", 1.0),   # just past the single-CTA route (multi-block sort)
+    (300, 256, 512, 8, 2, "static", 0.1),      # static with drops, one-launch fused FFN
+])
+def test_layer_edge_shapes_fused_default(S, TD, HD, E, k, mode, C):
+    """The default (fused, packed) path on edge shapes: routing bit-exact,
+    output within TOL_OUT of the fp32 oracle run with the GPU's routing."""
+    shape = LayerShape(TD, HD, E, k)
+    w = make_weights(shape, seed=SEED)
+    layer = MoeLayer(shape, S, mode=mode, capacity_factor=C, weights=w, keep_logits=True)
+    x = make_tokens(S, TD, seed=SEED)
+    out = layer(x)
+    torch.cuda.synchronize()
+    layer.check_errors()
+    v = layer.view()
+    idx, gw = _check_routing(layer, x, w, v, S, E, k)
+    if mode == "dynamic":
+        ref = OL.layer_forward(_f32(x), _f32(w[1]), _f32(w[2]), idx, gw.astype(np.float64), E)
+    else:
+        cap, slots, dropped, pos = N.c_static_dispatch(idx, E, C)
+        assert (v["order"].cpu().numpy()[:E * cap].reshape(E, cap) == slots).all()
+        wz = gw.astype(np.float64).copy()
+        wz.reshape(-1)[pos < 0] = 0.0  # dropped assignments contribute nothing (gating.hpp:177-181)
+        ref = OL.layer_forward(_f32(x), _f32(w[1]), _f32(w[2]), idx, wz, E)
+    err = OL.rel_fro(_f32(out), ref)
+    print(f"{mode} S={S} E={E} k={k}: rel_fro={err:.2e}")
+    assert err < TOL_OUT
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_layer_routed_all_tokens_on_few_experts(k):
+    """Caller routing that puts every token on expert 3 (and 5): S rows on one
+    expert (many work items of one expert), every other expert empty."""
+    S, TD, HD, E = 1000, 256, 512, 16
+    shape = LayerShape(TD, HD, E, k)
+    w = make_weights(shape, seed=SEED)
+    layer = MoeLayer(shape, S, weights=w)
+    x = make_tokens(S, TD, seed=SEED)
+    ex = np.tile(np.array([3, 5][:k], np.int32), (S, 1))
+    gw = np.tile(np.array([0.75, 0.25][:k] if k == 2 else [1.0], np.float32), (S, 1))
+    out = layer.forward_routed(x, torch.from_numpy(ex).cuda(), torch.from_numpy(gw).cuda())
+    torch.cuda.synchronize()
+    layer.check_errors()
+    v = layer.view()
+    counts = v["counts"].cpu().numpy()
+    assert counts[3] == S and counts.sum() == S * k
+    ref = OL.layer_forward(_f32(x), _f32(w[1]), _f32(w[2]), ex, gw.astype(np.float64), E)
+    err = OL.rel_fro(_f32(out), ref)
+    assert err < TOL_OUT
