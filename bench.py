@@ -14,7 +14,7 @@ launching stream, max over ranks.  The per-step working set (8.7 GB of expert
 weights) is ~70x the 126 MB L2, so no L2 flush is needed between steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                  [--workload lm|mt|cfg1|lm-static|mt-static]
+                  [--workload lm|mt|mt-l256|cfg1|lm-static|mt-static|mt-cache]
 
 N > 1 (torchrun): one rank per GPU, expert parallelism -- E/N experts per GPU
 (greedy load-balanced placement), 16384 tokens per GPU (weak scaling), NCCL
@@ -41,6 +41,9 @@ WORKLOADS = {
                   "configs[1] comparison: LM layer, static gating CF=0.05 (cap 820)"),
     "mt": (6144, 2048, 8192, 128, 2, "dynamic", 0.0,
            "configs[2]: MT MoE layer TD=2048 HD=8192 E=128 top-2, batch 48 x seq 128, dynamic gating"),
+    "mt-l256": (12288, 2048, 8192, 128, 2, "dynamic", 0.0,
+                "configs[2], longer sequences: MT MoE layer TD=2048 HD=8192 E=128 top-2, batch 48 x seq 256, "
+                "dynamic gating (SURVEY.md section 8 cfg3 'also report L=256')"),
     "mt-static": (6144, 2048, 8192, 128, 2, "static", 1.0,
                   "configs[2] comparison: MT layer, static gating CF=1 (cap 6144)"),
     "cfg1": (2048, 1024, 4096, 8, 1, "dynamic", 0.0,
