@@ -479,7 +479,7 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
   }
   L->rows_max = (int)rows_l;
   const double avg = (double)L->rows_max / E;
-  L->tile_n = d.tile_n ? d.tile_n : (avg > 160.0 ? 256 : 128);
+  L->tile_n = d.tile_n ? d.tile_n : auto_tile_n(avg, E, d.token_dim, d.hidden_dim, ctx->sms);
   if (L->tile_n != 128 && L->tile_n != 256) {
     delete L;
     return fail(MOE_ERR_INVALID_ARGUMENT, "tile_n must be 0, 128 or 256");
@@ -996,7 +996,7 @@ int moe_ffn_create(moe_ctx* ctx, const moe_ffn_desc* desc, const void* W1, const
   F->ctx = ctx;
   F->d = d;
   const double avg = (double)d.max_rows / d.num_experts;
-  F->tile_n = d.tile_n ? d.tile_n : (avg > 160.0 ? 256 : 128);
+  F->tile_n = d.tile_n ? d.tile_n : auto_tile_n(avg, d.num_experts, d.token_dim, d.hidden_dim, ctx->sms);
   if (F->tile_n != 128 && F->tile_n != 256) {
     delete F;
     return fail(MOE_ERR_INVALID_ARGUMENT, "tile_n must be 0, 128 or 256");

@@ -86,6 +86,18 @@ inline int encode_rows(moe::RowMaps* m, const void* ptr, uint64_t rows, uint64_t
   return MOE_OK;
 }
 
+// Work-item width of the grouped FFN: 256-token items (N = 256 MMAs, each
+// expert's weights streamed once per 256 tokens) once experts average more
+// than ~160 rows, unless that leaves fewer than ~4 waves of tiles for the
+// persistent grid (few experts, e.g. cfg1: 8 experts x 256 tokens ran 5 %
+// faster as 128-token items).  rows_per_expert = expected rows / expert.
+inline int auto_tile_n(double rows_per_expert, int experts, int TD, int HD, int sms) {
+  if (rows_per_expert <= 160.0) return 128;
+  const double items = experts * std::ceil(rows_per_expert / 256.0);
+  const double tiles = items * (HD / 128 + TD / 128);
+  return tiles >= 4.0 * sms ? 256 : 128;
+}
+
 // Reference check_batch (gating.cpp:12-18), verbatim messages.
 inline int check_batch(int S, int k, int E) {
   if (E < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "num_experts must be positive");

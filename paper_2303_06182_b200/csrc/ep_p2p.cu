@@ -468,7 +468,7 @@ int moe_ep_create(moe_ctx* ctx, const moe_ep_desc* desc, const void* Wg, const v
   // once the expected rows per local expert (D * S * k / E) pass ~160, as the
   // single-GPU layer picks; MOE_EP_TILE_N overrides
   const double per_expert = (double)D * d.max_tokens * d.top_k / E;
-  P->tile_n = per_expert > 160.0 ? 256 : 128;
+  P->tile_n = auto_tile_n(per_expert, El, d.token_dim, d.hidden_dim, ctx->sms);
   if (const char* v = getenv("MOE_EP_TILE_N")) P->tile_n = atoi(v) == 256 ? 256 : 128;
   P->items_max = (int)(R / P->tile_n + El + 1);
   const size_t TD = d.token_dim, HD = d.hidden_dim, S = d.max_tokens, k = d.top_k;

@@ -122,10 +122,15 @@ def test_gate_ties_go_to_lower_expert():
 
 
 def test_layer_cfg1_shape():
-    """configs[0] shape: TD=1024 HD=4096 E=8 top-1, 2048 tokens (tile_n auto = 256)."""
+    """configs[0] shape: TD=1024 HD=4096 E=8 top-1, 2048 tokens (tile_n auto =
+    128: 256 rows per expert, but 256-token items would leave only ~2 waves of
+    tiles for 8 experts), and the 256-token items forced."""
     S, TD, HD, E, k = 2048, 1024, 4096, 8, 1
     layer, x, out, w, v = _run(S, TD, HD, E, k)
-    assert v["tile_n"] == 256
+    assert v["tile_n"] == 128
+    layer256, _, out256, _, v256 = _run(S, TD, HD, E, k, tile_n=256, weights=w, x=x)
+    assert v256["tile_n"] == 256
+    assert torch.equal(out, out256)  # a row's FFN does not depend on the item width
     idx, gw = _check_routing(layer, x, w, v, S, E, k)
     order, counts, splits, pos = N.c_dynamic_dispatch(idx, E)
     assert (v["order"].cpu().numpy()[:S * k] == order).all()
