@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_trigger();
+  if (!g.late_trigger) pdl_trigger();
   pdl_wait();  // the work list and activations come from the previous kernel
   if (g.prof && threadIdx.x == 0) g.prof[2 * blockIdx.x] = globaltimer_ns();
 
@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   ptx::tc_fence_after();
   if (warp == 2) ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  if (g.late_trigger) pdl_trigger();
   if (g.prof && threadIdx.x == 0) g.prof[2 * blockIdx.x + 1] = globaltimer_ns();
 }
 
@@ -429,8 +430,16 @@ cudaError_t launch_fused_ffn(const CUtensorMap& tmW1, const RowMaps& xp, const C
     const char* v = getenv("MOE_FFN_PROF");
     return v ? atoi(v) : 0;
   }();
+  // the dependent kernel (combine) is released only as FFN CTAs retire:
+  // launched at the FFN's start, its 2048 waiting CTAs measured 11-16 us per
+  // LM step slower (same-box A/B); MOE_FFN_LATE_TRIGGER=0 restores it
+  static const int late = [] {
+    const char* v = getenv("MOE_FFN_LATE_TRIGGER");
+    return v ? atoi(v) : 1;
+  }();
   FusedFfnArgs args = args_in;
   args.full_fence = full_fence;
+  args.late_trigger = late;
   if (!prof) return launch_fused_ffn_impl(tmW1, xp, tmW2, h, args, tile_n, grid, stream);
   // experiments only: per-CTA start/end spread of this launch (eager path)
   static unsigned long long* prof_buf = nullptr;
