@@ -21,8 +21,8 @@ namespace {
 
 __global__ void __launch_bounds__(256)
     gather_rows_kernel(const uint4* __restrict__ X, const int32_t* __restrict__ order, int rows,
-                       int k, int vec_per_row, uint4* __restrict__ Xp) {
-  pdl_trigger();
+                       int k, int vec_per_row, uint4* __restrict__ Xp, int late) {
+  if (!late) pdl_trigger();
   pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(256)
     }
     for (; v < vec_per_row; v += 32) dst[v] = __ldg(src + v);
   }
+  if (late) pdl_trigger();
 }
 
 // TMA form of the gather: rows move global -> shared -> global as 1-D bulk
@@ -137,8 +138,8 @@ __device__ __forceinline__ void add_bf16x8(float (&acc)[8], const uint4& v) {
 
 __global__ void __launch_bounds__(256)
     combine_kernel(const uint4* __restrict__ Yw, const int32_t* __restrict__ pos, int S, int k,
-                   int vec_per_row, uint4* __restrict__ out) {
-  pdl_trigger();
+                   int vec_per_row, uint4* __restrict__ out, int late) {
+  if (!late) pdl_trigger();
   pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -157,6 +158,7 @@ __global__ void __launch_bounds__(256)
       out[static_cast<size_t>(t) * vec_per_row + v] = o;
     }
   }
+  if (late) pdl_trigger();
 }
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
@@ -201,6 +203,16 @@ __global__ void fill_segments_kernel(const int32_t* __restrict__ counts, int n, 
   }
 }
 
+// Release the next kernel of the chain only when this one's CTAs finish
+// instead of at their start (see ffn_fused.cu).  Default on for the combine
+// (the next step's gate CTAs, 200 KB of smem each, otherwise sit resident
+// while it streams: 8-25 us per LM step, 3 of 3 same-box A/B rounds), off for
+// the gather (no consistent effect).
+int late_trigger(const char* env, int dflt) {
+  const char* v = getenv(env);
+  return v ? atoi(v) : dflt;
+}
+
 int grid_for(int64_t warps_needed, int sms) {
   const int64_t blocks = (warps_needed + 7) / 8;
   const int64_t cap = static_cast<int64_t>(sms) * 16;
@@ -237,7 +249,7 @@ cudaError_t launch_gather_rows(const __nv_bfloat16* X, const int32_t* order, int
   }
   return launch_chain(gather_rows_kernel, dim3(grid_for(rows, sm_count())), dim3(256), 0, stream,
                       false, reinterpret_cast<const uint4*>(X), order, rows, k, TD / 8,
-                      reinterpret_cast<uint4*>(Xp));
+                      reinterpret_cast<uint4*>(Xp), late_trigger("MOE_GATHER_LATE_TRIGGER", 0));
 }
 
 cudaError_t launch_combine(const __nv_bfloat16* Yw, const int32_t* pos, int S, int k, int TD,
@@ -245,7 +257,7 @@ cudaError_t launch_combine(const __nv_bfloat16* Yw, const int32_t* pos, int S, i
   if (S <= 0) return cudaSuccess;
   return launch_chain(combine_kernel, dim3(grid_for(S, sm_count())), dim3(256), 0, stream, false,
                       reinterpret_cast<const uint4*>(Yw), pos, S, k, TD / 8,
-                      reinterpret_cast<uint4*>(out));
+                      reinterpret_cast<uint4*>(out), late_trigger("MOE_COMBINE_LATE_TRIGGER", 1));
 }
 
 cudaError_t launch_fill_segments(const int32_t* counts, int n_segments, int mod, int32_t* out,
