@@ -334,7 +334,8 @@ __device__ __forceinline__ void add8(float (&acc)[8], const uint4& v) {
 
 __global__ void __launch_bounds__(256) ep_combine_kernel(EpCombineArgs a) {
   __shared__ int s_ok;
-  pdl_trigger();
+  // the next step's gate is released only as these CTAs finish (as the
+  // single-GPU combine, rowops.cu)
   pdl_wait();
   EpHdr* h = hdr(a.peers.base[a.rank]);
   const unsigned long long e = h->epoch;
@@ -344,7 +345,10 @@ __global__ void __launch_bounds__(256) ep_combine_kernel(EpCombineArgs a) {
     s_ok = ok;
   }
   __syncthreads();
-  if (!s_ok) return;
+  if (!s_ok) {
+    pdl_trigger();
+    return;
+  }
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   const int nwarps = gridDim.x * wpb;
@@ -383,6 +387,7 @@ __global__ void __launch_bounds__(256) ep_combine_kernel(EpCombineArgs a) {
       }
     }
   }
+  pdl_trigger();
 }
 
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
