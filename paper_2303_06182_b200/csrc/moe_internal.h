@@ -93,6 +93,7 @@ struct RouteArgs {
   int32_t* error_flag;        // [1] set to 1 on an out-of-range expert id
   int32_t* zero;              // optional [zero_n] buffer zeroed by the kernel (FFN counters)
   int zero_n;
+  int late_trigger;           // release the next kernel (gather) only at completion
 };
 
 size_t route_smem_bytes(int E);

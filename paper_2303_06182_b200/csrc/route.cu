@@ -132,7 +132,7 @@ __device__ __forceinline__ void load_keys(const RouteArgs& a, int base0, int hi,
 template <bool kSingle>
 __global__ void __launch_bounds__(kSingle ? kSingleThreads : kMultiThreads)
     route_kernel(RouteArgs a) {
-  pdl_trigger();
+  if (!a.late_trigger) pdl_trigger();
   pdl_wait();
   // zero the FFN's per-item / tile counters for this forward (saves a
   // memset node between the gather and the FFN, which would break the PDL chain)
@@ -371,6 +371,11 @@ size_t route_smem_bytes(int E) { return smem_bytes(E, kMultiThreads / 32); }
 
 cudaError_t launch_route(RouteArgs a, int max_blocks, cudaStream_t stream) {
   const int total = a.total_slots;
+  static const int late = [] {
+    const char* v = getenv("MOE_ROUTE_LATE_TRIGGER");
+    return v ? atoi(v) : 0;
+  }();
+  a.late_trigger = late;
   const size_t single_smem = smem_bytes(a.num_experts, kSingleThreads / 32);
   if (total <= kSingleMaxSlots && single_smem <= 200 * 1024) {
     a.chunk = (total + kSingleThreads - 1) / kSingleThreads * kSingleThreads;
