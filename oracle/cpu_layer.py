@@ -86,8 +86,32 @@ class CpuLayer:
         return "reference gating.cpp (verbatim build)" if self.use_ref else "C restatement"
 
 
+def blas_threads() -> int:
+    """Threads the BLAS backing numpy will use (threadpoolctl)."""
+    try:
+        from threadpoolctl import threadpool_info
+
+        n = [p.get("num_threads", 1) for p in threadpool_info() if p.get("user_api") == "blas"]
+        return max(n) if n else 1
+    except Exception:
+        return 1
+
+
 def cpu_layer_bench(S, TD, HD, E, k, min_seconds=10.0, max_passes=200, weight_pool=8, layer=None):
-    """Full layer passes until >= min_seconds of timed CPU work; median pass."""
+    """Full layer passes until >= min_seconds of timed CPU work; median pass.
+    BLAS runs on every host core whatever OMP_NUM_THREADS says (torchrun sets
+    it to 1), so the baseline is the CPU path at full width."""
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:  # pragma: no cover
+        threadpool_limits = None
+    if threadpool_limits is not None:
+        with threadpool_limits(limits=os.cpu_count(), user_api="blas"):
+            return _cpu_layer_bench(S, TD, HD, E, k, min_seconds, max_passes, weight_pool, layer)
+    return _cpu_layer_bench(S, TD, HD, E, k, min_seconds, max_passes, weight_pool, layer)
+
+
+def _cpu_layer_bench(S, TD, HD, E, k, min_seconds, max_passes, weight_pool, layer):
     L = layer or CpuLayer(S, TD, HD, E, k, weight_pool=weight_pool)
     passes = []
     t_all = 0.0
@@ -105,9 +129,10 @@ def cpu_layer_bench(S, TD, HD, E, k, min_seconds=10.0, max_passes=200, weight_po
         "breakdown_s": {kk: v for kk, v in med.items() if kk != "total"},
         "dispatch_impl": L.dispatch_impl,
         "weight_pool": L.n_pool,
-        "cores": os.cpu_count(),
+        "cores": blas_threads(),
         "sample": (f"{len(passes)} full layer passes (all {S} tokens, {S * k} slots, {E} experts; "
                    f"expert weights cycled over {L.n_pool} materialised experts), median pass; "
-                   f"dispatch/combine = {L.dispatch_impl}; gate/FFN numpy/OpenBLAS fp32 on "
-                   f"{os.cpu_count()} host cores; {t_all:.1f} s timed"),
+                   f"dispatch/combine = {L.dispatch_impl} (single-threaded, as the reference); "
+                   f"gate/FFN numpy/OpenBLAS fp32 on {blas_threads()} threads ({os.cpu_count()} host "
+                   f"cores); {t_all:.1f} s timed"),
     }
