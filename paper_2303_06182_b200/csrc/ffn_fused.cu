@@ -120,6 +120,11 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ int last_consumer;
+  // dynamic tail: tiles [t_dyn, total) are claimed from a global counter by
+  // the producer and handed to the MMA / epilogue warps through this ring
+  constexpr int kRing = 4;
+  __shared__ int ring_t[kRing];
+  __shared__ __align__(8) uint64_t ring_full[kRing], ring_empty[kRing];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -139,6 +144,10 @@ __global__ void __launch_bounds__(256, 1)
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
       ptx::mbar_init(&tempty[s], 4);
+    }
+    for (int s = 0; s < kRing; ++s) {
+      ptx::mbar_init(&ring_full[s], 1);
+      ptx::mbar_init(&ring_empty[s], 5);  // MMA thread + 4 epilogue warps
     }
     ptx::fence_barrier_init();
   }
@@ -160,6 +169,42 @@ __global__ void __launch_bounds__(256, 1)
   const int KB1 = g.TD / Cfg::kStageK, KB2 = g.HD / Cfg::kStageK;
   const int L = min(g.lag, n);
   const int total = n * (MT1 + MT2);
+  // Tile order per CTA: round robin over [0, t_dyn), then the tail (the
+  // GEMM2-only segment of the last `lag` items: big, equal tiles whose last
+  // partial wave left most SMs idle) claimed dynamically, so the CTAs finish
+  // together.  Claims are in increasing sequence order, so a GEMM2 tile still
+  // only waits for GEMM1 tiles that are claimed and running.
+  const int t_dyn = g.tile_ctr ? max(0, total - (g.dyn_tail > 0 ? g.dyn_tail : L * MT2)) : total;
+  int rs = 0;
+  uint32_t rph = 0;
+  // producer: claim the next tail tile and hand it to the consumers
+  auto claim = [&]() -> int {
+    if (!g.tile_ctr) return -1;  // round robin only: the static sequence is exhausted
+    const int c = t_dyn + atomicAdd(g.tile_ctr, 1);
+    const int t = c < total ? c : -1;
+    ptx::mbar_wait(&ring_empty[rs], rph ^ 1);
+    ring_t[rs] = t;
+    ptx::mbar_arrive(&ring_full[rs]);
+    if (++rs == kRing) {
+      rs = 0;
+      rph ^= 1;
+    }
+    return t;
+  };
+  // MMA thread / epilogue warps: the next tail tile from the ring (a whole
+  // epilogue warp reads it, then its lane 0 arrives for the warp)
+  auto take = [&](bool warp_wide) -> int {
+    if (!g.tile_ctr) return -1;
+    ptx::mbar_wait(&ring_full[rs], rph);
+    const int t = ring_t[rs];
+    if (warp_wide) __syncwarp();
+    if (!warp_wide || lane == 0) ptx::mbar_arrive(&ring_empty[rs]);
+    if (++rs == kRing) {
+      rs = 0;
+      rph ^= 1;
+    }
+    return t;
+  };
 
   if (warp == 0 && lane == 0) {
     // ------------------------------------------------------------ producer
@@ -167,7 +212,8 @@ __global__ void __launch_bounds__(256, 1)
     const uint64_t pol_x = ptx::policy_evict_last();
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int t = blockIdx.x < t_dyn ? blockIdx.x : claim(); t >= 0;
+         t = t + gridDim.x < t_dyn ? t + gridDim.x : claim()) {
       const TileRef tr = decode_tile(t, n, L, MT1, MT2);
       const FfnItem it = items[tr.item];
       const int nrows = (it.len + 15) & ~15;
@@ -228,7 +274,8 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int t = blockIdx.x < t_dyn ? blockIdx.x : take(false); t >= 0;
+         t = t + gridDim.x < t_dyn ? t + gridDim.x : take(false)) {
       const TileRef tr = decode_tile(t, n, L, MT1, MT2);
       const FfnItem it = items[tr.item];
       const int nn = (it.len + 15) & ~15;
@@ -280,7 +327,8 @@ __global__ void __launch_bounds__(256, 1)
     __nv_bfloat16* stg = sEpi + q * 32 * 32;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int t = blockIdx.x < t_dyn ? blockIdx.x : take(true); t >= 0;
+         t = t + gridDim.x < t_dyn ? t + gridDim.x : take(true)) {
       const TileRef tr = decode_tile(t, n, L, MT1, MT2);
       const FfnItem it = items[tr.item];
       const int m_total = tr.gemm ? g.TD : g.HD;
@@ -437,8 +485,14 @@ cudaError_t launch_fused_ffn(const CUtensorMap& tmW1, const RowMaps& xp, const C
     const char* v = getenv("MOE_FFN_LATE_TRIGGER");
     return v ? atoi(v) : 1;
   }();
+  static const int dyn_tail = [] {
+    const char* v = getenv("MOE_FFN_DYN_TAIL");  // tiles claimed dynamically; 0 = lag * MT2, <0 = off
+    return v ? atoi(v) : 0;
+  }();
   FusedFfnArgs args = args_in;
   args.full_fence = full_fence;
+  args.dyn_tail = dyn_tail;
+  if (dyn_tail < 0) args.tile_ctr = nullptr;
   args.late_trigger = late;
   if (!prof) return launch_fused_ffn_impl(tmW1, xp, tmW2, h, args, tile_n, grid, stream);
   // experiments only: per-CTA start/end spread of this launch (eager path)

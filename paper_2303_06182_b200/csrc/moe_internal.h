@@ -147,7 +147,8 @@ struct FusedFfnArgs {
   int full_fence;           // A/B: per-thread fence.sc before publishing an H tile
   int32_t* tile_ctr;        // zeroed tile counter (dynamic scheduling); null = round robin
   unsigned long long* prof;  // experiments (MOE_FFN_PROF): per-CTA start/end globaltimer
-  int late_trigger;         // A/B: let the next kernel launch only as CTAs finish
+  int late_trigger;         // let the next kernel launch only as CTAs finish
+  int dyn_tail;             // tail tiles claimed dynamically (0 = the last lag * MT2)
   int spread;               // tile-order window (items), see ffn_fused.cu TileSeq; <= 1 item-major
 };
 // One activation matrix (Xp or H) seen by TMA at four box heights: a B tile
