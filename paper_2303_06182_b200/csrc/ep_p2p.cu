@@ -59,7 +59,7 @@ struct EpHdr {
 static_assert(sizeof(EpHdr) <= 512, "header");
 
 struct EpLayout {
-  size_t counts_all, recv_w, recv_x, recv_y, total;
+  size_t counts_all, arrived, recv_w, recv_x, recv_y, total;
 };
 
 struct EpPeers {
@@ -154,12 +154,18 @@ struct EpDispatchArgs {
   int32_t* err;            // [0] timeout, [1] receive capacity exceeded
   unsigned long long timeout_ns;
   int full_fence;          // A/B: per-thread fence.sc.sys before the arrival
+  int overlap;             // expert-ordered rows + per-expert arrival counters
 };
+
+__device__ __forceinline__ void red_add_release_sys_u32(unsigned* p, unsigned v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 __global__ void __launch_bounds__(512) ep_dispatch_kernel(EpDispatchArgs a) {
   __shared__ int32_t s_off[512];
   __shared__ int32_t s_split[513];
   __shared__ int32_t s_scan[512];
+  __shared__ int32_t s_vstart[513];  // overlap: segment starts in (local expert, device) order
   __shared__ int s_ok;
   pdl_trigger();
   pdl_wait();
@@ -196,16 +202,45 @@ __global__ void __launch_bounds__(512) ep_dispatch_kernel(EpDispatchArgs a) {
     }
     if (q == 0) s_split[a.E] = a.splits[a.E];
     __syncthreads();
+    if (a.overlap) {
+      // Rows are visited in (local expert, device) order, so every warp sweeps
+      // the local experts upward and a destination's expert e completes early
+      // when e is small: its FFN starts on expert 0 while later rows still fly.
+      // j = e * D + p indexes the segment of key p * El + e.
+      if (q < a.E) {
+        const int e_ = q / a.D, p_ = q % a.D, key = p_ * a.El + e_;
+        s_scan[q] = a.splits[key + 1] - a.splits[key];
+      }
+      __syncthreads();
+      segmented_scan(s_scan, a.E, a.E);
+      if (q < a.E) s_vstart[q + 1] = s_scan[q];
+      if (q == 0) s_vstart[0] = 0;
+      __syncthreads();
+    }
 
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     const int nwarps = gridDim.x * wpb;
-    for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < a.rows; i += nwarps) {
-      int lo = 0, hi = a.E - 1;  // last key whose segment starts at or before i
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_split[mid] <= i) lo = mid;
-        else hi = mid - 1;
+    for (int v_ = blockIdx.x * wpb + (threadIdx.x >> 5); v_ < a.rows; v_ += nwarps) {
+      int lo, i;
+      if (a.overlap) {
+        int jl = 0, jh = a.E - 1;  // last (e, p) segment starting at or before v_
+        while (jl < jh) {
+          const int mid = (jl + jh + 1) >> 1;
+          if (s_vstart[mid] <= v_) jl = mid;
+          else jh = mid - 1;
+        }
+        lo = (jl % a.D) * a.El + jl / a.D;
+        i = s_split[lo] + (v_ - s_vstart[jl]);
+      } else {
+        i = v_;
+        lo = 0;
+        int hi = a.E - 1;  // last key whose segment starts at or before i
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_split[mid] <= i) lo = mid;
+          else hi = mid - 1;
+        }
       }
       const int p = lo / a.El;
       const int row = s_off[lo] + i;
@@ -233,6 +268,14 @@ __global__ void __launch_bounds__(512) ep_dispatch_kernel(EpDispatchArgs a) {
         reinterpret_cast<float*>(peer + a.lay.recv_w)[row] = a.wpos[i];
         a.dest[i] = (p << kRowBits) | row;
       }
+      if (a.overlap) {
+        // this row is visible at its owner before the owner's count moves
+        __syncwarp();
+        if (lane == 0) {
+          fence_acq_rel_sys();
+          red_add_release_sys_u32(reinterpret_cast<unsigned*>(peer + a.lay.arrived) + lo % a.El, 1u);
+        }
+      }
     }
   }
   if (a.full_fence) __threadfence_system();
@@ -249,6 +292,8 @@ struct EpRecvArgs {
   char* mine;
   EpLayout lay;
   int rank, D, E, El, tile_n, max_recv, dispatch_ctas;
+  int overlap;     // per-expert arrival waits in the FFN instead of a global one here
+  int32_t* expect; // [El] rows each local expert receives this step (overlap)
   FfnItem* items;
   int32_t* n_items;
   int32_t* done;  // fused-FFN counters, zeroed here
@@ -266,8 +311,9 @@ __global__ void __launch_bounds__(512) ep_recv_kernel(EpRecvArgs a) {
   EpHdr* h = hdr(a.mine);
   const unsigned long long e = h->epoch;
   if (threadIdx.x == 0)
-    s_ok = wait_geq(&h->sig_data, e * static_cast<unsigned long long>(a.D) * a.dispatch_ctas, a.err,
-                    a.timeout_ns);
+    s_ok = a.overlap ? 1
+                     : wait_geq(&h->sig_data, e * static_cast<unsigned long long>(a.D) * a.dispatch_ctas,
+                                a.err, a.timeout_ns);
   for (int i = threadIdx.x; i < a.done_n; i += blockDim.x) a.done[i] = 0;
   __syncthreads();
   const int q = threadIdx.x;  // local expert
@@ -280,6 +326,7 @@ __global__ void __launch_bounds__(512) ep_recv_kernel(EpRecvArgs a) {
   if (q < a.El) {
     s_rows[q] = n;
     s_items[q] = ni;
+    if (a.expect) a.expect[q] = n;
   }
   __syncthreads();
   segmented_scan(s_rows, a.El, a.El);
@@ -303,9 +350,13 @@ __global__ void __launch_bounds__(512) ep_recv_kernel(EpRecvArgs a) {
   }
 }
 
-__global__ void ep_done_kernel(EpPeers peers, int rank, int D) {
+__global__ void ep_done_kernel(EpPeers peers, EpLayout lay, int rank, int D, int El) {
   pdl_wait();
   const unsigned long long e = hdr(peers.base[rank])->epoch;
+  // the FFN consumed every arrival of this step: restart the per-expert
+  // counts before any sender may start the next step (it waits for this flag)
+  unsigned* arrived = reinterpret_cast<unsigned*>(peers.base[rank] + lay.arrived);
+  for (int i = threadIdx.x; i < El; i += blockDim.x) arrived[i] = 0;
   __threadfence_system();
   if (threadIdx.x < D) st_release_sys(&hdr(peers.base[threadIdx.x])->sig_ydone[rank], e);
 }
@@ -421,6 +472,14 @@ struct moe_ep {
   // receivers wait for D * dispatch_ctas arrivals); MOE_EP_DISPATCH_CTAS
   int dispatch_ctas = 256;
   int full_fence = 0;
+  // MOE_EP_OVERLAP=1: expert-ordered dispatch with per-expert arrival counts,
+  // GEMM1 tiles wait only for their expert's rows (the FFN starts while later
+  // rows are in flight).  Off by default: at world size 1 the per-row
+  // system-scope release costs 41 -> 140 us in the dispatch and the per-tile
+  // readiness check +15-19 us in the FFN, and the gain (hiding the
+  // all-to-all behind the FFN at D > 1) could not be measured on one GPU.
+  int overlap = 0;
+  DevBuf<int32_t> expect;
   cudaEvent_t tev[MOE_EP_NUM_STAGES + 1] = {};  // per-stage timing (eager forwards)
   bool timing = false;
   cudaGraphExec_t graph = nullptr;
@@ -480,6 +539,8 @@ int moe_ep_create(moe_ctx* ctx, const moe_ep_desc* desc, const void* Wg, const v
   size_t off = align256(sizeof(EpHdr));
   P->lay.counts_all = off;
   off = align256(off + sizeof(int32_t) * D * E);
+  P->lay.arrived = off;  // [E/D] rows of each local expert stored so far this step
+  off = align256(off + sizeof(uint32_t) * El);
   P->lay.recv_w = off;
   off = align256(off + sizeof(float) * R);
   P->lay.recv_x = off;
@@ -526,6 +587,8 @@ int moe_ep_create(moe_ctx* ctx, const moe_ep_desc* desc, const void* Wg, const v
   if (const char* v = getenv("MOE_EP_TIMEOUT_MS")) P->timeout_ns = (unsigned long long)atoll(v) * 1000000ull;
   if (const char* v = getenv("MOE_EP_DISPATCH_CTAS")) P->dispatch_ctas = std::max(1, atoi(v));
   if (const char* v = getenv("MOE_EP_FENCE")) P->full_fence = atoi(v);
+  if (const char* v = getenv("MOE_EP_OVERLAP")) P->overlap = atoi(v);
+  if ((st = P->expect.reserve(El))) return bail(st);
   *out = P;
   return MOE_OK;
 }
@@ -555,6 +618,7 @@ int moe_ep_destroy(moe_ep* P) {
   P->h.release();
   P->w1p.release();
   P->w2p.release();
+  P->expect.release();
   delete P;
   return MOE_OK;
 }
@@ -642,6 +706,7 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   da.err = P->err.p;
   da.timeout_ns = P->timeout_ns;
   da.full_fence = P->full_fence;
+  da.overlap = P->overlap;
   mark(2);
   ce = launch_chain(ep_dispatch_kernel, dim3(P->dispatch_ctas), dim3(512), 0, s, false, da);
   if (ce != cudaSuccess) return cuda_fail(ce, "EP dispatch launch");
@@ -656,6 +721,8 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   ra.tile_n = P->tile_n;
   ra.max_recv = P->max_recv;
   ra.dispatch_ctas = P->dispatch_ctas;
+  ra.overlap = P->overlap;
+  ra.expect = P->overlap ? P->expect.p : nullptr;
   ra.items = P->items.p;
   ra.n_items = P->n_items.p;
   ra.done = P->done.p;
@@ -677,6 +744,12 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   fa.done1 = P->done.p;
   fa.done2 = P->done.p + P->items_max;
   fa.tile_ctr = P->done.p + 2 * P->items_max;
+  if (P->overlap) {  // GEMM1 tiles wait for their expert's rows, not for every row
+    fa.arrived = reinterpret_cast<const unsigned*>(P->window + P->lay.arrived);
+    fa.arrived_expect = P->expect.p;
+    fa.arrive_err = P->err.p;
+    fa.arrive_timeout_ns = P->timeout_ns;
+  }
   const int per_item = HD / 128 + TD / 128;
   fa.lag = std::max(2, (8 * P->ctx->sms + per_item - 1) / per_item);
   fa.discard_h = 1;
@@ -686,7 +759,8 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   if (ce != cudaSuccess) return cuda_fail(ce, "EP fused ffn launch");
   // 6. outputs ready -> every peer
   mark(5);
-  ce = launch_chain(ep_done_kernel, dim3(1), dim3(32), 0, s, false, P->peers, d.rank, D);
+  ce = launch_chain(ep_done_kernel, dim3(1), dim3(32), 0, s, false, P->peers, P->lay, d.rank, D,
+                    P->El);
   if (ce != cudaSuccess) return cuda_fail(ce, "EP done launch");
   // 7. return leg fused with the combine
   EpCombineArgs ca{};

@@ -89,6 +89,12 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 
+__device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void red_release_add(int32_t* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -224,6 +230,24 @@ __global__ void __launch_bounds__(256, 1)
       // prepacked: first 128 x 64 tile of this weight block
       const int a_tile = (wslot * (tr.gemm ? MT2 : MT1) + tr.m) * ((tr.gemm ? g.HD : g.TD) / kChunkK);
       const int KB = tr.gemm ? KB2 : KB1;
+      if (!tr.gemm && g.arrived) {
+        // expert parallelism: this expert's token rows are stored by the peer
+        // ranks; wait for all of them (system-scope acquire), then order the
+        // generic-proxy stores before this thread's TMA reads
+        const unsigned need = static_cast<unsigned>(g.arrived_expect[it.expert]);
+        if (ld_acquire_sys_u32(g.arrived + it.expert) < need) {
+          const unsigned long long t0 = globaltimer_ns();
+          while (ld_acquire_sys_u32(g.arrived + it.expert) < need) {
+            if (*reinterpret_cast<volatile int32_t*>(g.arrive_err) != 0) break;
+            if (globaltimer_ns() - t0 > g.arrive_timeout_ns) {
+              atomicExch(g.arrive_err, 1);
+              break;
+            }
+            __nanosleep(128);
+          }
+        }
+        fence_proxy_async_global();
+      }
       if (tr.gemm) {
         // H rows of this item: every GEMM1 tile stored (acquire), then make
         // the generic-proxy stores visible to this thread's TMA reads

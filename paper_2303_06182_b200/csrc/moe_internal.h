@@ -149,6 +149,13 @@ struct FusedFfnArgs {
   unsigned long long* prof;  // experiments (MOE_FFN_PROF): per-CTA start/end globaltimer
   int late_trigger;         // let the next kernel launch only as CTAs finish
   int dyn_tail;             // tail tiles claimed dynamically (0 = the last lag * MT2)
+  // expert parallelism (ep_p2p.cu): a GEMM1 tile's token rows are loaded only
+  // once arrived[expert] >= arrived_expect[expert] (peer stores, acquire.sys);
+  // after arrive_timeout_ns the wait gives up and sets arrive_err[0]
+  const unsigned* arrived;
+  const int32_t* arrived_expect;
+  int32_t* arrive_err;
+  unsigned long long arrive_timeout_ns;
   int spread;               // tile-order window (items), see ffn_fused.cu TileSeq; <= 1 item-major
 };
 // One activation matrix (Xp or H) seen by TMA at four box heights: a B tile

@@ -139,10 +139,15 @@ def _worker(rank, world, port, S, TD, HD, E, k, steps, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("S,TD,HD,E,k", [(512, 256, 512, 16, 2), (4096, 1024, 4096, 64, 2)])
-def test_peer_ep_two_ranks_bitwise_equals_single_gpu(S, TD, HD, E, k):
+@pytest.mark.parametrize("S,TD,HD,E,k,overlap", [(512, 256, 512, 16, 2, "0"), (4096, 1024, 4096, 64, 2, "0"),
+                                                 (4096, 1024, 4096, 64, 2, "1")])
+def test_peer_ep_two_ranks_bitwise_equals_single_gpu(S, TD, HD, E, k, overlap, monkeypatch):
+    """overlap "1": expert-ordered dispatch with per-expert arrival counters
+    and GEMM1 tiles waiting per expert (MOE_EP_OVERLAP)."""
     from paper_2303_06182_b200.ep import recv_layout
     from test_ep_gpu import collect
+
+    monkeypatch.setenv("MOE_EP_OVERLAP", overlap)
 
     world, steps = 2, 4
     ctx = mp.get_context("spawn")
