@@ -732,7 +732,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference", "ours"])
     ap.add_argument("--workload", default="lm", choices=sorted(WORKLOADS))
     ap.add_argument("--tile-n", type=int, default=0)
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=60)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--json-out", default="")
