@@ -64,6 +64,12 @@ def measured_peaks():
         return 6650.0, 1590.0, "fallback"
 
 
+def cpu_seconds() -> float:
+    """Timed CPU work per CPU-baseline measurement (>= 10 s by default;
+    MOE_CPU_BASELINE_SECONDS shortens it for the CPU contract tests)."""
+    return float(os.environ.get("MOE_CPU_BASELINE_SECONDS", "10"))
+
+
 def sustained_tflops(default):
     """bf16 TF/s sustained under the power cap (for a kernel timed inside a
     long step, B200_PROFILING.md); the burst figure if absent."""
@@ -226,7 +232,7 @@ def run_reference(args):
     vals, secs = [], []
     r = None
     for _ in range(max(1, min(args.steps, 3))):
-        r = cpu_layer_bench(S, TD, HD, E, k, min_seconds=10.0, layer=L)
+        r = cpu_layer_bench(S, TD, HD, E, k, min_seconds=cpu_seconds(), layer=L)
         vals.append(r["tokens_per_s"])
         secs.append(r["seconds_per_layer"])
     vals.sort()
@@ -675,7 +681,7 @@ def run_b200(args):
     if world == 1 and not args.no_cpu_baseline:
         from oracle.cpu_layer import cpu_layer_bench
 
-        r = cpu_layer_bench(S, TD, HD, E, k, min_seconds=10.0)
+        r = cpu_layer_bench(S, TD, HD, E, k, min_seconds=cpu_seconds())
         cpu = {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": r["cores"], "kind": "port",
                "sample": r["sample"], "breakdown_s": r["breakdown_s"]}
     line = {
