@@ -588,33 +588,47 @@ def run_b200(args):
         for _ in range(2):
             layer.forward(x, out, graph=use_graph, stream=stream)
     stream.synchronize()
-    sampler = ClockSampler(local) if not args.no_clocks else None
-    if sampler:
-        sampler.start()
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
-    barrier(world)
-    torch.cuda.synchronize()
-    if sampler:
-        sampler.mark_start()
-    with torch.cuda.stream(stream):
-        for i in range(K):
-            evs[i].record(stream)
-            layer.forward(x, out, graph=use_graph, stream=stream)
-        evs[K].record(stream)
-    stream.synchronize()
-    torch.cuda.synchronize()
-    if sampler:
-        sampler.mark_stop()
-    barrier(world)
-    elapsed_ms = evs[0].elapsed_time(evs[K])
-    layer.check_errors(stream)
-    step_ms = np.array([evs[i].elapsed_time(evs[i + 1]) for i in range(K)])
+
+    def timed_region():
+        sampler = ClockSampler(local) if not args.no_clocks else None
+        if sampler:
+            sampler.start()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+        barrier(world)
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.mark_start()
+        with torch.cuda.stream(stream):
+            for i in range(K):
+                evs[i].record(stream)
+                layer.forward(x, out, graph=use_graph, stream=stream)
+            evs[K].record(stream)
+        stream.synchronize()
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.mark_stop()
+        barrier(world)
+        layer.check_errors(stream)
+        if sampler:
+            sampler.stop()
+        return (evs[0].elapsed_time(evs[K]), np.array([evs[i].elapsed_time(evs[i + 1]) for i in range(K)]),
+                sampler.summary() if sampler else None)
+
+    elapsed_ms, step_ms, clocks = timed_region()
+    # a timed region that saw hardware / thermal slowdown is measured again once
+    # (sw_power_cap is normal for a 1 kW part and kept)
+    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    throttled = bool(clocks and bad & set(clocks.get("reasons", [])))
+    remeasured = None
+    if max_over_ranks(1.0 if throttled else 0.0, world) > 0:
+        remeasured = {"first_attempt_reasons": clocks.get("reasons") if clocks else None,
+                      "first_attempt_ms_per_step": elapsed_ms / K}
+        elapsed_ms, step_ms, clocks = timed_region()
     elapsed_max = max_over_ranks(elapsed_ms, world)
     p50 = float(np.median(step_ms))
     p50_max = max_over_ranks(p50, world)
-    if sampler:
-        sampler.stop()
-    clocks = sampler.summary() if sampler else None
+    if remeasured and clocks is not None:
+        clocks = dict(clocks, remeasured=remeasured)
 
     # ---- e2e through the public C-ABI host path (pinned host in/out, copies in the timed region)
     xh = x.cpu().pin_memory()
