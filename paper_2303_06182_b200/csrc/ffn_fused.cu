@@ -51,7 +51,9 @@ struct FusedCfg {
   static constexpr int kBBytes = KCH * kBChunk;
   static constexpr int kSmem = 1024 + STAGES * (kABytes + kBBytes) + kEpiBytes +
                                (2 * STAGES + 4) * 8 + 16;
-  static constexpr int kTmemCols = 2 * BN;
+  // accumulator column stride (a power of two: TMEM allocations are)
+  static constexpr int kAccStride = BN <= 64 ? 64 : (BN <= 128 ? 128 : 256);
+  static constexpr int kTmemCols = 2 * kAccStride;
 };
 
 struct TileRef {
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(256, 1)
       const int KB = tr.gemm ? KB2 : KB1;
       ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
       ptx::tc_fence_after();
-      const uint32_t d = tmem_base + acc * BN;
+      const uint32_t d = tmem_base + acc * Cfg::kAccStride;
       for (int kb = 0; kb < KB; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
@@ -362,7 +364,7 @@ __global__ void __launch_bounds__(256, 1)
       const int col0 = tr.m * kBlockM + q * 32;
       for (int c0 = 0; c0 < ((g.dbg & 8) ? 0 : it.len); c0 += 32) {
         uint32_t r[32];
-        ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c0, r);
+        ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * Cfg::kAccStride + c0, r);
         ptx::tmem_ld_wait();
         if (tr.gemm == 0) {
 #pragma unroll
