@@ -33,13 +33,15 @@ constexpr int kBlockM = 128;  // weight rows per CTA (256 per pair)
 constexpr int kChunkK = 64;
 constexpr int kUmmaK = 16;
 constexpr int kEpiBytes = 4 * 32 * 32 * 2;
-constexpr int kBN = 128;      // max tokens per work item (tile_n)
 constexpr int kAChunk = kBlockM * kChunkK * 2;      // 16 KB
-constexpr int kBChunk = (kBN / 2) * kChunkK * 2;    // 8 KB: half of the token rows
-constexpr int kTmemCols = 2 * kBN;
 
-template <int STAGES, int KCH>
+// BN = max tokens per work item (tile_n, 128 or 256); each CTA of the pair
+// stages half of the item's token rows.
+template <int BN, int STAGES, int KCH>
 struct PairCfg {
+  static constexpr int kBN = BN;
+  static constexpr int kBChunk = (BN / 2) * kChunkK * 2;  // half of the token rows
+  static constexpr int kTmemCols = 2 * BN;
   static constexpr int kStages = STAGES;
   static constexpr int kKch = KCH;  // 64-wide k-chunks per stage
   static constexpr int kStageK = KCH * kChunkK;
@@ -143,15 +145,16 @@ __device__ __forceinline__ void load_rows(uint8_t* dst, const RowMaps* m, uint32
   if (r < h) tma_load_2d_pair(dst + r * 128, &m->m8, bar, k0, r0 + r, pol);
 }
 
-template <int STAGES, int KCH>
+template <int BN, int STAGES, int KCH>
 __global__ void __launch_bounds__(256, 1)
     fused_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmW1,
                           const __grid_constant__ RowMaps xpm,
                           const __grid_constant__ CUtensorMap tmW2,
                           const __grid_constant__ RowMaps hm, FusedFfnArgs g) {
-  using Cfg = PairCfg<STAGES, KCH>;
+  using Cfg = PairCfg<BN, STAGES, KCH>;
   constexpr int kStages = Cfg::kStages, kKch = Cfg::kKch, kStageK = Cfg::kStageK;
   constexpr int kABytes = Cfg::kABytes, kBBytes = Cfg::kBBytes;
+  constexpr int kBN = Cfg::kBN, kBChunk = Cfg::kBChunk, kTmemCols = Cfg::kTmemCols;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(256, 1)
   ptx::cluster_sync();  // barriers and TMEM of both CTAs exist before any remote use
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_trigger();
+  if (!g.late_trigger) pdl_trigger();
   pdl_wait();
 
   const int item0 = g.item_off ? g.item_off[g.e_lo] : 0;
@@ -387,6 +390,7 @@ __global__ void __launch_bounds__(256, 1)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "n"(kTmemCols)
                  : "memory");
+  if (g.late_trigger) pdl_trigger();
 }
 
 // MOE_FFN_PAIR_STAGES=4 selects 4 stages of 128-deep k (default: 8 x 64)
@@ -399,14 +403,14 @@ int pair_cfg() {
   return v;
 }
 
-template <int STAGES, int KCH>
+template <int BN, int STAGES, int KCH>
 int pair_grid(int sms) {
   static int grid = -1;
   if (grid >= 0) return grid;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(sms & ~1);
   cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = PairCfg<STAGES, KCH>::kSmem;
+  cfg.dynamicSmemBytes = PairCfg<BN, STAGES, KCH>::kSmem;
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeClusterDimension;
   attr.val.clusterDim.x = 2;
@@ -415,7 +419,7 @@ int pair_grid(int sms) {
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, fused_ffn_pair_kernel<STAGES, KCH>, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, fused_ffn_pair_kernel<BN, STAGES, KCH>, &cfg) != cudaSuccess) {
     cudaGetLastError();
     n = 0;
   }
@@ -424,15 +428,15 @@ int pair_grid(int sms) {
   return grid;
 }
 
-template <int STAGES, int KCH>
+template <int BN, int STAGES, int KCH>
 cudaError_t launch_pair(const CUtensorMap& tmW1, const RowMaps& xp, const CUtensorMap& tmW2,
                         const RowMaps& h, const FusedFfnArgs& args, int sms, cudaStream_t stream) {
-  const int grid = pair_grid<STAGES, KCH>(sms);
+  const int grid = pair_grid<BN, STAGES, KCH>(sms);
   if (grid < 2) return cudaErrorNotSupported;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = PairCfg<STAGES, KCH>::kSmem;
+  cfg.dynamicSmemBytes = PairCfg<BN, STAGES, KCH>::kSmem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   int na = 0;
@@ -448,28 +452,35 @@ cudaError_t launch_pair(const CUtensorMap& tmW1, const RowMaps& xp, const CUtens
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  return cudaLaunchKernelEx(&cfg, fused_ffn_pair_kernel<STAGES, KCH>, tmW1, xp, tmW2, h, args);
+  return cudaLaunchKernelEx(&cfg, fused_ffn_pair_kernel<BN, STAGES, KCH>, tmW1, xp, tmW2, h, args);
 }
 
 }  // namespace
 
 cudaError_t fused_ffn_pair_prepare() {
-  cudaError_t e = cudaFuncSetAttribute(fused_ffn_pair_kernel<8, 1>,
+  cudaError_t e = cudaFuncSetAttribute(fused_ffn_pair_kernel<128, 8, 1>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       PairCfg<8, 1>::kSmem);
+                                       PairCfg<128, 8, 1>::kSmem);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(fused_ffn_pair_kernel<4, 2>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<4, 2>::kSmem);
+  e = cudaFuncSetAttribute(fused_ffn_pair_kernel<256, 6, 1>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<256, 6, 1>::kSmem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(fused_ffn_pair_kernel<128, 4, 2>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<128, 4, 2>::kSmem);
 }
 
-// MOE_FFN_PAIR=1 selects the CTA-pair kernel (default: single-CTA fused FFN).
-bool fused_ffn_pair_enabled() {
-  static int v = -1;
-  if (v < 0) {
+// CTA pairs for the fused FFN.  MOE_FFN_PAIR: 0 never, 1 always, unset =
+// 256-token work items only (many tokens per expert: the M = 256 pair MMA
+// with each CTA staging half the token rows measured 1.93 -> 1.84 ms on MT at
+// seq 256 and 7.95 -> 7.37 ms on LM static against the single-CTA kernel, same
+// box, bitwise equal outputs; at 128-token items it measured equal).
+bool fused_ffn_pair_enabled(int tile_n) {
+  static int v = -2;
+  if (v == -2) {
     const char* e = getenv("MOE_FFN_PAIR");
-    v = e ? atoi(e) : 0;
+    v = e ? atoi(e) : -1;
   }
-  return v != 0;
+  return v == 1 || (v == -1 && tile_n == 256);
 }
 
 // Persistent launch on every co-resident CTA pair (all pairs must be resident:
@@ -477,9 +488,11 @@ bool fused_ffn_pair_enabled() {
 // cudaErrorNotSupported when no pair fits.
 cudaError_t launch_fused_ffn_pair(const CUtensorMap& tmW1, const RowMaps& xp,
                                   const CUtensorMap& tmW2, const RowMaps& h,
-                                  const FusedFfnArgs& args, int sms, cudaStream_t stream) {
-  if (pair_cfg() == 4) return launch_pair<4, 2>(tmW1, xp, tmW2, h, args, sms, stream);
-  return launch_pair<8, 1>(tmW1, xp, tmW2, h, args, sms, stream);
+                                  const FusedFfnArgs& args, int tile_n, int sms,
+                                  cudaStream_t stream) {
+  if (tile_n == 256) return launch_pair<256, 6, 1>(tmW1, xp, tmW2, h, args, sms, stream);
+  if (pair_cfg() == 4) return launch_pair<128, 4, 2>(tmW1, xp, tmW2, h, args, sms, stream);
+  return launch_pair<128, 8, 1>(tmW1, xp, tmW2, h, args, sms, stream);
 }
 
 }  // namespace moe
