@@ -145,7 +145,7 @@ struct FusedFfnArgs {
                             // 4 = skip MMAs, 8 = skip the epilogue
   int packed;               // tmW1/tmW2 address prepacked 128 x 64 tiles (launch_pack_tiles)
   int full_fence;           // A/B: per-thread fence.sc before publishing an H tile
-  int32_t* tile_ctr;        // zeroed tile counter (dynamic scheduling); null = round robin
+  int32_t* tile_ctr;        // zeroed tile counter for the dynamic tail; null = all round robin
   unsigned long long* prof;  // experiments (MOE_FFN_PROF): per-CTA start/end globaltimer
   int late_trigger;         // let the next kernel launch only as CTAs finish
   int dyn_tail;             // tail tiles claimed dynamically (0 = the last lag * MT2)
@@ -156,7 +156,6 @@ struct FusedFfnArgs {
   const int32_t* arrived_expect;
   int32_t* arrive_err;
   unsigned long long arrive_timeout_ns;
-  int spread;               // tile-order window (items), see ffn_fused.cu TileSeq; <= 1 item-major
 };
 // One activation matrix (Xp or H) seen by TMA at four box heights: a B tile
 // of n rows (n % 8 == 0) is n/64 boxes of 64 rows plus at most one each of 32,
