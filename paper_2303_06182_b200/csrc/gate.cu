@@ -21,6 +21,7 @@
 #include <cooperative_groups.h>
 #include <float.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -90,6 +91,106 @@ __device__ __forceinline__ void topk_insert(float (&bv)[K], int (&bi)[K], float 
     e = t ? ti : e;
     carry = t;
   }
+}
+
+// Top-K epilogue of one 128-token tile (all 8 warps of the CTA): TMEM lane =
+// token, columns = expert logits.  Warps q and q+4 share TMEM lane quadrant q
+// (tokens 32q..32q+31); warps 0-3 scan the first half of the expert columns,
+// warps 4-7 the second half, then the two partial top-K lists are merged
+// through shared memory (the stage buffers, free once tfull fired).
+template <int K>
+__device__ __forceinline__ void gate_epilogue(const GateArgs& a, uint32_t tmem_base,
+                                              uint64_t* tfull, int tok0, uint8_t* smem, int* s_e,
+                                              float* s_w) {
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  ptx::mbar_wait(tfull, 0);
+  ptx::tc_fence_after();
+  const int q = warp & 3;
+  const int half = warp >> 2;
+  const int tl = q * 32 + lane;  // token within the tile
+  const int tok = tok0 + tl;
+  const int nchunk = (a.E + 31) / 32;
+  const int split = (nchunk + 1) / 2;
+  const int c_begin = half ? split * 32 : 0;
+  const int c_end = half ? nchunk * 32 : split * 32;
+  float bv[K];
+  int bi[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    bv[j] = -INFINITY;
+    bi[j] = 0x7fffffff;
+  }
+  for (int c0 = c_begin; c0 < c_end; c0 += 32) {
+    uint32_t r[32];
+    ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + c0, r);
+    ptx::tmem_ld_wait();
+    if (a.logits && tok < a.S) {
+      float* dst = a.logits + static_cast<size_t>(tok) * a.E + c0;
+      if (c0 + 32 <= a.E && (a.E & 3) == 0) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4*>(dst + i) =
+              make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
+                          __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (c0 + i < a.E) dst[i] = __uint_as_float(r[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float v = (c0 + i < a.E) ? __uint_as_float(r[i]) : -INFINITY;
+      if (K == 1) {
+        topk_insert<K>(bv, bi, v, c0 + i);
+      } else if (__any_sync(0xffffffffu, v > bv[K - 1])) {
+        topk_insert<K>(bv, bi, v, c0 + i);
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  // partial lists of the upper half -> smem (stage buffers are free: all TMA
+  // writes landed and all MMAs retired before tfull fired)
+  float* pv = reinterpret_cast<float*>(smem);
+  int* pi = reinterpret_cast<int*>(smem + kBlockM * K * sizeof(float));
+  if (half == 1) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      pv[j * kBlockM + tl] = bv[j];
+      pi[j * kBlockM + tl] = bi[j];
+    }
+  }
+  __syncthreads();
+  if (half == 0 && tok < a.S) {
+    // upper-half ids are all larger, so inserting them in order keeps ties
+    // resolved toward the lower id
+#pragma unroll
+    for (int j = 0; j < K; ++j) topk_insert<K>(bv, bi, pv[j * kBlockM + tl], pi[j * kBlockM + tl]);
+    const int k = a.k;
+    float ex[K];
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      ex[j] = (j < k) ? expf(bv[j] - bv[0]) : 0.f;
+      sum += ex[j];
+    }
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (j < k) {
+        const float wj = (j < k - 1) ? ex[j] / sum : 1.f - acc;
+        acc += wj;
+        a.idx[static_cast<size_t>(tok) * k + j] = bi[j];
+        a.w[static_cast<size_t>(tok) * k + j] = wj;
+        if (s_e) {
+          s_e[tl * k + j] = bi[j];
+          s_w[tl * k + j] = wj;
+        }
+      }
+    }
+  }
+
 }
 
 // One 128-token tile of the gate: TMA + tcgen05 logits, top-K epilogue on all
@@ -207,96 +308,7 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
     __syncwarp();
   }
 
-  // -------------------------------------------------------- epilogue (all 8 warps)
-  // Warps q and q+4 share TMEM lane quadrant q (tokens 32q..32q+31); warps
-  // 0-3 scan the first half of the expert columns, warps 4-7 the second half,
-  // then the two partial top-K lists are merged through shared memory.
-  ptx::mbar_wait(tfull, 0);
-  ptx::tc_fence_after();
-  const int q = warp & 3;
-  const int half = warp >> 2;
-  const int tl = q * 32 + lane;  // token within the tile
-  const int tok = tok0 + tl;
-  const int nchunk = (a.E + 31) / 32;
-  const int split = (nchunk + 1) / 2;
-  const int c_begin = half ? split * 32 : 0;
-  const int c_end = half ? nchunk * 32 : split * 32;
-  float bv[K];
-  int bi[K];
-#pragma unroll
-  for (int j = 0; j < K; ++j) {
-    bv[j] = -INFINITY;
-    bi[j] = 0x7fffffff;
-  }
-  for (int c0 = c_begin; c0 < c_end; c0 += 32) {
-    uint32_t r[32];
-    ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + c0, r);
-    ptx::tmem_ld_wait();
-    if (a.logits && tok < a.S) {
-      float* dst = a.logits + static_cast<size_t>(tok) * a.E + c0;
-      if (c0 + 32 <= a.E && (a.E & 3) == 0) {
-#pragma unroll
-        for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4*>(dst + i) =
-              make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
-                          __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c0 + i < a.E) dst[i] = __uint_as_float(r[i]);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const float v = (c0 + i < a.E) ? __uint_as_float(r[i]) : -INFINITY;
-      if (K == 1) {
-        topk_insert<K>(bv, bi, v, c0 + i);
-      } else if (__any_sync(0xffffffffu, v > bv[K - 1])) {
-        topk_insert<K>(bv, bi, v, c0 + i);
-      }
-    }
-  }
-  ptx::tc_fence_before();
-  // partial lists of the upper half -> smem (stage buffers are free: all TMA
-  // writes landed and all MMAs retired before tfull fired)
-  float* pv = reinterpret_cast<float*>(smem);
-  int* pi = reinterpret_cast<int*>(smem + kBlockM * K * sizeof(float));
-  if (half == 1) {
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      pv[j * kBlockM + tl] = bv[j];
-      pi[j * kBlockM + tl] = bi[j];
-    }
-  }
-  __syncthreads();
-  if (half == 0 && tok < a.S) {
-    // upper-half ids are all larger, so inserting them in order keeps ties
-    // resolved toward the lower id
-#pragma unroll
-    for (int j = 0; j < K; ++j) topk_insert<K>(bv, bi, pv[j * kBlockM + tl], pi[j * kBlockM + tl]);
-    const int k = a.k;
-    float ex[K];
-    float sum = 0.f;
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      ex[j] = (j < k) ? expf(bv[j] - bv[0]) : 0.f;
-      sum += ex[j];
-    }
-    float acc = 0.f;
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      if (j < k) {
-        const float wj = (j < k - 1) ? ex[j] / sum : 1.f - acc;
-        acc += wj;
-        a.idx[static_cast<size_t>(tok) * k + j] = bi[j];
-        a.w[static_cast<size_t>(tok) * k + j] = wj;
-        if (s_e) {
-          s_e[tl * k + j] = bi[j];
-          s_w[tl * k + j] = wj;
-        }
-      }
-    }
-  }
+  gate_epilogue<K>(a, tmem_base, tfull, tok0, smem, s_e, s_w);
 
   __syncthreads();
   ptx::tc_fence_after();
@@ -315,6 +327,134 @@ __device__ __forceinline__ uint8_t* aligned_smem() {
   extern __shared__ uint8_t smem_raw[];
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                     ~static_cast<uintptr_t>(1023));
+}
+
+// ---------------------------------------------------------------- CTA-pair gate
+// For E a multiple of 256 (the LM layer: E = 512) the gate is MMA-bound: a
+// cluster of two CTAs covers 256 tokens with tcgen05.mma.cta_group::2
+// (M = 256, N = 256 per instruction).  Each CTA stages its own 128 X rows and
+// HALF of every 256-expert Wg chunk (the instruction reads the B halves of
+// both CTAs); the leader issues the MMAs and commits to both CTAs' barriers;
+// each CTA then runs the usual top-K epilogue on its own TMEM lanes.
+struct GatePairLayout {
+  int nch;         // 256-expert chunks
+  int stage;       // bytes per stage and CTA: X 8 KB + nch x 128 Wg rows x 64 B
+  int stages;
+  int smem;
+};
+__host__ __device__ inline GatePairLayout gate_pair_layout(int E) {
+  GatePairLayout L;
+  L.nch = (E + 255) / 256;
+  L.stage = kABytes + L.nch * 128 * kBlockK * 2;
+  int s = (200 * 1024 - 2048) / L.stage;
+  L.stages = s > 8 ? 8 : s;
+  L.smem = 1024 + L.stages * L.stage + (2 * L.stages + 2) * 8 + 16;
+  return L;
+}
+
+template <int K>
+__global__ void __launch_bounds__(256, 1)
+    gate_pair_kernel(const __grid_constant__ CUtensorMap tmX,
+                     const __grid_constant__ CUtensorMap tmWg, GateArgs a, int box_rows) {
+  const GatePairLayout L = gate_pair_layout(a.E);
+  uint8_t* smem = aligned_smem();
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.stages * L.stage);
+  uint64_t* empty = full + L.stages;
+  uint64_t* tfull = empty + L.stages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int tok0 = blockIdx.x * kBlockM;  // consecutive blocks form the pair
+  const int KB = a.TD / kBlockK;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmX);
+    ptx::prefetch_tmap(&tmWg);
+    for (int s = 0; s < L.stages; ++s) {
+      ptx::mbar_init(&full[s], 1);   // leader: its producer's arrive (+ both CTAs' bytes)
+      ptx::mbar_init(&empty[s], 1);  // the leader's MMA commit
+    }
+    ptx::mbar_init(tfull, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) {
+    if (L.nch > 1)
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       ptx::smem_u32(tmem_slot)) : "memory");
+    else
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                       ptx::smem_u32(tmem_slot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();  // both CTAs' barriers and TMEM exist before any remote use
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
+
+  if (warp == 0 && lane == 0) {
+    // ------------------------------------------------ producer (both CTAs)
+    const uint64_t pol_x = ptx::policy_evict_first();
+    const uint64_t pol_w = ptx::policy_evict_last();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int kb = 0; kb < KB; ++kb) {
+      ptx::mbar_wait(&empty[stage], phase ^ 1);
+      const uint32_t fb = ptx::leader_smem_addr(&full[stage]);
+      if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * L.stage);
+      uint8_t* st = smem + stage * L.stage;
+      ptx::tma_load_2d_pair(st, &tmX, fb, kb * kBlockK, tok0, pol_x);
+      for (int j = 0; j < L.nch; ++j)
+        for (int r = 0; r < 128; r += box_rows)
+          ptx::tma_load_2d_pair(st + kABytes + (j * 128 + r) * kBlockK * 2, &tmWg, fb, kb * kBlockK,
+                                j * 256 + static_cast<int>(rank) * 128 + r, pol_w);
+      if (++stage == L.stages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ------------------------------------------------ MMA issuer (leader)
+    const uint32_t idesc = ptx::idesc_bf16(2 * kBlockM, 256);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int kb = 0; kb < KB; ++kb) {
+      ptx::mbar_wait(&full[stage], phase);
+      ptx::tc_fence_after();
+      const uint32_t a0 = ptx::smem_u32(smem + stage * L.stage);
+      const uint32_t b0 = a0 + kABytes;
+#pragma unroll
+      for (int kk = 0; kk < kBlockK / 16; ++kk)
+        for (int j = 0; j < L.nch; ++j)
+          ptx::mma_bf16_pair(tmem_base + j * 256, ptx::umma_desc_sw64(a0 + kk * 32),
+                             ptx::umma_desc_sw64(b0 + j * 128 * kBlockK * 2 + kk * 32), idesc,
+                             (kb | kk) != 0 ? 1u : 0u);
+      ptx::mma_commit_pair(&empty[stage]);
+      if (++stage == L.stages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    ptx::mma_commit_pair(tfull);
+  }
+  __syncwarp();
+
+  gate_epilogue<K>(a, tmem_base, tfull, tok0, smem, nullptr, nullptr);
+
+  // the leader's last commits into the peer and the peer's TMA completions on
+  // the leader's barriers must land before either CTA leaves
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  if (warp == 2) {
+    if (L.nch > 1)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 256;" ::"r"(tmem_base) : "memory");
+  }
 }
 
 template <int K, int C>
@@ -568,6 +708,18 @@ cudaError_t gate_prepare(int E) {
       if (e != cudaSuccess) return e;
     }
   }
+  {
+    const int psmem = gate_pair_layout(E).smem;
+    const void* pfns[] = {reinterpret_cast<const void*>(gate_pair_kernel<1>),
+                          reinterpret_cast<const void*>(gate_pair_kernel<2>),
+                          reinterpret_cast<const void*>(gate_pair_kernel<4>),
+                          reinterpret_cast<const void*>(gate_pair_kernel<8>)};
+    for (const void* fn : pfns) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           std::max(psmem, L.smem));
+      if (e != cudaSuccess) return e;
+    }
+  }
   granted = L.smem;
   return cudaSuccess;
 }
@@ -631,12 +783,56 @@ cudaError_t launch_gate_k(const CUtensorMap& tmX, const CUtensorMap& tmWg, const
   return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 1>, tmX, tmWg, a);
 }
 
+template <int K>
+cudaError_t launch_gate_pair_k(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateArgs& a,
+                               int tiles, cudaStream_t stream) {
+  const GatePairLayout P = gate_pair_layout(a.E);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((tiles + 1) / 2 * 2);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = P.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  attr[n].id = cudaLaunchAttributeClusterDimension;
+  attr[n].val.clusterDim.x = 2;
+  attr[n].val.clusterDim.y = 1;
+  attr[n].val.clusterDim.z = 1;
+  ++n;
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, gate_pair_kernel<K>, tmX, tmWg, a, gate_layout(a.E).box_rows);
+}
+
+// CTA-pair gate for E a multiple of 256: MOE_GATE_PAIR=1.  Off by default:
+// correct (all GPU tests pass with it) but measured 31.2 vs 29.7 us at LM
+// (same box): the gate is not MMA-bound, and the pair gives up the 4-CTA Wg
+// multicast.
+bool gate_pair_enabled(int E) {
+  static const int v = [] {
+    const char* e = getenv("MOE_GATE_PAIR");
+    return e ? atoi(e) : 0;
+  }();
+  return v != 0 && E % 256 == 0 && 128 % gate_layout(E).box_rows == 0;
+}
+
 cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateArgs& a,
                         cudaStream_t stream) {
   if (a.k < 1 || a.k > kMaxK || a.E > 512 || a.E < a.k || (a.TD % kBlockK) != 0)
     return cudaErrorInvalidValue;
   const GateLayout L = gate_layout(a.E);
   const int tiles = (a.S + kBlockM - 1) / kBlockM;
+  if (gate_pair_enabled(a.E)) {
+    if (a.k == 1) return launch_gate_pair_k<1>(tmX, tmWg, a, tiles, stream);
+    if (a.k == 2) return launch_gate_pair_k<2>(tmX, tmWg, a, tiles, stream);
+    if (a.k <= 4) return launch_gate_pair_k<4>(tmX, tmWg, a, tiles, stream);
+    return launch_gate_pair_k<8>(tmX, tmWg, a, tiles, stream);
+  }
   // cached per (E, tiles): the occupancy query is not free
   static std::mutex mu;
   static std::map<std::pair<int, int>, int> cache;
