@@ -167,6 +167,12 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ int last_consumer;
+  // dynamic tail (as ffn_fused.cu): the leader's producer claims the tail's
+  // pair-tiles from a global counter and hands them to its MMA / epilogue
+  // warps and to the peer's producer / epilogue warps through this ring
+  constexpr int kRing = 4;
+  __shared__ int ring_t[kRing];
+  __shared__ __align__(8) uint64_t ring_full[kRing], ring_empty[kRing];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -189,6 +195,11 @@ __global__ void __launch_bounds__(256, 1)
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
       ptx::mbar_init(&tempty[s], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    for (int s = 0; s < kRing; ++s) {
+      ptx::mbar_init(&ring_full[s], 1);
+      // leader's copy: leader MMA + 4 leader epilogue warps + peer producer + 4 peer epilogue warps
+      ptx::mbar_init(&ring_empty[s], 10);
     }
     ptx::fence_barrier_init();
   }
@@ -218,6 +229,44 @@ __global__ void __launch_bounds__(256, 1)
   const int total = n * (P1 + P2);
   const int cid = blockIdx.x >> 1;
   const int ncl = gridDim.x >> 1;
+  const int t_dyn = g.tile_ctr ? max(0, total - (g.dyn_tail > 0 ? g.dyn_tail / 2 : L * P2)) : total;
+  int rs = 0;
+  uint32_t rph = 0;
+  // leader producer: claim the next tail tile, publish it in both CTAs' rings
+  auto claim = [&]() -> int {
+    if (!g.tile_ctr) return -1;
+    const int c = t_dyn + atomicAdd(g.tile_ctr, 1);
+    const int t = c < total ? c : -1;
+    ptx::mbar_wait_cluster(&ring_empty[rs], rph ^ 1);
+    ring_t[rs] = t;
+    uint32_t peer_t, peer_full;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 1;" : "=r"(peer_t) : "r"(ptx::smem_u32(&ring_t[rs])));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 1;" : "=r"(peer_full) : "r"(ptx::smem_u32(&ring_full[rs])));
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(peer_t), "r"(t) : "memory");
+    ptx::mbar_arrive(&ring_full[rs]);
+    arrive_remote(peer_full);
+    if (++rs == kRing) {
+      rs = 0;
+      rph ^= 1;
+    }
+    return t;
+  };
+  // every other consumer: read the slot, then release it on the leader's copy
+  auto take = [&](bool warp_wide) -> int {
+    if (!g.tile_ctr) return -1;
+    ptx::mbar_wait_cluster(&ring_full[rs], rph);
+    const int t = ring_t[rs];
+    if (warp_wide) __syncwarp();
+    if (!warp_wide || lane == 0) {
+      if (leader) ptx::mbar_arrive(&ring_empty[rs]);
+      else arrive_remote(leader_addr(&ring_empty[rs]));
+    }
+    if (++rs == kRing) {
+      rs = 0;
+      rph ^= 1;
+    }
+    return t;
+  };
 
   if (warp == 0 && lane == 0) {
     // ------------------------------------------------------------ producer (both CTAs)
@@ -225,7 +274,8 @@ __global__ void __launch_bounds__(256, 1)
     const uint64_t pol_x = ptx::policy_evict_last();
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = cid; t < total; t += ncl) {
+    auto next = [&]() -> int { return leader ? claim() : take(false); };
+    for (int t = cid < t_dyn ? cid : next(); t >= 0; t = t + ncl < t_dyn ? t + ncl : next()) {
       const TileRef tr = decode_tile(t, n, L, P1, P2);
       const FfnItem it = items[tr.item];
       const int nrows = (it.len + 15) & ~15;
@@ -275,7 +325,8 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = cid; t < total; t += ncl) {
+    for (int t = cid < t_dyn ? cid : take(false); t >= 0;
+         t = t + ncl < t_dyn ? t + ncl : take(false)) {
       const TileRef tr = decode_tile(t, n, L, P1, P2);
       const FfnItem it = items[tr.item];
       const int nn = (it.len + 15) & ~15;
@@ -314,7 +365,8 @@ __global__ void __launch_bounds__(256, 1)
     const uint32_t tempty_l[2] = {leader_addr(&tempty[0]), leader_addr(&tempty[1])};
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = cid; t < total; t += ncl) {
+    for (int t = cid < t_dyn ? cid : take(true); t >= 0;
+         t = t + ncl < t_dyn ? t + ncl : take(true)) {
       const TileRef tr = decode_tile(t, n, L, P1, P2);
       const FfnItem it = items[tr.item];
       const int m = 2 * tr.mp + rank;

@@ -62,6 +62,22 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   return ok != 0;
 }
 
+// Same, acquiring at cluster scope (data released by another CTA of the cluster)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t ok = 0, polls = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred done;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 done, [%1], %2, 100000;\n\t"
+        "selp.u32 %0, 1, 0, done;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (!ok && ++polls == (1u << 26)) __trap();
+  }
+}
+
 // Blocking wait for the phase with the given parity.  A watchdog turns a
 // pipeline deadlock into a trapped launch (cudaErrorLaunchFailure) after
 // ~2^26 polls instead of a hung GPU.
