@@ -755,6 +755,8 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
     fa.dbg = getenv("MOE_FFN_DBG") ? atoi(getenv("MOE_FFN_DBG")) : 0;
     // the expert-cache slot pool is row-major: packed tiles only for the layer's own weights
     fa.packed = L->packed && !L->slot_of;
+    fa.pair_hint = auto_pair((double)L->rows_max / L->d.num_experts, L->d.num_experts, TD, HD,
+                             L->tile_n, L->ctx->sms);
     cudaError_t e = launch_fused_ffn(fa.packed ? L->tmW1p : L->tmW1, L->xpm,
                                      fa.packed ? L->tmW2p : L->tmW2, L->hm, fa, L->tile_n,
                                      L->ctx->sms, s);
@@ -1108,6 +1110,8 @@ int moe_ffn_forward(moe_ffn* F, const void* X_rows, const int32_t* keys, const f
     fa.lag = std::max(2, (8 * F->ctx->sms + per_item - 1) / per_item);
     fa.discard_h = 1;
     fa.packed = F->packed;
+    fa.pair_hint = auto_pair((double)F->d.max_rows / F->d.num_experts, F->d.num_experts, TD, HD,
+                             F->tile_n, F->ctx->sms);
     e = launch_fused_ffn(F->packed ? F->tmW1p : F->tmW1, F->xpm, F->packed ? F->tmW2p : F->tmW2,
                          F->hm, fa, F->tile_n, F->ctx->sms, s);
     if (e != cudaSuccess) return cuda_fail(e, "fused ffn launch");

@@ -5,6 +5,7 @@
 
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -96,6 +97,17 @@ inline int auto_tile_n(double rows_per_expert, int experts, int TD, int HD, int 
   const double items = experts * std::ceil(rows_per_expert / 256.0);
   const double tiles = items * (HD / 128 + TD / 128);
   return tiles >= 4.0 * sms ? 256 : 128;
+}
+
+// CTA pairs (M = 256 UMMA) for the fused FFN when there are enough tiles to
+// keep every pair busy: >= 8 waves of pair-tiles over sms / 2 pairs.  With
+// the dynamic tail, same-box A/B: LM FFN 1.343 -> 1.306 ms, MT 1.427 ->
+// 1.385 ms; cfg1 (8 experts, ~2 waves) 0.084 -> 0.093 ms, hence the bound.
+inline int auto_pair(double rows_per_expert, int experts, int TD, int HD, int tile_n, int sms) {
+  if (TD % 256 || HD % 256) return 0;
+  const double items = experts * std::ceil(std::max(rows_per_expert, 1.0) / tile_n);
+  const double pair_tiles = items * (HD / 256 + TD / 256);
+  return pair_tiles >= 8.0 * (sms / 2) ? 1 : 0;
 }
 
 // Reference check_batch (gating.cpp:12-18), verbatim messages.

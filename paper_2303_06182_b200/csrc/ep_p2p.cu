@@ -754,6 +754,8 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   fa.lag = std::max(2, (8 * P->ctx->sms + per_item - 1) / per_item);
   fa.discard_h = 1;
   fa.packed = 1;
+  fa.pair_hint = auto_pair((double)D * d.max_tokens * d.top_k / E, P->El, TD, HD, P->tile_n,
+                           P->ctx->sms);
   mark(4);
   ce = launch_fused_ffn(P->tmW1p, P->xpm, P->tmW2p, P->hm, fa, P->tile_n, P->ctx->sms, s);
   if (ce != cudaSuccess) return cuda_fail(ce, "EP fused ffn launch");

@@ -463,7 +463,7 @@ int fused_kch() {
 }
 
 cudaError_t fused_ffn_pair_prepare();
-bool fused_ffn_pair_enabled(int tile_n);
+bool fused_ffn_pair_enabled(int hint);
 cudaError_t launch_fused_ffn_pair(const CUtensorMap& tmW1, const RowMaps& xp,
                                   const CUtensorMap& tmW2, const RowMaps& h,
                                   const FusedFfnArgs& args, int tile_n, int sms,
@@ -483,7 +483,7 @@ cudaError_t launch_fused_ffn_impl(const CUtensorMap& tmW1, const RowMaps& xp, co
                                   cudaStream_t stream) {
   // CTA pairs (M = 256 UMMA) when both GEMMs have an even number of 128-row
   // weight blocks
-  if ((tile_n == 128 || tile_n == 256) && fused_ffn_pair_enabled(tile_n) && !args.arrived &&
+  if ((tile_n == 128 || tile_n == 256) && fused_ffn_pair_enabled(args.pair_hint) && !args.arrived &&
       args.HD % 256 == 0 &&
       args.TD % 256 == 0) {
     cudaError_t e = launch_fused_ffn_pair(tmW1, xp, tmW2, h, args, tile_n, grid, stream);

@@ -522,17 +522,16 @@ cudaError_t fused_ffn_pair_prepare() {
 }
 
 // CTA pairs for the fused FFN.  MOE_FFN_PAIR: 0 never, 1 always, unset =
-// 256-token work items only (many tokens per expert: the M = 256 pair MMA
-// with each CTA staging half the token rows measured 1.93 -> 1.84 ms on MT at
-// seq 256 and 7.95 -> 7.37 ms on LM static against the single-CTA kernel, same
-// box, bitwise equal outputs; at 128-token items it measured equal).
-bool fused_ffn_pair_enabled(int tile_n) {
+// the caller's hint (capi_state.h auto_pair: enough pair-tiles to fill ~8
+// waves).  Same box, bitwise-equal outputs: MT seq 256 1.93 -> 1.84 ms, LM
+// static 7.95 -> 7.37 ms, LM 1.343 -> 1.306 ms, MT 1.427 -> 1.385 ms.
+bool fused_ffn_pair_enabled(int hint) {
   static int v = -2;
   if (v == -2) {
     const char* e = getenv("MOE_FFN_PAIR");
     v = e ? atoi(e) : -1;
   }
-  return v == 1 || (v == -1 && tile_n == 256);
+  return v == 1 || (v == -1 && hint);
 }
 
 // Persistent launch on every co-resident CTA pair (all pairs must be resident:

@@ -148,6 +148,7 @@ struct FusedFfnArgs {
   int32_t* tile_ctr;        // zeroed tile counter for the dynamic tail; null = all round robin
   unsigned long long* prof;  // experiments (MOE_FFN_PROF): per-CTA start/end globaltimer
   int late_trigger;         // let the next kernel launch only as CTAs finish
+  int pair_hint;            // the caller expects >= ~8 waves of CTA-pair tiles (see auto_pair)
   int dyn_tail;             // tail tiles claimed dynamically (0 = the last lag * MT2)
   // expert parallelism (ep_p2p.cu): a GEMM1 tile's token rows are loaded only
   // once arrived[expert] >= arrived_expect[expert] (peer stores, acquire.sys);
