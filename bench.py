@@ -710,8 +710,11 @@ def run_b200(args):
                    "parallelism": f"replicas x{world} (all experts on every GPU)" if world > 1 else "single GPU",
                    "l2": "no flush: per-step working set (expert weights, %.1f GB) >> 126 MB L2" % (
                        2 * active * TD * HD * 2 / 1e9)},
-        "roofline": {"kernel": ("fused_ffn_kernel (GEMM1+GEMM2, one launch, H in L2)" if one_launch
-                                else "grouped_gemm_kernel (FFN GEMM1 + GEMM2)"),
+        "roofline": {"kernel": {0: "grouped_gemm_kernel (FFN GEMM1 + GEMM2, two launches)",
+                                1: "fused_ffn_kernel (GEMM1+GEMM2, one launch, H in L2)",
+                                2: "fused_ffn_pair_kernel (GEMM1+GEMM2, one launch, H in L2, CTA pairs: "
+                                   "tcgen05.mma.cta_group::2, M=256)"}.get(int(v.get("ffn_kernel", 1)),
+                                                                          "fused_ffn_kernel"),
                      "bound": "tensor" if tensor_bound else "hbm",
                      "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
                      "peak_kind": peak_kind + (" (sustained)" if tensor_bound and ffn_ms > 1.0 else ""),

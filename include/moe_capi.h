@@ -243,6 +243,8 @@ typedef struct moe_layer_view {
   int rows;            /* rows of xp/h/yw used by the last forward */
   int capacity;        /* static capacity of the last forward */
   int tile_n;
+  int ffn_kernel;      /* FFN of the last forward: 0 two launches, 1 fused
+                          one-SM, 2 fused CTA pairs (cta_group::2) */
 } moe_layer_view;
 int moe_layer_get_view(moe_layer* layer, moe_layer_view* view);
 

@@ -82,7 +82,7 @@ class LayerView(C.Structure):
         ("splits", C.c_void_p), ("order", C.c_void_p), ("pos", C.c_void_p),
         ("dropped", C.c_void_p), ("n_dropped", C.c_void_p), ("xp", C.c_void_p),
         ("h", C.c_void_p), ("yw", C.c_void_p), ("n_items", C.c_void_p), ("rows", C.c_int),
-        ("capacity", C.c_int), ("tile_n", C.c_int),
+        ("capacity", C.c_int), ("tile_n", C.c_int), ("ffn_kernel", C.c_int),
     ]
 
 

@@ -757,6 +757,7 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
     fa.packed = L->packed && !L->slot_of;
     fa.pair_hint = auto_pair((double)L->rows_max / L->d.num_experts, L->d.num_experts, TD, HD,
                              L->tile_n, L->ctx->sms);
+    L->last_ffn_kernel = fused_ffn_uses_pair(fa, L->tile_n) ? 2 : 1;
     cudaError_t e = launch_fused_ffn(fa.packed ? L->tmW1p : L->tmW1, L->xpm,
                                      fa.packed ? L->tmW2p : L->tmW2, L->hm, fa, L->tile_n,
                                      L->ctx->sms, s);
@@ -764,6 +765,7 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
     mark(4);
     return MOE_OK;
   }
+  L->last_ffn_kernel = 0;
   GemmArgs g1{L->items.p, L->n_items.p, L->slot_of, HD, TD, kEpiReluBf16, L->h.p, nullptr, nullptr,
               off, e_lo, e_hi};
   cudaError_t e = launch_grouped_gemm(L->tmW1, L->tmXp, g1, L->tile_n, L->ctx->sms, s);
@@ -1145,6 +1147,7 @@ int moe_layer_get_view(moe_layer* L, moe_layer_view* v) {
   v->rows = L->last_rows;
   v->capacity = L->last_cap;
   v->tile_n = L->tile_n;
+  v->ffn_kernel = L->last_ffn_kernel;
   return MOE_OK;
 }
 

@@ -208,6 +208,7 @@ struct moe_layer {
   int last_rows = 0;
   int last_cap = 0;
   bool counters_zeroed = false;  // the route kernel of this forward zeroed `done`
+  int last_ffn_kernel = 0;       // moe_layer_view::ffn_kernel
   // per-stage timing ring (eager path)
   std::vector<cudaEvent_t> tev;
   int t_slots = 0;

@@ -478,14 +478,17 @@ cudaError_t fused_ffn_prepare() {
   return prepare_fused<256, 4, 1>();
 }
 
+bool fused_ffn_uses_pair(const FusedFfnArgs& args, int tile_n) {
+  return (tile_n == 128 || tile_n == 256) && fused_ffn_pair_enabled(args.pair_hint) &&
+         !args.arrived && args.HD % 256 == 0 && args.TD % 256 == 0;
+}
+
 cudaError_t launch_fused_ffn_impl(const CUtensorMap& tmW1, const RowMaps& xp, const CUtensorMap& tmW2,
                                   const RowMaps& h, const FusedFfnArgs& args, int tile_n, int grid,
                                   cudaStream_t stream) {
   // CTA pairs (M = 256 UMMA) when both GEMMs have an even number of 128-row
   // weight blocks
-  if ((tile_n == 128 || tile_n == 256) && fused_ffn_pair_enabled(args.pair_hint) && !args.arrived &&
-      args.HD % 256 == 0 &&
-      args.TD % 256 == 0) {
+  if (fused_ffn_uses_pair(args, tile_n)) {
     cudaError_t e = launch_fused_ffn_pair(tmW1, xp, tmW2, h, args, tile_n, grid, stream);
     if (e != cudaErrorNotSupported) return e;
   }

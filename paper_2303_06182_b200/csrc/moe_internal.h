@@ -165,6 +165,8 @@ struct RowMaps {
   CUtensorMap m8, m16, m32, m64;
 };
 cudaError_t fused_ffn_prepare();
+// whether launch_fused_ffn will run the CTA-pair kernel for these arguments
+bool fused_ffn_uses_pair(const FusedFfnArgs& args, int tile_n);
 cudaError_t launch_fused_ffn(const CUtensorMap& tmW1, const RowMaps& xp, const CUtensorMap& tmW2,
                              const RowMaps& h, const FusedFfnArgs& args, int tile_n, int grid,
                              cudaStream_t stream);

@@ -187,7 +187,7 @@ class MoeLayer:
             "pos": wrap(v.pos, S * k, torch.int32), "n_items": wrap(v.n_items, 1, torch.int32),
             "xp": wrap(v.xp, rows * TD, torch.bfloat16), "h": wrap(v.h, rows * HD, torch.bfloat16),
             "yw": wrap(v.yw, rows * TD, torch.bfloat16), "rows": rows, "capacity": v.capacity,
-            "tile_n": v.tile_n,
+            "tile_n": v.tile_n, "ffn_kernel": v.ffn_kernel,
         }
         if v.dropped:
             out["dropped"] = wrap(v.dropped, 2 * S * k, torch.int32)
