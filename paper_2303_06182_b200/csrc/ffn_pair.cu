@@ -445,12 +445,14 @@ __global__ void __launch_bounds__(256, 1)
   if (g.late_trigger) pdl_trigger();
 }
 
-// MOE_FFN_PAIR_STAGES=4 selects 4 stages of 128-deep k (default: 8 x 64)
+// Pair stage shape: 4 stages of 128-deep k (two 64-wide chunks, default:
+// LM FFN 1.303 -> 1.284 ms, MT 1.384 -> 1.340 ms against 8 x 64-deep on the
+// same box) or MOE_FFN_PAIR_STAGES=8 for 8 x 64-deep.
 int pair_cfg() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("MOE_FFN_PAIR_STAGES");
-    v = (e && atoi(e) == 4) ? 4 : 8;
+    v = (e && atoi(e) == 8) ? 8 : 4;
   }
   return v;
 }
@@ -517,6 +519,9 @@ cudaError_t fused_ffn_pair_prepare() {
   e = cudaFuncSetAttribute(fused_ffn_pair_kernel<256, 6, 1>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<256, 6, 1>::kSmem);
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(fused_ffn_pair_kernel<256, 3, 2>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<256, 3, 2>::kSmem);
+  if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(fused_ffn_pair_kernel<128, 4, 2>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<128, 4, 2>::kSmem);
 }
@@ -541,7 +546,17 @@ cudaError_t launch_fused_ffn_pair(const CUtensorMap& tmW1, const RowMaps& xp,
                                   const CUtensorMap& tmW2, const RowMaps& h,
                                   const FusedFfnArgs& args, int tile_n, int sms,
                                   cudaStream_t stream) {
-  if (tile_n == 256) return launch_pair<256, 6, 1>(tmW1, xp, tmW2, h, args, sms, stream);
+  if (tile_n == 256) {
+    // 3 x 128-deep k stages (default: MT seq 256 FFN 1.82 -> 1.78-1.80 ms,
+    // LM static 7.76 -> 7.59-7.68 ms against 6 x 64, same box);
+    // MOE_FFN_PAIR256_STAGES=6 restores 6 x 64
+    static const int s256 = [] {
+      const char* e = getenv("MOE_FFN_PAIR256_STAGES");
+      return e ? atoi(e) : 3;
+    }();
+    if (s256 == 3) return launch_pair<256, 3, 2>(tmW1, xp, tmW2, h, args, sms, stream);
+    return launch_pair<256, 6, 1>(tmW1, xp, tmW2, h, args, sms, stream);
+  }
   if (pair_cfg() == 4) return launch_pair<128, 4, 2>(tmW1, xp, tmW2, h, args, sms, stream);
   return launch_pair<128, 8, 1>(tmW1, xp, tmW2, h, args, sms, stream);
 }
