@@ -672,7 +672,7 @@ def run_b200(args):
     value = world * S / (ms_per_step * 1e-3)
     mean_stage = stage.mean(0)
     one_launch = ((mode == "dynamic" or os.environ.get("MOE_FUSED_STATIC", "1") != "0")
-                  and int(v["tile_n"]) in (128, 256) and not args.split_ffn and not args.fuse_combine
+                  and int(v["tile_n"]) in (128, 256) and not args.split_ffn
                   and (int(v["tile_n"]) == 128 or os.environ.get("MOE_FUSED_256", "1") != "0"))
     launches_per_step = ((1 if args.fuse_front else 3) + (1 if one_launch else 2)
                          + (0 if args.fuse_combine else 1))

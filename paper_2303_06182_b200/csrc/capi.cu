@@ -712,7 +712,7 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
     const char* e = getenv("MOE_FUSED_STATIC");
     return e ? atoi(e) : 1;
   }();
-  const bool one_launch = !L->d.split_ffn && !fcomb &&
+  const bool one_launch = !L->d.split_ffn &&
                           (L->d.mode == MOE_GATING_DYNAMIC || fused_static) &&
                           (L->tile_n == 128 || fused256_enabled());
   if (one_launch) {
@@ -757,6 +757,17 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
     fa.packed = L->packed && !L->slot_of;
     fa.pair_hint = auto_pair((double)L->rows_max / L->d.num_experts, L->d.num_experts, TD, HD,
                              L->tile_n, L->ctx->sms);
+    if (fcomb && L->d.top_k == 1) {
+      // one contribution per token: GEMM2 writes the layer output row directly
+      fa.Yw = static_cast<__nv_bfloat16*>(L->fwd_out);
+      fa.out_rows = L->order.p;
+    } else if (fcomb) {
+      fa.top_k = L->d.top_k;
+      fa.comb_order = L->order.p;
+      fa.comb_pos = L->pos.p;
+      fa.comb_cnt = L->comb_cnt.p;
+      fa.comb_out = static_cast<__nv_bfloat16*>(L->fwd_out);
+    }
     L->last_ffn_kernel = fused_ffn_uses_pair(fa, L->tile_n) ? 2 : 1;
     cudaError_t e = launch_fused_ffn(fa.packed ? L->tmW1p : L->tmW1, L->xpm,
                                      fa.packed ? L->tmW2p : L->tmW2, L->hm, fa, L->tile_n,

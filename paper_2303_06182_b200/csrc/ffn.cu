@@ -18,6 +18,7 @@
 // Two TMEM accumulators (2 x tile_n columns) let the epilogue of tile i
 // overlap the MMAs of tile i+1.  Tiles = (work item, 128-row m-block); the
 // work list comes from the route kernel, so no host sync is needed.
+#include "combine_epi.cuh"
 #include "moe_internal.h"
 #include "ptx.cuh"
 
@@ -40,56 +41,12 @@ struct GemmCfg {
   static constexpr int kTmemCols = 2 * BN;
 };
 
-// Fused combine for one GEMM2 tile (128 output features x it.len rows), run
-// by the 4 epilogue warps (tid 0..127) after the tile's bf16 partials
-// (gate-weighted, Yw[row]) are stored.  Each row bumps its token's counter for
-// this 128-feature block; the k-th arrival is the finisher, which sums the k
-// partials of the token in slot order (j = 0..k-1) in fp32 and writes the
-// bf16 layer output -- the arithmetic of combine_kernel, so the result is
-// bitwise the same whatever order the contributions arrive in.  All rows of
-// the tile are handled together: one fence, one round of atomics, one round
-// of partial loads.
+// Fused combine for one GEMM2 tile (combine_epi.cuh).
 __device__ __forceinline__ void combine_tile(const GemmArgs& g, const FfnItem& it, int m, int MT,
                                              int tid, int* fin_tok, int* fin_cnt) {
-  const int k = g.top_k;
-  __threadfence();  // this thread's partial stores are visible device-wide
-  if (tid == 0) fin_cnt[0] = 0;
-  asm volatile("bar.sync 1, 128;" ::: "memory");
-  for (int r = tid; r < it.len; r += 128) {
-    const int tk = g.comb_order[it.row0 + r] / k;
-    int* cnt = g.comb_cnt + static_cast<size_t>(tk) * MT + m;
-    if (atomicAdd(cnt, 1) == k - 1) {
-      *cnt = 0;  // self-reset for the next forward
-      fin_tok[atomicAdd(fin_cnt, 1)] = tk;
-    }
-  }
-  __threadfence();
-  asm volatile("bar.sync 1, 128;" ::: "memory");
-  const int nfin = fin_cnt[0];
-  const int col = m * 128;
-  for (int w = tid; w < nfin * 16; w += 128) {
-    const int tk = fin_tok[w >> 4];
-    const int c = (w & 15) * 8;  // 8 bf16 = 16 bytes
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int j = 0; j < k; ++j) {
-      const int p = g.comb_pos[static_cast<size_t>(tk) * k + j];
-      const uint4 v = __ldcg(reinterpret_cast<const uint4*>(g.out + static_cast<size_t>(p) * g.m_total +
-                                                             col + c));
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float2 f = __bfloat1622float2(h[i]);
-        acc[2 * i] += f.x;
-        acc[2 * i + 1] += f.y;
-      }
-    }
-    uint4 o;
-    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
-    *reinterpret_cast<uint4*>(g.comb_out + static_cast<size_t>(tk) * g.m_total + col + c) = o;
-  }
-  asm volatile("bar.sync 1, 128;" ::: "memory");  // fin_tok is reused by the next tile
+  (void)MT;
+  combine_rows_epilogue(g.out, g.m_total, g.top_k, g.comb_order, g.comb_pos, g.comb_cnt,
+                        g.comb_out, it.row0, it.len, m, tid, fin_tok, fin_cnt);
 }
 
 template <int BN, int STAGES>

@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "combine_epi.cuh"
 #include "moe_internal.h"
 #include "ptx.cuh"
 
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ int last_consumer;
+  __shared__ int fin_tok[256], fin_cnt;  // combine epilogue (g.comb_out)
   // dynamic tail: tiles [t_dyn, total) are claimed from a global counter by
   // the producer and handed to the MMA / epilogue warps through this ring
   constexpr int kRing = 4;
@@ -410,6 +412,9 @@ __global__ void __launch_bounds__(256, 1)
           if (tid == 0) red_release_add(done1 + tr.item, 1);
         }
       } else {
+        if (g.comb_out)
+          combine_rows_epilogue(g.Yw, g.TD, g.top_k, g.comb_order, g.comb_pos, g.comb_cnt,
+                                g.comb_out, it.row0, it.len, tr.m, tid, fin_tok, &fin_cnt);
         // this tile's MMAs (hence its H reads) are complete; the last consumer
         // of the item drops the item's H lines from L2 without write-back
         asm volatile("bar.sync 1, 128;" ::: "memory");

@@ -22,6 +22,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "combine_epi.cuh"
 #include "moe_internal.h"
 #include "ptx.cuh"
 
@@ -167,6 +168,7 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ int last_consumer;
+  __shared__ int fin_tok[256], fin_cnt;  // combine epilogue (g.comb_out)
   // dynamic tail (as ffn_fused.cu): the leader's producer claims the tail's
   // pair-tiles from a global counter and hands them to its MMA / epilogue
   // warps and to the peer's producer / epilogue warps through this ring
@@ -418,6 +420,9 @@ __global__ void __launch_bounds__(256, 1)
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (tid == 0) atomicAdd(done1 + tr.item, 1);
       } else {
+        if (g.comb_out)
+          combine_rows_epilogue(g.Yw, g.TD, g.top_k, g.comb_order, g.comb_pos, g.comb_cnt,
+                                g.comb_out, it.row0, it.len, m, tid, fin_tok, &fin_cnt);
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (tid == 0) last_consumer = atomicAdd(done2 + tr.item, 1) == MT2 - 1;
         asm volatile("bar.sync 1, 128;" ::: "memory");

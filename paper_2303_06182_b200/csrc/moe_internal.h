@@ -157,6 +157,12 @@ struct FusedFfnArgs {
   const int32_t* arrived_expect;
   int32_t* arrive_err;
   unsigned long long arrive_timeout_ns;
+  // combine in the GEMM2 epilogue (combine_epi.cuh); comb_out null = off
+  int top_k;
+  const int32_t* comb_order;  // row -> slot (token * k + j)
+  const int32_t* comb_pos;    // slot -> row
+  int32_t* comb_cnt;          // [tokens, TD / 128], zero between forwards
+  __nv_bfloat16* comb_out;    // [tokens, TD]
 };
 // One activation matrix (Xp or H) seen by TMA at four box heights: a B tile
 // of n rows (n % 8 == 0) is n/64 boxes of 64 rows plus at most one each of 32,

@@ -271,14 +271,17 @@ def test_repeat_forward_is_deterministic():
 
 @pytest.mark.parametrize("S,TD,HD,E,k", [(300, 256, 512, 8, 2), (1000, 256, 384, 16, 1), (257, 128, 256, 33, 3),
                                          (2048, 1024, 4096, 8, 1), (4096, 1024, 2048, 64, 2),
-                                         (16384, 1024, 4096, 512, 2)])
-def test_fused_combine_bitwise_equal_combine_kernel(S, TD, HD, E, k):
+                                         (16384, 1024, 4096, 512, 2), (6144, 2048, 8192, 128, 2)])
+@pytest.mark.parametrize("split", [False, True])
+def test_fused_combine_bitwise_equal_combine_kernel(S, TD, HD, E, k, split):
     """The combine inside the GEMM2 epilogue computes exactly the arithmetic of
-    the separate combine kernel, whatever order the k contributions land in."""
+    the separate combine kernel, whatever order the k contributions land in --
+    in the persistent fused FFN (1-SM or CTA-pair kernel) and in the two-launch
+    grouped GEMM."""
     shape = LayerShape(TD, HD, E, k)
     w = make_weights(shape, seed=SEED)
     x = make_tokens(S, TD, seed=SEED)
-    fused = MoeLayer(shape, S, weights=w, fuse_combine=True)
+    fused = MoeLayer(shape, S, weights=w, fuse_combine=True, split_ffn=split)
     plain = MoeLayer(shape, S, weights=w)
     a = fused(x)
     b = plain(x)
