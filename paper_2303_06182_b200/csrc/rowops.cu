@@ -161,6 +161,65 @@ __global__ void __launch_bounds__(256)
   if (late) pdl_trigger();
 }
 
+// Same arithmetic as combine_kernel for a compile-time k: the token's k slot
+// rows are read once, then each lane keeps 4 x k independent 16-byte loads in
+// flight (the generic loop has k, behind a dependent pos load).  Sums stay in
+// slot order, dropped slots (pos < 0) are skipped: bitwise equal.
+template <int K>
+__global__ void __launch_bounds__(256)
+    combine_k_kernel(const uint4* __restrict__ Yw, const int32_t* __restrict__ pos, int S,
+                     int vec_per_row, uint4* __restrict__ out, int late) {
+  if (!late) pdl_trigger();
+  pdl_wait();
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp; t < S; t += nwarps) {
+    const uint4* src[K];
+    bool live[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int p = pos[static_cast<size_t>(t) * K + j];
+      live[j] = p >= 0;
+      src[j] = Yw + static_cast<size_t>(live[j] ? p : 0) * vec_per_row;
+    }
+    uint4* dst = out + static_cast<size_t>(t) * vec_per_row;
+    int v = lane;
+    for (; v + 96 < vec_per_row; v += 128) {
+      uint4 x[K][4];
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (live[j]) x[j][u] = __ldg(src[j] + v + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+          if (live[j]) add_bf16x8(acc, x[j][u]);
+        uint4 o;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+        dst[v + 32 * u] = o;
+      }
+    }
+    for (; v < vec_per_row; v += 32) {
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (live[j]) add_bf16x8(acc, __ldg(src[j] + v));
+      uint4 o;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+      dst[v] = o;
+    }
+  }
+  if (late) pdl_trigger();
+}
+
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
@@ -255,9 +314,25 @@ cudaError_t launch_gather_rows(const __nv_bfloat16* X, const int32_t* order, int
 cudaError_t launch_combine(const __nv_bfloat16* Yw, const int32_t* pos, int S, int k, int TD,
                            __nv_bfloat16* out, cudaStream_t stream) {
   if (S <= 0) return cudaSuccess;
-  return launch_chain(combine_kernel, dim3(grid_for(S, sm_count())), dim3(256), 0, stream, false,
-                      reinterpret_cast<const uint4*>(Yw), pos, S, k, TD / 8,
-                      reinterpret_cast<uint4*>(out), late_trigger("MOE_COMBINE_LATE_TRIGGER", 1));
+  const int late = late_trigger("MOE_COMBINE_LATE_TRIGGER", 1);
+  static const bool by_k = [] {
+    const char* e = getenv("MOE_COMBINE_K");
+    return e ? atoi(e) != 0 : true;
+  }();
+  const dim3 grid(grid_for(S, sm_count()));
+  const uint4* y = reinterpret_cast<const uint4*>(Yw);
+  uint4* o = reinterpret_cast<uint4*>(out);
+  if (by_k) {
+    switch (k) {
+      case 1: return launch_chain(combine_k_kernel<1>, grid, dim3(256), 0, stream, false, y, pos, S, TD / 8, o, late);
+      case 2: return launch_chain(combine_k_kernel<2>, grid, dim3(256), 0, stream, false, y, pos, S, TD / 8, o, late);
+      case 3: return launch_chain(combine_k_kernel<3>, grid, dim3(256), 0, stream, false, y, pos, S, TD / 8, o, late);
+      case 4: return launch_chain(combine_k_kernel<4>, grid, dim3(256), 0, stream, false, y, pos, S, TD / 8, o, late);
+      default: break;
+    }
+  }
+  return launch_chain(combine_kernel, grid, dim3(256), 0, stream, false, y, pos, S, k, TD / 8, o,
+                      late);
 }
 
 cudaError_t launch_fill_segments(const int32_t* counts, int n_segments, int mod, int32_t* out,
