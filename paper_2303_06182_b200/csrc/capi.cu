@@ -686,7 +686,10 @@ int moe::capi::layer_front(moe_layer* L, const void* X, int S, const int32_t* id
   L->counters_zeroed = true;
   // 3. gather token rows into expert-grouped order
   mark(2);
-  cudaError_t e = launch_gather_rows((const __nv_bfloat16*)X, L->order.p, rows, k, TD, L->xp.p, s);
+  cudaError_t e =
+      d.mode == MOE_GATING_DYNAMIC && gather_by_token(k)
+          ? launch_gather_tokens((const __nv_bfloat16*)X, L->pos.p, S, k, TD, L->xp.p, s)
+          : launch_gather_rows((const __nv_bfloat16*)X, L->order.p, rows, k, TD, L->xp.p, s);
   if (e != cudaSuccess) return cuda_fail(e, "gather launch");
   return MOE_OK;
 }

@@ -217,6 +217,10 @@ cudaError_t launch_gather_rows(const __nv_bfloat16* X, const int32_t* order, int
                                int TD, __nv_bfloat16* Xp, cudaStream_t stream);
 cudaError_t launch_combine(const __nv_bfloat16* Yw, const int32_t* pos, int S, int k, int TD,
                            __nv_bfloat16* out, cudaStream_t stream);
+// dynamic gating only (every slot has a row, no placeholders): X[t] -> Xp[pos[t*k+j]]
+cudaError_t launch_gather_tokens(const __nv_bfloat16* X, const int32_t* pos, int S, int k,
+                                 int TD, __nv_bfloat16* Xp, cudaStream_t stream);
+bool gather_by_token(int k);  // launch_gather_tokens applies (MOE_GATHER_TOKENS=0 disables)
 // row-major [rows, K] bf16 -> 128 x 64 tiles, 16 KB each, contiguous
 cudaError_t launch_pack_tiles(const __nv_bfloat16* src, __nv_bfloat16* dst, long rows, int K,
                               cudaStream_t stream);

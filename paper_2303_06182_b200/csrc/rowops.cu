@@ -220,6 +220,50 @@ __global__ void __launch_bounds__(256)
   if (late) pdl_trigger();
 }
 
+// Gather by token (dynamic gating: pos is a bijection slot -> row, no
+// placeholder rows): each X row is read once and stored to its k expert rows,
+// 4 loads and 4k stores in flight per lane -- X is read once instead of k
+// times (the row form relies on L2 for the repeats).
+template <int K>
+__global__ void __launch_bounds__(256)
+    gather_tokens_k_kernel(const uint4* __restrict__ X, const int32_t* __restrict__ pos, int S,
+                           int vec_per_row, uint4* __restrict__ Xp, int late) {
+  if (!late) pdl_trigger();
+  pdl_wait();
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp; t < S; t += nwarps) {
+    uint4* dst[K];
+    bool live[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int p = pos[static_cast<size_t>(t) * K + j];
+      live[j] = p >= 0;
+      dst[j] = Xp + static_cast<size_t>(live[j] ? p : 0) * vec_per_row;
+    }
+    const uint4* src = X + static_cast<size_t>(t) * vec_per_row;
+    int v = lane;
+    for (; v + 96 < vec_per_row; v += 128) {
+      uint4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = __ldg(src + v + 32 * u);
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (live[j]) dst[j][v + 32 * u] = x[u];
+    }
+    for (; v < vec_per_row; v += 32) {
+      const uint4 x = __ldg(src + v);
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (live[j]) dst[j][v] = x;
+    }
+  }
+  if (late) pdl_trigger();
+}
+
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
@@ -309,6 +353,30 @@ cudaError_t launch_gather_rows(const __nv_bfloat16* X, const int32_t* order, int
   return launch_chain(gather_rows_kernel, dim3(grid_for(rows, sm_count())), dim3(256), 0, stream,
                       false, reinterpret_cast<const uint4*>(X), order, rows, k, TD / 8,
                       reinterpret_cast<uint4*>(Xp), late_trigger("MOE_GATHER_LATE_TRIGGER", 0));
+}
+
+cudaError_t launch_gather_tokens(const __nv_bfloat16* X, const int32_t* pos, int S, int k,
+                                 int TD, __nv_bfloat16* Xp, cudaStream_t stream) {
+  if (S <= 0) return cudaSuccess;
+  const int late = late_trigger("MOE_GATHER_LATE_TRIGGER", 0);
+  const dim3 grid(grid_for(S, sm_count()));
+  const uint4* x = reinterpret_cast<const uint4*>(X);
+  uint4* xp = reinterpret_cast<uint4*>(Xp);
+  switch (k) {
+    case 1: return launch_chain(gather_tokens_k_kernel<1>, grid, dim3(256), 0, stream, false, x, pos, S, TD / 8, xp, late);
+    case 2: return launch_chain(gather_tokens_k_kernel<2>, grid, dim3(256), 0, stream, false, x, pos, S, TD / 8, xp, late);
+    case 3: return launch_chain(gather_tokens_k_kernel<3>, grid, dim3(256), 0, stream, false, x, pos, S, TD / 8, xp, late);
+    case 4: return launch_chain(gather_tokens_k_kernel<4>, grid, dim3(256), 0, stream, false, x, pos, S, TD / 8, xp, late);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+bool gather_by_token(int k) {
+  static const int env = [] {
+    const char* v = getenv("MOE_GATHER_TOKENS");
+    return v ? atoi(v) : 1;
+  }();
+  return env != 0 && k >= 1 && k <= 4;
 }
 
 cudaError_t launch_combine(const __nv_bfloat16* Yw, const int32_t* pos, int S, int k, int TD,
