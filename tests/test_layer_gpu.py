@@ -75,7 +75,11 @@ def _check_routing(layer, x, w, v, S, E, k):
 
 
 @pytest.mark.parametrize("S,TD,HD,E,k,tile_n", [(300, 256, 512, 8, 2, 0), (1000, 256, 384, 16, 1, 0),
-                                                (257, 128, 256, 33, 3, 256), (64, 512, 256, 512, 2, 0)])
+                                                (257, 128, 256, 33, 3, 256), (64, 512, 256, 512, 2, 0),
+                                                # k = 4 (per-k gather/combine), k = 6 (generic row
+                                                # forms), TD = 1152 (a 4-vector sweep plus a tail)
+                                                (333, 128, 256, 12, 4, 0), (200, 256, 256, 40, 6, 0),
+                                                (129, 1152, 256, 9, 4, 0)])
 def test_layer_small_all_stages(S, TD, HD, E, k, tile_n):
     layer, x, out, w, v = _run(S, TD, HD, E, k, tile_n=tile_n)
     idx, gw = _check_routing(layer, x, w, v, S, E, k)

@@ -21,6 +21,6 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > $out/bench_r
 MOE_BENCH_ONE_GPU_TEST=1 timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 10 --warmup 3 > $out/bench_ep2_onegpu.log 2>&1; echo "ep2 one-gpu rc=$?" >> $out/status.txt
 $NCU --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file $out/launches_lm.csv python tools/prof_step.py --steps 8 > /dev/null 2>&1; echo "ncu launches rc=$?" >> $out/status.txt
 $NCU --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file $out/launches_ep1.csv python tools/prof_step.py --steps 8 --ep > /dev/null 2>&1
-$NCU --set full --clock-control none --import-source on -k regex:"gate_topk|route_kernel|gather_rows|fused_ffn|combine_kernel" -s 5 -c 5 -o $out/full_lm python tools/prof_step.py --steps 3 > /dev/null 2>&1; echo "ncu full rc=$?" >> $out/status.txt
+$NCU --set full --clock-control none --import-source on -k regex:"gate_topk|route_kernel|gather|fused_ffn|combine" -s 5 -c 5 -o $out/full_lm python tools/prof_step.py --steps 3 > /dev/null 2>&1; echo "ncu full rc=$?" >> $out/status.txt
 $NCU --set full --clock-control none --import-source on -k regex:"ep_" -s 5 -c 5 -o $out/full_ep1 python tools/prof_step.py --steps 3 --ep > /dev/null 2>&1
 cat $out/status.txt
