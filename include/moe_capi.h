@@ -206,7 +206,7 @@ int moe_layer_forward_host(moe_layer* layer, const void* X_host, int S, void* ou
 
 /* End-to-end host path over a stream of n independent batches (a serving
  * queue): batch i's H2D copy, its forward (graph replay on `stream`) and its
- * D2H copy run on three streams with double-buffered device staging, so batch
+ * D2H copy run on three streams with triple-buffered device staging, so batch
  * i+1's upload and batch i-1's read-back overlap batch i's compute.  Every
  * byte of every batch crosses PCIe; synchronous (returns when all out_host[i]
  * are written).  Output of batch i is bitwise equal to

@@ -581,7 +581,7 @@ int moe_layer_destroy(moe_layer* L) {
   cudaSetDevice(L->ctx->device);
   L->drop_graphs();
   for (cudaEvent_t e : L->tev) cudaEventDestroy(e);
-  for (int b = 0; b < 2; ++b) {
+  for (int b = 0; b < moe_layer::kPipeBufs; ++b) {
     if (L->ev_in[b]) cudaEventDestroy(L->ev_in[b]);
     if (L->ev_comp[b]) cudaEventDestroy(L->ev_comp[b]);
     if (L->ev_out[b]) cudaEventDestroy(L->ev_out[b]);
@@ -939,12 +939,13 @@ int moe_layer_forward_host_batches(moe_layer* L, const void* const* X_host, cons
   cudaSetDevice(L->ctx->device);
   const size_t elems = (size_t)L->d.max_tokens * L->d.token_dim;
   int st;
-  for (int b = 0; b < 2; ++b)
+  constexpr int NB = moe_layer::kPipeBufs;
+  for (int b = 0; b < NB; ++b)
     if ((st = L->pin[b].reserve(elems)) || (st = L->pout[b].reserve(elems))) return st;
   if (!L->h2d) {
     MOE_CUDA(cudaStreamCreateWithFlags(&L->h2d, cudaStreamNonBlocking));
     MOE_CUDA(cudaStreamCreateWithFlags(&L->d2h, cudaStreamNonBlocking));
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NB; ++b) {
       MOE_CUDA(cudaEventCreateWithFlags(&L->ev_in[b], cudaEventDisableTiming));
       MOE_CUDA(cudaEventCreateWithFlags(&L->ev_comp[b], cudaEventDisableTiming));
       MOE_CUDA(cudaEventCreateWithFlags(&L->ev_out[b], cudaEventDisableTiming));
@@ -952,29 +953,55 @@ int moe_layer_forward_host_batches(moe_layer* L, const void* const* X_host, cons
   }
   cudaStream_t s = (cudaStream_t)stream;
   // the copy streams start after whatever the caller queued on `stream`
-  MOE_CUDA(cudaEventRecord(L->ev_comp[0], s));
+  for (int b = 0; b < NB; ++b) MOE_CUDA(cudaEventRecord(L->ev_comp[b], s));
   MOE_CUDA(cudaStreamWaitEvent(L->h2d, L->ev_comp[0], 0));
   MOE_CUDA(cudaStreamWaitEvent(L->d2h, L->ev_comp[0], 0));
-  MOE_CUDA(cudaEventRecord(L->ev_comp[1], s));
+  // experiments (MOE_HOST_PIPE_PROF=1): timing events around every copy and
+  // compute, a per-batch timeline printed for a few steady-state batches
+  static const bool prof = getenv("MOE_HOST_PIPE_PROF") != nullptr;
+  std::vector<cudaEvent_t> pev;
+  if (prof) {
+    pev.resize((size_t)n * 6);
+    for (cudaEvent_t& e : pev) cudaEventCreate(&e);
+  }
+  auto rec = [&](int i, int j, cudaStream_t st_) {
+    if (prof) cudaEventRecord(pev[(size_t)i * 6 + j], st_);
+  };
   for (int i = 0; i < n; ++i) {
-    const int b = i & 1;
+    const int b = i % NB;
     const size_t nb = (size_t)S[i] * L->d.token_dim * 2;
-    // batch i's input lands in pin[b] once batch i-2's compute has consumed it
+    // batch i's input lands in pin[b] once batch i-NB's compute has consumed it
+    // (three buffers: the upload of batch i overlaps the compute of i-1 and i-2)
     MOE_CUDA(cudaStreamWaitEvent(L->h2d, L->ev_comp[b], 0));
+    rec(i, 0, L->h2d);
     MOE_CUDA(cudaMemcpyAsync(L->pin[b].p, X_host[i], nb, cudaMemcpyHostToDevice, L->h2d));
+    rec(i, 1, L->h2d);
     MOE_CUDA(cudaEventRecord(L->ev_in[b], L->h2d));
-    // compute waits for its input and for batch i-2's read-back of pout[b]
+    // compute waits for its input and for batch i-NB's read-back of pout[b]
     MOE_CUDA(cudaStreamWaitEvent(s, L->ev_in[b], 0));
-    if (i >= 2) MOE_CUDA(cudaStreamWaitEvent(s, L->ev_out[b], 0));
+    if (i >= NB) MOE_CUDA(cudaStreamWaitEvent(s, L->ev_out[b], 0));
+    rec(i, 2, s);
     if ((st = moe_layer_forward_graph(L, L->pin[b].p, S[i], L->pout[b].p, s))) return st;
+    rec(i, 3, s);
     MOE_CUDA(cudaEventRecord(L->ev_comp[b], s));
     MOE_CUDA(cudaStreamWaitEvent(L->d2h, L->ev_comp[b], 0));
+    rec(i, 4, L->d2h);
     MOE_CUDA(cudaMemcpyAsync(out_host[i], L->pout[b].p, nb, cudaMemcpyDeviceToHost, L->d2h));
+    rec(i, 5, L->d2h);
     MOE_CUDA(cudaEventRecord(L->ev_out[b], L->d2h));
   }
   MOE_CUDA(cudaStreamSynchronize(L->h2d));
   MOE_CUDA(cudaStreamSynchronize(L->d2h));
   MOE_CUDA(cudaStreamSynchronize(s));
+  if (prof) {
+    for (int i = n / 2; i < std::min(n, n / 2 + 4); ++i) {
+      float t[6];
+      for (int j = 0; j < 6; ++j) cudaEventElapsedTime(&t[j], pev[0], pev[(size_t)i * 6 + j]);
+      fprintf(stderr, "[host pipe] batch %d: h2d %.1f-%.1f  compute %.1f-%.1f  d2h %.1f-%.1f us\n", i,
+              t[0] * 1e3, t[1] * 1e3, t[2] * 1e3, t[3] * 1e3, t[4] * 1e3, t[5] * 1e3);
+    }
+    for (cudaEvent_t e : pev) cudaEventDestroy(e);
+  }
   return moe_check_errors(L->ctx, s);
 }
 

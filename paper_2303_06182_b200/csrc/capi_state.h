@@ -222,7 +222,7 @@ struct moe_layer {
     cudaStream_t stream = nullptr;
     uint64_t used = 0;
   };
-  static constexpr int kGraphSlots = 4;
+  static constexpr int kGraphSlots = 6;
   GraphEntry graphs[kGraphSlots];
   uint64_t graph_clock = 0;
   void drop_graphs() {
@@ -232,9 +232,10 @@ struct moe_layer {
     }
   }
   // pipelined host forward: double-buffered device staging + two copy streams
-  DevBuf<__nv_bfloat16> pin[2], pout[2];
+  static constexpr int kPipeBufs = 3;  // moe_layer_forward_host_batches ring depth
+  DevBuf<__nv_bfloat16> pin[kPipeBufs], pout[kPipeBufs];
   cudaStream_t h2d = nullptr, d2h = nullptr;
-  cudaEvent_t ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};
+  cudaEvent_t ev_in[kPipeBufs] = {}, ev_comp[kPipeBufs] = {}, ev_out[kPipeBufs] = {};
 };
 
 struct moe_ffn {

@@ -16,7 +16,7 @@ try:
     st = d.get("stage_ms", {})
     print(f"{os.path.basename(sys.argv[1]):36s} step {d['ms_per_step']:.4f} ms  ffn {st.get('ffn_gemm1', 0) + st.get('ffn_gemm2', 0):.4f} ms  "
           f"gate {st.get('gate_topk', 0)*1e3:.1f} route {st.get('route', 0)*1e3:.1f} gather {st.get('gather', 0)*1e3:.1f} "
-          f"combine {st.get('combine', 0)*1e3:.1f} us", flush=True)
+          f"combine {st.get('combine', 0)*1e3:.1f} us  e2e {d['e2e']['ms_per_step']:.4f} ms", flush=True)
 except Exception as e:
     print(sys.argv[1], "failed:", e, open("gpurun_out/ab.err").read()[-500:])
 PY
