@@ -662,7 +662,8 @@ def run_b200(args):
     e1.record(stream)
     e1.synchronize()
     wall_ms = (time.perf_counter() - t0) * 1e3 / Ke
-    e2e_ms = max_over_ranks(max(e0.elapsed_time(e1) / Ke, wall_ms), world)
+    e2e_dev_ms = e0.elapsed_time(e1) / Ke
+    e2e_ms = max_over_ranks(max(e2e_dev_ms, wall_ms), world)
     if not torch.equal(ring_o[0], oh):
         raise RuntimeError("pipelined host path differs from moe_layer_forward_host")
 
@@ -730,6 +731,7 @@ def run_b200(args):
                 "api": ("moe_layer_forward_host_batches (C ABI): %d batches from pinned host buffers, "
                         "upload/compute/read-back pipelined over 3 streams; time = max(device events, "
                         "host wall clock)" % Ke),
+                "device_ms_per_step": e2e_dev_ms, "wall_ms_per_step": wall_ms,
                 "per_call_sync": {"value": world * S / (e2e_sync_ms * 1e-3), "ms_per_step": e2e_sync_ms,
                                   "api": "moe_layer_forward_host (one synchronous call per batch)"}},
         "cpu_baseline": cpu,

@@ -353,6 +353,7 @@ __global__ void __launch_bounds__(256, 1)
     const int q = warp & 3;
     const int tid = threadIdx.x - 128;
     __nv_bfloat16* stg = sEpi + q * 32 * 32;
+    const uint64_t pol_keep = ptx::policy_evict_last();
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x < t_dyn ? blockIdx.x : take(true); t >= 0;
@@ -388,7 +389,11 @@ __global__ void __launch_bounds__(256, 1)
             const uint4 v = *reinterpret_cast<const uint4*>(stg + tok * 32 + ch * 8);
             int row = it.row0 + c0 + tok;
             if (tr.gemm && g.out_rows) row = g.out_rows[row];
-            *reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * m_total + col0 + ch * 8) = v;
+            __nv_bfloat16* dst = out + static_cast<size_t>(row) * m_total + col0 + ch * 8;
+            if (tr.gemm && g.yw_keep)
+              ptx::st_global_hint(dst, v, pol_keep);
+            else
+              *reinterpret_cast<uint4*>(dst) = v;
           }
         }
         __syncwarp();
@@ -526,8 +531,13 @@ cudaError_t launch_fused_ffn(const CUtensorMap& tmW1, const RowMaps& xp, const C
     const char* v = getenv("MOE_FFN_DYN_TAIL");  // tiles claimed dynamically; 0 = lag * MT2, <0 = off
     return v ? atoi(v) : 0;
   }();
+  static const int yw_keep = [] {
+    const char* v = getenv("MOE_FFN_YW_KEEP");
+    return v ? atoi(v) : 0;
+  }();
   FusedFfnArgs args = args_in;
   args.full_fence = full_fence;
+  args.yw_keep = yw_keep;
   args.dyn_tail = dyn_tail;
   if (dyn_tail < 0) args.tile_ctr = nullptr;
   args.late_trigger = late;

@@ -364,6 +364,7 @@ __global__ void __launch_bounds__(256, 1)
     const int q = warp & 3;
     const int tid = threadIdx.x - 128;
     __nv_bfloat16* stg = sEpi + q * 32 * 32;
+    const uint64_t pol_keep = ptx::policy_evict_last();
     const uint32_t tempty_l[2] = {leader_addr(&tempty[0]), leader_addr(&tempty[1])};
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -401,7 +402,11 @@ __global__ void __launch_bounds__(256, 1)
             const uint4 v = *reinterpret_cast<const uint4*>(stg + tok * 32 + ch * 8);
             int row = it.row0 + c0 + tok;
             if (tr.gemm && g.out_rows) row = g.out_rows[row];
-            *reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * m_total + col0 + ch * 8) = v;
+            __nv_bfloat16* dst = out + static_cast<size_t>(row) * m_total + col0 + ch * 8;
+            if (tr.gemm && g.yw_keep)
+              ptx::st_global_hint(dst, v, pol_keep);
+            else
+              *reinterpret_cast<uint4*>(dst) = v;
           }
         }
         __syncwarp();

@@ -43,6 +43,12 @@ constexpr int kBlockK = 32;
 constexpr int kABytes = kBlockM * kBlockK * 2;
 constexpr int kMaxK = 8;
 constexpr int kMaxSmem = 220 * 1024;
+// more stages (16) measured equal at MT and cfg1 (same box): the gate is not
+// bound by loads in flight
+#ifndef MOE_GATE_MAX_STAGES
+#define MOE_GATE_MAX_STAGES 8
+#endif
+constexpr int kMaxStages = MOE_GATE_MAX_STAGES;
 
 struct GateLayout {
   int e_pad;      // E rounded up to 16
@@ -68,7 +74,7 @@ __host__ __device__ inline GateLayout gate_layout(int E) {
   L.box_rows = L.b_rows / L.n_box;  // multiple of 8: every box starts on a swizzle atom
   const int stage = kABytes + L.b_rows * kBlockK * 2;
   int s = (kMaxSmem - 2048) / stage;
-  L.stages = s > 8 ? 8 : s;
+  L.stages = s > kMaxStages ? kMaxStages : s;
   L.smem = 1024 + L.stages * stage + (2 * L.stages + 2) * 8 + 16;
   return L;
 }

@@ -157,6 +157,7 @@ struct FusedFfnArgs {
   const int32_t* arrived_expect;
   int32_t* arrive_err;
   unsigned long long arrive_timeout_ns;
+  int yw_keep;               // GEMM2 stores Yw with an L2 evict_last hint (read next by the combine)
   // combine in the GEMM2 epilogue (combine_epi.cuh); comb_out null = off
   int top_k;
   const int32_t* comb_order;  // row -> slot (token * k + j)

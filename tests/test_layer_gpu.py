@@ -225,7 +225,7 @@ def test_graph_and_host_paths_bitwise_equal_to_eager(S, TD, HD, E, k):
 @pytest.mark.parametrize("S,TD,HD,E,k", [(1024, 256, 512, 16, 2), (16384, 1024, 4096, 512, 2)])
 def test_pipelined_host_batches_bitwise_equal_per_call(S, TD, HD, E, k):
     """moe_layer_forward_host_batches: every batch of the queue (different
-    tokens, different sizes, double-buffered staging reused) equals its own
+    tokens, different sizes, triple-buffered staging reused) equals its own
     synchronous moe_layer_forward_host call."""
     shape = LayerShape(TD, HD, E, k)
     layer = MoeLayer(shape, S, weights=make_weights(shape, seed=SEED))
