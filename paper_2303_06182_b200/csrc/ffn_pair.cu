@@ -58,6 +58,12 @@ struct TileRef {
   int mp;  // 256-row weight block (pair of 128-row blocks)
 };
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ TileRef decode_tile(int t, int n, int L, int P1, int P2) {
   const int head = L * P1;
   if (t < head) return {t / P1, 0, t % P1};
@@ -218,6 +224,7 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem_base = *tmem_slot;
   if (!g.late_trigger) pdl_trigger();
   pdl_wait();
+  if (g.prof && threadIdx.x == 0) g.prof[2 * blockIdx.x] = globaltimer_ns();
 
   const int item0 = g.item_off ? g.item_off[g.e_lo] : 0;
   const int n = g.item_off ? g.item_off[g.e_hi] - item0 : *g.n_items;
@@ -443,6 +450,7 @@ __global__ void __launch_bounds__(256, 1)
     }
   }
 
+  if (g.prof && threadIdx.x == 128) g.prof[2 * blockIdx.x + 1] = globaltimer_ns();
   // the peer's last arrivals on the leader's barriers and the leader's last
   // commits into the peer must land before either CTA leaves
   ptx::tc_fence_before();
