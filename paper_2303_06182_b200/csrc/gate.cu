@@ -22,10 +22,12 @@
 #include <float.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
 #include <utility>
+#include <vector>
 
 #include "moe_internal.h"
 #include "ptx.cuh"
@@ -83,6 +85,12 @@ __host__ __device__ inline GateLayout gate_layout(int E) {
 // candidate's id is larger than every id already in the list, so on equal
 // values it stays behind; once placed, every later entry shifts down.
 // Branch-free (selects only) so the 32 lanes never diverge.
+__device__ __forceinline__ unsigned long long gate_clock() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <int K>
 __device__ __forceinline__ void topk_insert(float (&bv)[K], int (&bi)[K], float v, int e) {
   bool carry = false;
@@ -112,6 +120,7 @@ __device__ __forceinline__ void gate_epilogue(const GateArgs& a, uint32_t tmem_b
   const int lane = threadIdx.x & 31;
   ptx::mbar_wait(tfull, 0);
   ptx::tc_fence_after();
+  if (a.prof && threadIdx.x == 0) a.prof[3 * blockIdx.x + 1] = gate_clock();
   const int q = warp & 3;
   const int half = warp >> 2;
   const int tl = q * 32 + lane;  // token within the tile
@@ -127,6 +136,10 @@ __device__ __forceinline__ void gate_epilogue(const GateArgs& a, uint32_t tmem_b
     bv[j] = -INFINITY;
     bi[j] = 0x7fffffff;
   }
+  // K = 2: a second list for the odd columns (two independent compare /
+  // select chains instead of one vote-guarded insert per value)
+  float ov0 = -INFINITY, ov1 = -INFINITY;
+  int oi0 = 0x7fffffff, oi1 = 0x7fffffff;
   for (int c0 = c_begin; c0 < c_end; c0 += 32) {
     uint32_t r[32];
     ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + c0, r);
@@ -145,14 +158,47 @@ __device__ __forceinline__ void gate_epilogue(const GateArgs& a, uint32_t tmem_b
           if (c0 + i < a.E) dst[i] = __uint_as_float(r[i]);
       }
     }
+    if constexpr (K == 2) {
+      // strict > within a list: ids ascend, so ties keep the lower id
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const float v = (c0 + i < a.E) ? __uint_as_float(r[i]) : -INFINITY;
-      if (K == 1) {
-        topk_insert<K>(bv, bi, v, c0 + i);
-      } else if (__any_sync(0xffffffffu, v > bv[K - 1])) {
-        topk_insert<K>(bv, bi, v, c0 + i);
+      for (int i = 0; i < 32; i += 2) {
+        const float v = (c0 + i < a.E) ? __uint_as_float(r[i]) : -INFINITY;
+        const float w = (c0 + i + 1 < a.E) ? __uint_as_float(r[i + 1]) : -INFINITY;
+        const bool t0 = v > bv[0], t1 = v > bv[1];
+        bv[1] = t0 ? bv[0] : (t1 ? v : bv[1]);
+        bi[1] = t0 ? bi[0] : (t1 ? c0 + i : bi[1]);
+        bv[0] = t0 ? v : bv[0];
+        bi[0] = t0 ? c0 + i : bi[0];
+        const bool u0 = w > ov0, u1 = w > ov1;
+        ov1 = u0 ? ov0 : (u1 ? w : ov1);
+        oi1 = u0 ? oi0 : (u1 ? c0 + i + 1 : oi1);
+        ov0 = u0 ? w : ov0;
+        oi0 = u0 ? c0 + i + 1 : oi0;
       }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float v = (c0 + i < a.E) ? __uint_as_float(r[i]) : -INFINITY;
+        if (K == 1) {
+          topk_insert<K>(bv, bi, v, c0 + i);
+        } else if (__any_sync(0xffffffffu, v > bv[K - 1])) {
+          topk_insert<K>(bv, bi, v, c0 + i);
+        }
+      }
+    }
+  }
+  if constexpr (K == 2) {
+    // merge the odd-column list: order by (value desc, id asc)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float v = j ? ov1 : ov0;
+      const int e = j ? oi1 : oi0;
+      const bool t0 = v > bv[0] || (v == bv[0] && e < bi[0]);
+      const bool t1 = v > bv[1] || (v == bv[1] && e < bi[1]);
+      bv[1] = t0 ? bv[0] : (t1 ? v : bv[1]);
+      bi[1] = t0 ? bi[0] : (t1 ? e : bi[1]);
+      bv[0] = t0 ? v : bv[0];
+      bi[0] = t0 ? e : bi[0];
     }
   }
   ptx::tc_fence_before();
@@ -208,6 +254,7 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
                                           const GateArgs& a, uint8_t* smem, int* s_e,
                                           float* s_w) {
   static_assert(C == 1 || C == 2 || C == 4, "cluster of 1, 2 or 4 CTAs");
+  if (a.prof && threadIdx.x == 0) a.prof[3 * blockIdx.x] = gate_clock();
   const GateLayout L = gate_layout(a.E);
   const int stage_bytes = kABytes + L.b_rows * kBlockK * 2;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.stages * stage_bytes);
@@ -317,6 +364,7 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
   gate_epilogue<K>(a, tmem_base, tfull, tok0, smem, s_e, s_w);
 
   __syncthreads();
+  if (a.prof && threadIdx.x == 0) a.prof[3 * blockIdx.x + 2] = gate_clock();
   ptx::tc_fence_after();
   if (warp == 2) {
     if (L.e_pad <= 32) ptx::tmem_dealloc<32>(tmem_base);
@@ -849,10 +897,34 @@ cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const G
     if (it == cache.end()) it = cache.emplace(std::make_pair(L.e_pad, tiles), gate_cluster(L, tiles, L.smem)).first;
     C = it->second;
   }
-  if (a.k == 1) return launch_gate_k<1>(tmX, tmWg, a, C, tiles, L.smem, stream);
-  if (a.k == 2) return launch_gate_k<2>(tmX, tmWg, a, C, tiles, L.smem, stream);
-  if (a.k <= 4) return launch_gate_k<4>(tmX, tmWg, a, C, tiles, L.smem, stream);
-  return launch_gate_k<8>(tmX, tmWg, a, C, tiles, L.smem, stream);
+  static const bool prof = getenv("MOE_GATE_PROF") != nullptr;
+  GateArgs b = a;
+  static unsigned long long* prof_buf = nullptr;
+  if (prof) {
+    if (!prof_buf) cudaMalloc(&prof_buf, 3 * 4096 * sizeof(unsigned long long));
+    b.prof = prof_buf;
+  }
+  cudaError_t e;
+  if (a.k == 1) e = launch_gate_k<1>(tmX, tmWg, b, C, tiles, L.smem, stream);
+  else if (a.k == 2) e = launch_gate_k<2>(tmX, tmWg, b, C, tiles, L.smem, stream);
+  else if (a.k <= 4) e = launch_gate_k<4>(tmX, tmWg, b, C, tiles, L.smem, stream);
+  else e = launch_gate_k<8>(tmX, tmWg, b, C, tiles, L.smem, stream);
+  if (!prof || e != cudaSuccess || tiles > 4096) return e;
+  // experiments only: per-CTA mainloop / epilogue split of this launch
+  std::vector<unsigned long long> h(3 * (size_t)tiles);
+  cudaStreamSynchronize(stream);
+  cudaMemcpy(h.data(), prof_buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  unsigned long long t0 = ~0ull, t2 = 0;
+  double m = 0, ep = 0;
+  for (int i = 0; i < tiles; ++i) {
+    t0 = std::min(t0, h[3 * i]);
+    t2 = std::max(t2, h[3 * i + 2]);
+    m += (double)(h[3 * i + 1] - h[3 * i]);
+    ep += (double)(h[3 * i + 2] - h[3 * i + 1]);
+  }
+  fprintf(stderr, "[gate prof] %d CTAs (cluster %d): mean mainloop %.1f us, mean epilogue %.1f us, span %.1f us\n",
+          tiles, C, m / tiles * 1e-3, ep / tiles * 1e-3, (t2 - t0) * 1e-3);
+  return e;
 }
 
 }  // namespace moe

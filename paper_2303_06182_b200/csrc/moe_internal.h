@@ -190,6 +190,7 @@ struct GateArgs {
   int32_t* idx;     // [S*k]
   float* w;         // [S*k]
   float* logits;    // optional [S*E]
+  unsigned long long* prof = nullptr;  // experiments (MOE_GATE_PROF): per-CTA phase times
 };
 // Gate + dynamic dispatch + gather in one cooperative launch (gate.cu).
 struct DispatchArgs {
