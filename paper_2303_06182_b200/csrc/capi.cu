@@ -385,9 +385,9 @@ int moe_gate_topk(moe_ctx* ctx, const void* X, const void* Wg, int S, int TD, in
   cudaError_t e = gate_prepare(E);
   if (e != cudaSuccess) return cuda_fail(e, "gate_prepare");
   CUtensorMap tmX, tmWg;
-  st = encode_bf16(&tmX, X, S, TD, 128, moe::gate_box_cols());
+  st = encode_bf16(&tmX, X, S, TD, 128, moe::gate_box_cols(E));
   if (st) return st;
-  st = encode_bf16(&tmWg, Wg, E, TD, gate_box_rows(E), moe::gate_box_cols());
+  st = encode_bf16(&tmWg, Wg, E, TD, gate_box_rows(E), moe::gate_box_cols(E));
   if (st) return st;
   GateArgs a{S, TD, E, k, idx, w, logits};
   e = launch_gate(tmX, tmWg, a, (cudaStream_t)stream);
@@ -514,7 +514,7 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
   cudaMemset(L->xp.p, 0, Rp * TD * 2);
   cudaMemset(L->comb_cnt.p, 0, sizeof(int32_t) * (size_t)S * (d.token_dim / 128));
   cudaMemset(L->h.p, 0, Rp * HD * 2);
-  if ((st = encode_bf16(&L->tmWg, Wg, E, TD, moe::gate_box_rows(E), moe::gate_box_cols())) ||
+  if ((st = encode_bf16(&L->tmWg, Wg, E, TD, moe::gate_box_rows(E), moe::gate_box_cols(E, d.fuse_front))) ||
       (st = encode_bf16(&L->tmW1, W1, (uint64_t)E * HD, TD, 128)) ||
       (st = encode_bf16(&L->tmW2, W2, (uint64_t)E * TD, HD, 128)) ||
       (st = encode_bf16(&L->tmXp, L->xp.p, Rp, TD, 16)) ||
@@ -636,7 +636,9 @@ int moe::capi::layer_front(moe_layer* L, const void* X, int S, const int32_t* id
   // 1. gate
   mark(0);
   if (X != L->tmX_ptr || S != L->tmX_rows) {
-    if ((st = encode_bf16(&L->tmX, X, (uint64_t)S, TD, 128, moe::gate_box_cols()))) return st;
+    if ((st = encode_bf16(&L->tmX, X, (uint64_t)S, TD, 128,
+                          moe::gate_box_cols(L->d.num_experts, L->d.fuse_front))))
+      return st;
     L->tmX_ptr = X;
     L->tmX_rows = S;
   }

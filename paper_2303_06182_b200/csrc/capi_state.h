@@ -18,7 +18,9 @@
 
 namespace moe {
 int gate_box_rows(int E);
-int gate_box_cols();  // inner (K) extent of the gate's X / Wg TMA boxes
+// inner (K) extent of the gate's X / Wg TMA boxes (64 or 32; 32 for the
+// cooperative gate + dispatch kernel)
+int gate_box_cols(int E, bool fused_front = false);
 
 namespace capi {
 

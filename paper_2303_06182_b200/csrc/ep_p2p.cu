@@ -572,7 +572,7 @@ int moe_ep_create(moe_ctx* ctx, const moe_ep_desc* desc, const void* Wg, const v
   MOE_CUDA(cudaMemset(P->err.p, 0, 2 * sizeof(int32_t)));
   MOE_CUDA(cudaMemset(P->h.p, 0, (R + 256) * HD * 2));
   char* rx = P->window + P->lay.recv_x;
-  if ((st = encode_bf16(&P->tmWg, Wg, E, TD, moe::gate_box_rows(E), moe::gate_box_cols())) ||
+  if ((st = encode_bf16(&P->tmWg, Wg, E, TD, moe::gate_box_rows(E), moe::gate_box_cols(E))) ||
       (st = encode_bf16(&P->tmW1p, P->w1p.p, n1 / 64, 64, 128)) ||
       (st = encode_bf16(&P->tmW2p, P->w2p.p, n1 / 64, 64, 128)) ||
       (st = encode_rows(&P->xpm, rx, R + 256, TD)) || (st = encode_rows(&P->hm, P->h.p, R + 256, HD)))
@@ -669,7 +669,7 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   const int k = d.top_k, E = d.num_experts, TD = d.token_dim, HD = d.hidden_dim, D = d.world_size;
   int st;
   if (X != P->tmX_ptr || S != P->tmX_rows) {
-    if ((st = encode_bf16(&P->tmX, X, (uint64_t)S, TD, 128, moe::gate_box_cols()))) return st;
+    if ((st = encode_bf16(&P->tmX, X, (uint64_t)S, TD, 128, moe::gate_box_cols(P->d.num_experts)))) return st;
     P->tmX_ptr = X;
     P->tmX_rows = S;
   }

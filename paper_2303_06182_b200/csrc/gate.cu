@@ -63,7 +63,7 @@ struct GateLayout {
 
 // Wg k-block slab = n_box boxes; a cluster of C CTAs (C | n_box) splits the
 // boxes between its CTAs and multicasts each to all of them.
-__host__ __device__ inline GateLayout gate_layout(int E) {
+__host__ __device__ inline GateLayout gate_layout(int E, int bk = kBlockK) {
   GateLayout L;
   L.e_pad = (E + 15) & ~15;
   if (L.e_pad >= 128) {
@@ -74,7 +74,7 @@ __host__ __device__ inline GateLayout gate_layout(int E) {
     L.n_box = 1;
   }
   L.box_rows = L.b_rows / L.n_box;  // multiple of 8: every box starts on a swizzle atom
-  const int stage = kABytes + L.b_rows * kBlockK * 2;
+  const int stage = kBlockM * bk * 2 + L.b_rows * bk * 2;
   int s = (kMaxSmem - 2048) / stage;
   L.stages = s > kMaxStages ? kMaxStages : s;
   L.smem = 1024 + L.stages * stage + (2 * L.stages + 2) * 8 + 16;
@@ -249,14 +249,16 @@ __device__ __forceinline__ void gate_epilogue(const GateArgs& a, uint32_t tmem_b
 // 8 warps, idx / w written to global; with s_e/s_w the tile's routing is also
 // left in shared memory (slot t*k+j of the tile) for a fused dispatch.
 // Ends with a block barrier and the TMEM released.
-template <int K, int C = 1>
+template <int K, int C = 1, int BK = kBlockK>
 __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensorMap& tmWg,
                                           const GateArgs& a, uint8_t* smem, int* s_e,
                                           float* s_w) {
   static_assert(C == 1 || C == 2 || C == 4, "cluster of 1, 2 or 4 CTAs");
+  static_assert(BK == 32 || BK == 64, "32-deep (64-byte swizzle) or 64-deep (128-byte) k-blocks");
+  constexpr int kABytes = kBlockM * BK * 2;
   if (a.prof && threadIdx.x == 0) a.prof[3 * blockIdx.x] = gate_clock();
-  const GateLayout L = gate_layout(a.E);
-  const int stage_bytes = kABytes + L.b_rows * kBlockK * 2;
+  const GateLayout L = gate_layout(a.E, BK);
+  const int stage_bytes = kABytes + L.b_rows * BK * 2;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.stages * stage_bytes);
   uint64_t* empty = full + L.stages;
   uint64_t* tfull = empty + L.stages;
@@ -265,7 +267,10 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int tok0 = blockIdx.x * kBlockM;
-  const int KB = a.TD / kBlockK;
+  const int KB = a.TD / BK;
+  auto desc = [](uint32_t addr) {
+    return BK == 64 ? ptx::umma_desc_sw128(addr) : ptx::umma_desc_sw64(addr);
+  };
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmX);
@@ -307,15 +312,14 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         ptx::mbar_arrive_expect_tx(&full[stage], stage_bytes);
         uint8_t* st = smem + stage * stage_bytes;
-        ptx::tma_load_2d(st, &tmX, &full[stage], kb * kBlockK, tok0, pol_x);
+        ptx::tma_load_2d(st, &tmX, &full[stage], kb * BK, tok0, pol_x);
         for (int b = b_lo; b < b_lo + per; ++b) {
           const int r = b * L.box_rows;
           if (C > 1)
-            ptx::tma_load_2d_mc(st + kABytes + r * kBlockK * 2, &tmWg, &full[stage], kb * kBlockK,
-                                r, static_cast<uint16_t>((1u << C) - 1), pol_w);
+            ptx::tma_load_2d_mc(st + kABytes + r * BK * 2, &tmWg, &full[stage], kb * BK, r,
+                                static_cast<uint16_t>((1u << C) - 1), pol_w);
           else
-            ptx::tma_load_2d(st + kABytes + r * kBlockK * 2, &tmWg, &full[stage], kb * kBlockK, r,
-                             pol_w);
+            ptx::tma_load_2d(st + kABytes + r * BK * 2, &tmWg, &full[stage], kb * BK, r, pol_w);
         }
         if (++stage == L.stages) {
           stage = 0;
@@ -339,13 +343,12 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
         const uint32_t a0 = ptx::smem_u32(smem + stage * stage_bytes);
         const uint32_t b0 = a0 + kABytes;
 #pragma unroll
-        for (int kk = 0; kk < kBlockK / 16; ++kk) {
+        for (int kk = 0; kk < BK / 16; ++kk) {
           const uint32_t acc = (kb | kk) != 0 ? 1u : 0u;
-          ptx::mma_bf16(tmem_base, ptx::umma_desc_sw64(a0 + kk * 32),
-                        ptx::umma_desc_sw64(b0 + kk * 32), id0, acc);
+          ptx::mma_bf16(tmem_base, desc(a0 + kk * 32), desc(b0 + kk * 32), id0, acc);
           if (n1 > 0)
-            ptx::mma_bf16(tmem_base + 256, ptx::umma_desc_sw64(a0 + kk * 32),
-                          ptx::umma_desc_sw64(b0 + 256 * kBlockK * 2 + kk * 32), id1, acc);
+            ptx::mma_bf16(tmem_base + 256, desc(a0 + kk * 32), desc(b0 + 256 * BK * 2 + kk * 32), id1,
+                          acc);
         }
         if (C > 1)
           ptx::mma_commit_mc(&empty[stage], static_cast<uint16_t>((1u << C) - 1));
@@ -511,11 +514,11 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
-template <int K, int C>
+template <int K, int C, int BK = kBlockK>
 __global__ void __launch_bounds__(256, 1)
     gate_topk_kernel(const __grid_constant__ CUtensorMap tmX,
                      const __grid_constant__ CUtensorMap tmWg, GateArgs a) {
-  gate_tile<K, C>(tmX, tmWg, a, aligned_smem(), nullptr, nullptr);
+  gate_tile<K, C, BK>(tmX, tmWg, a, aligned_smem(), nullptr, nullptr);
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -731,14 +734,26 @@ __global__ void __launch_bounds__(256, 1)
 }  // namespace
 
 int gate_box_rows(int E) { return gate_layout(E).box_rows; }
-int gate_box_cols() { return kBlockK; }
+// 64-deep k-blocks with 128-byte rows for E <= 128 (a 32 KB stage at E = 128,
+// six stages): 32-deep boxes of 64-byte rows streamed X at ~35-65 GB/s per SM
+// (MOE_GATE_PROF); the cooperative gate + dispatch and the CTA-pair gate keep
+// 32.  MOE_GATE_WIDE=0 restores 32 everywhere.
+bool gate_pair_enabled(int E);
+bool gate_wide(int E) {
+  static const int env = [] {
+    const char* v = getenv("MOE_GATE_WIDE");
+    return v ? atoi(v) : 1;
+  }();
+  return env != 0 && gate_layout(E).e_pad <= 128 && !gate_pair_enabled(E);
+}
+int gate_box_cols(int E, bool fused_front) { return !fused_front && gate_wide(E) ? 64 : kBlockK; }
 
-template <int C>
+template <int C, int BK = kBlockK>
 const void* gate_fn(int k) {
-  return k == 1   ? reinterpret_cast<const void*>(gate_topk_kernel<1, C>)
-         : k == 2 ? reinterpret_cast<const void*>(gate_topk_kernel<2, C>)
-         : k <= 4 ? reinterpret_cast<const void*>(gate_topk_kernel<4, C>)
-                  : reinterpret_cast<const void*>(gate_topk_kernel<8, C>);
+  return k == 1   ? reinterpret_cast<const void*>(gate_topk_kernel<1, C, BK>)
+         : k == 2 ? reinterpret_cast<const void*>(gate_topk_kernel<2, C, BK>)
+         : k <= 4 ? reinterpret_cast<const void*>(gate_topk_kernel<4, C, BK>)
+                  : reinterpret_cast<const void*>(gate_topk_kernel<8, C, BK>);
 }
 
 cudaError_t gate_prepare(int E) {
@@ -756,9 +771,15 @@ cudaError_t gate_prepare(int E) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem);
     if (e != cudaSuccess) return e;
   }
+  const int wsmem = gate_layout(E, 64).smem;
   for (int k : {1, 2, 4, 8}) {
     for (const void* fn : {gate_fn<1>(k), gate_fn<2>(k), gate_fn<4>(k)}) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem);
+      if (e != cudaSuccess) return e;
+    }
+    for (const void* fn : {gate_fn<1, 64>(k), gate_fn<2, 64>(k), gate_fn<4, 64>(k)}) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           std::max(wsmem, L.smem));
       if (e != cudaSuccess) return e;
     }
   }
@@ -780,7 +801,7 @@ cudaError_t gate_prepare(int E) {
 
 // Cluster size for the gate: the largest C | n_box (<= MOE_GATE_CLUSTER, default
 // 4) for which every cluster of the grid is co-resident (one wave).
-int gate_cluster(const GateLayout& L, int tiles, int smem) {
+int gate_cluster(const GateLayout& L, int tiles, int smem, bool wide = false) {
   static int env = -1;
   if (env < 0) {
     const char* v = getenv("MOE_GATE_CLUSTER");
@@ -800,7 +821,8 @@ int gate_cluster(const GateLayout& L, int tiles, int smem) {
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     int n = 0;
-    const void* fn = C == 4 ? gate_fn<4>(2) : gate_fn<2>(2);
+    const void* fn = wide ? (C == 4 ? gate_fn<4, 64>(2) : gate_fn<2, 64>(2))
+                          : (C == 4 ? gate_fn<4>(2) : gate_fn<2>(2));
     if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) {
       cudaGetLastError();
       continue;
@@ -810,7 +832,7 @@ int gate_cluster(const GateLayout& L, int tiles, int smem) {
   return 1;
 }
 
-template <int K>
+template <int K, int BK = kBlockK>
 cudaError_t launch_gate_k(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateArgs& a,
                           int C, int tiles, int smem, cudaStream_t stream) {
   cudaLaunchConfig_t cfg = {};
@@ -832,9 +854,9 @@ cudaError_t launch_gate_k(const CUtensorMap& tmX, const CUtensorMap& tmWg, const
   }
   cfg.attrs = attr;
   cfg.numAttrs = n;
-  if (C == 4) return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 4>, tmX, tmWg, a);
-  if (C == 2) return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 2>, tmX, tmWg, a);
-  return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 1>, tmX, tmWg, a);
+  if (C == 4) return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 4, BK>, tmX, tmWg, a);
+  if (C == 2) return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 2, BK>, tmX, tmWg, a);
+  return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 1, BK>, tmX, tmWg, a);
 }
 
 template <int K>
@@ -877,9 +899,10 @@ bool gate_pair_enabled(int E) {
 
 cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateArgs& a,
                         cudaStream_t stream) {
-  if (a.k < 1 || a.k > kMaxK || a.E > 512 || a.E < a.k || (a.TD % kBlockK) != 0)
+  const bool wide = gate_wide(a.E);
+  if (a.k < 1 || a.k > kMaxK || a.E > 512 || a.E < a.k || (a.TD % (wide ? 64 : kBlockK)) != 0)
     return cudaErrorInvalidValue;
-  const GateLayout L = gate_layout(a.E);
+  const GateLayout L = gate_layout(a.E, wide ? 64 : kBlockK);
   const int tiles = (a.S + kBlockM - 1) / kBlockM;
   if (gate_pair_enabled(a.E)) {
     if (a.k == 1) return launch_gate_pair_k<1>(tmX, tmWg, a, tiles, stream);
@@ -894,7 +917,7 @@ cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const G
   {
     std::lock_guard<std::mutex> lock(mu);
     auto it = cache.find({L.e_pad, tiles});
-    if (it == cache.end()) it = cache.emplace(std::make_pair(L.e_pad, tiles), gate_cluster(L, tiles, L.smem)).first;
+    if (it == cache.end()) it = cache.emplace(std::make_pair(L.e_pad, tiles), gate_cluster(L, tiles, L.smem, wide)).first;
     C = it->second;
   }
   static const bool prof = getenv("MOE_GATE_PROF") != nullptr;
@@ -905,7 +928,12 @@ cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const G
     b.prof = prof_buf;
   }
   cudaError_t e;
-  if (a.k == 1) e = launch_gate_k<1>(tmX, tmWg, b, C, tiles, L.smem, stream);
+  if (wide) {
+    if (a.k == 1) e = launch_gate_k<1, 64>(tmX, tmWg, b, C, tiles, L.smem, stream);
+    else if (a.k == 2) e = launch_gate_k<2, 64>(tmX, tmWg, b, C, tiles, L.smem, stream);
+    else if (a.k <= 4) e = launch_gate_k<4, 64>(tmX, tmWg, b, C, tiles, L.smem, stream);
+    else e = launch_gate_k<8, 64>(tmX, tmWg, b, C, tiles, L.smem, stream);
+  } else if (a.k == 1) e = launch_gate_k<1>(tmX, tmWg, b, C, tiles, L.smem, stream);
   else if (a.k == 2) e = launch_gate_k<2>(tmX, tmWg, b, C, tiles, L.smem, stream);
   else if (a.k <= 4) e = launch_gate_k<4>(tmX, tmWg, b, C, tiles, L.smem, stream);
   else e = launch_gate_k<8>(tmX, tmWg, b, C, tiles, L.smem, stream);
