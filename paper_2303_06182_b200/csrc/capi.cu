@@ -512,6 +512,10 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
     return st;
   }
   cudaMemset(L->xp.p, 0, Rp * TD * 2);
+  // no stale row index before the first forward: a slot whose expert id is
+  // rejected (error flag) keeps pos = -1 and is skipped by the gather
+  cudaMemset(L->pos.p, 0xff, sizeof(int32_t) * (size_t)S * k);
+  cudaMemset(L->order.p, 0xff, sizeof(int32_t) * R);
   cudaMemset(L->comb_cnt.p, 0, sizeof(int32_t) * (size_t)S * (d.token_dim / 128));
   cudaMemset(L->h.p, 0, Rp * HD * 2);
   if ((st = encode_bf16(&L->tmWg, Wg, E, TD, moe::gate_box_rows(E), moe::gate_box_cols(E, d.fuse_front))) ||

@@ -390,3 +390,31 @@ def test_layer_routed_all_tokens_on_few_experts(k):
     ref = OL.layer_forward(_f32(x), _f32(w[1]), _f32(w[2]), ex, gw.astype(np.float64), E)
     err = OL.rel_fro(_f32(out), ref)
     assert err < TOL_OUT
+
+
+def test_invalid_expert_ids_fail_cleanly_and_layer_recovers():
+    """Caller routing with ids outside [0, E) on a fresh layer: the forward
+    reports the reference's range error (no stale row indices reach the
+    gather, no device fault), and the next valid forward is exact."""
+    from paper_2303_06182_b200._capi import MoeError
+
+    S, TD, HD, E, k = 300, 256, 512, 8, 2
+    shape = LayerShape(TD, HD, E, k)
+    w = make_weights(shape, seed=SEED)
+    layer = MoeLayer(shape, S, weights=w)
+    x = make_tokens(S, TD, seed=SEED)
+    rng = np.random.default_rng(7)
+    ex = np.stack([rng.permutation(E)[:k] for _ in range(S)]).astype(np.int32)
+    gw = np.full((S, k), 0.5, np.float32)
+    bad = ex.copy()
+    bad[7, 1] = E
+    bad[100, 0] = -1
+    with pytest.raises(MoeError):
+        layer.forward_routed(x, torch.from_numpy(bad).cuda(), torch.from_numpy(gw).cuda())
+        torch.cuda.synchronize()
+        layer.check_errors()
+    out = layer.forward_routed(x, torch.from_numpy(ex).cuda(), torch.from_numpy(gw).cuda())
+    torch.cuda.synchronize()
+    layer.check_errors()
+    ref = OL.layer_forward(_f32(x), _f32(w[1]), _f32(w[2]), ex, gw.astype(np.float64), E)
+    assert OL.rel_fro(_f32(out), ref) < TOL_OUT
