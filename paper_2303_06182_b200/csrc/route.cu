@@ -379,7 +379,11 @@ cudaError_t launch_route(RouteArgs a, int max_blocks, cudaStream_t stream) {
   }();
   a.late_trigger = late;
   const size_t single_smem = smem_bytes(a.num_experts, kSingleThreads / 32);
-  if (total <= kSingleMaxSlots && single_smem <= 200 * 1024) {
+  static const int single_max = [] {
+    const char* v = getenv("MOE_ROUTE_SINGLE_MAX");  // A/B: largest slot count for the 1-CTA form
+    return v ? atoi(v) : kSingleMaxSlots;
+  }();
+  if (total <= std::min(single_max, kSingleMaxSlots) && single_smem <= 200 * 1024) {
     a.chunk = (total + kSingleThreads - 1) / kSingleThreads * kSingleThreads;
     if (a.chunk == 0) a.chunk = kSingleThreads;
     return launch_chain(route_kernel<true>, dim3(1), dim3(kSingleThreads), single_smem, stream,
