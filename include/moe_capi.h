@@ -303,6 +303,17 @@ int moe_cache_stats(const moe_cache* cache, int64_t* totals5, int* last5);
 /* Resident experts, oldest first (CacheState::insertion_order). */
 int moe_cache_resident(const moe_cache* cache, int32_t* experts, int* n);
 
+/* The cache's replacement controller on plain arrays -- access_batch of
+ * include/moesim/buffer.hpp:45-55 (src/buffer.cpp:57-130), the same code the
+ * GPU cache above runs.  resident[0..*n_resident) are the resident experts
+ * oldest first (CacheState::insertion_order; capacity cache_size), updated in
+ * place.  policy 0 LIFO, 1 FIFO, 2 MIN (MIN needs future: the flattened later
+ * accesses, n_future >= 0; n_future < 0 = no future given).  stats4: accesses,
+ * hits, misses, evictions of this batch.  Host only, no device work. */
+int moe_cache_policy_access(int32_t* resident, int* n_resident, int cache_size, int policy,
+                            const int32_t* active, int n_active, const int32_t* future,
+                            int64_t n_future, int32_t* stats4);
+
 /* Forward with caller-provided routing (idx [S,k] int32, w [S,k] fp32 on the
  * device) instead of the gate: trace replay and skewed synthetic workloads. */
 int moe_layer_forward_routed(moe_layer* layer, const void* X, const int32_t* idx, const float* w,
@@ -415,11 +426,13 @@ typedef struct moe_ep_view {
 int moe_ep_get_view(moe_ep* ep, moe_ep_view* view);
 
 /* exchange.cpp:95-120, payload phase, as slot counts: counts[src*D + dst] =
- * number of assignment slots whose token lives on src (token t on t % D,
- * exchange.cpp:35-37) and whose expert lives on dst = device_of[e].  Host
- * buffers, synchronous (computed on the GPU). */
+ * number of assignment slots whose token lives on src and whose expert lives
+ * on dst = device_of[e].  residency 0: token t on t % D (round robin,
+ * exchange.cpp:35-37, the EP layer's layout); 1: every token on device 0
+ * (Residency::kSingleSource).  Host buffers, synchronous (computed on the
+ * GPU; used by the moesim::plan_dynamic_exchange drop-in). */
 int moe_exchange_counts_host(moe_ctx* ctx, const int32_t* experts, int S, int k, int D,
-                             const int32_t* device_of, int E, int64_t* counts);
+                             const int32_t* device_of, int E, int residency, int64_t* counts);
 
 #ifdef __cplusplus
 }

@@ -5,12 +5,13 @@
 // Besides the types: the synthetic generator, the JSON Lines trace files and
 // the invariant checker / load matrix of the reference (trace.hpp:52-88), so
 // generated or recorded routing can be replayed through the GPU layer
-// (tools/moesim_measure --trace).  The reference's split/sparsity statistics
-// and CSV export are simulator reporting, not provided.
+// (tools/moesim_measure --trace), and the load-matrix utilities the
+// placement protocol uses (split_trace, sparsity_stats, CSV export).
 #pragma once
 
 #include <cstdint>
 #include <filesystem>
+#include <utility>
 #include <vector>
 
 #include <Eigen/Core>
@@ -84,5 +85,23 @@ void save_token_trace(const TokenTrace& trace, const std::filesystem::path& path
 
 /// share(e, b) = fraction of batch b's k * seq_len slots routed to expert e.
 LoadMatrix aggregate_loads(const TokenTrace& trace);
+
+struct SparsityReport {
+  std::vector<int> inactive_per_batch;      // experts with zero share, per batch
+  std::vector<double> top_share_per_batch;  // largest single-expert share
+  Eigen::VectorXd mean_load;                // per-expert mean over batches
+  double mean_inactive_fraction = 0.0;
+  double max_inactive_fraction = 0.0;
+  int never_active = 0;  // experts with zero share in every batch
+};
+
+/// Batch columns [0, cut) and [cut, B), cut = floor(fraction * B) (snapped
+/// when within 1e-9 of an integer); std::invalid_argument if a part is empty.
+std::pair<LoadMatrix, LoadMatrix> split_trace(const LoadMatrix& loads, double fraction);
+
+SparsityReport sparsity_stats(const LoadMatrix& loads);
+
+/// CSV "expert,b0,b1,..." with one row per expert (doubles as %.12g).
+void save_load_matrix_csv(const LoadMatrix& loads, const std::filesystem::path& path);
 
 }  // namespace moesim

@@ -55,6 +55,9 @@ def ref_lib():
         _sig(lib.ref_cache_access, _I, _P, _P, _I, _I, _I, _P, _I, _P, _P, _P)
         _sig(lib.ref_greedy_place, _I, _P, _I, _I, _I, _P)
         _sig(lib.ref_contiguous_place, _I, _I, _I, _P)
+        _sig(lib.ref_anticorr_place, _I, _P, _I, _I, _I, _D, _P)
+        _sig(lib.ref_pearson_corr, _I, _P, _I, _I, _P)
+        _sig(lib.ref_eval_balance, _I, _P, _I, _I, _P, _I, _P)
         _sig(lib.ref_plan_dynamic_exchange, _I, _P, _I, _I, _I, _I, _P, _I64, _P, _P)
         _sig(lib.ref_gen_synthetic_trace, _I, _I, _I, _I, _I, _D, _D, _D, C.c_uint64, _P, _P)
         _sig(lib.ref_save_synthetic_trace, _I, _I, _I, _I, _I, _D, _D, _D, C.c_uint64, C.c_char_p)
@@ -219,6 +222,40 @@ def ref_contiguous_place(E: int, D: int):
     if rc:
         raise OracleError(ref_lib().ref_last_error().decode())
     return out
+
+
+def _loads(loads):
+    l = np.ascontiguousarray(loads, dtype=np.float64)
+    return l, l.shape[0], l.shape[1]
+
+
+def ref_anticorr_place(loads: np.ndarray, D: int, weight: float = 0.5):
+    l, E, B = _loads(loads)
+    out = np.zeros(E, np.int32)
+    rc = ref_lib().ref_anticorr_place(_ptr(l), E, B, D, weight, _ptr(out))
+    if rc:
+        raise OracleError(ref_lib().ref_last_error().decode())
+    return out
+
+
+def ref_pearson_corr(loads: np.ndarray):
+    l, E, B = _loads(loads)
+    out = np.zeros((E, E), np.float64)
+    rc = ref_lib().ref_pearson_corr(_ptr(l), E, B, _ptr(out))
+    if rc:
+        raise OracleError(ref_lib().ref_last_error().decode())
+    return out
+
+
+def ref_eval_balance(device_of, D: int, loads: np.ndarray):
+    """(max_load, avg_max_load, objective) of balance.cpp:153-165."""
+    l, E, B = _loads(loads)
+    dev = np.ascontiguousarray(device_of, dtype=np.int32)
+    out = np.zeros(3, np.float64)
+    rc = ref_lib().ref_eval_balance(_ptr(dev), E, D, _ptr(l), B, _ptr(out))
+    if rc:
+        raise OracleError(ref_lib().ref_last_error().decode())
+    return tuple(float(x) for x in out)
 
 
 def ref_plan_dynamic_exchange(experts, E, D, device_of, token_bytes):

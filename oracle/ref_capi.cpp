@@ -230,6 +230,47 @@ int ref_contiguous_place(int E, int D, int* device_of) {
   });
 }
 
+int ref_anticorr_place(const double* loads, int E, int B, int D, double weight, int* device_of) {
+  return guarded([&] {
+    moesim::LoadMatrix lm;
+    lm.share = Eigen::MatrixXd::Zero(E, B);
+    for (int e = 0; e < E; ++e)
+      for (int b = 0; b < B; ++b) lm.share(e, b) = loads[static_cast<int64_t>(e) * B + b];
+    const auto p = moesim::anticorr_place(lm, D, weight);
+    for (int e = 0; e < E; ++e) device_of[e] = p.device_of[static_cast<std::size_t>(e)];
+  });
+}
+
+// pearson_corr (balance.cpp:69-90); corr is E x E row-major.
+int ref_pearson_corr(const double* loads, int E, int B, double* corr) {
+  return guarded([&] {
+    moesim::LoadMatrix lm;
+    lm.share = Eigen::MatrixXd::Zero(E, B);
+    for (int e = 0; e < E; ++e)
+      for (int b = 0; b < B; ++b) lm.share(e, b) = loads[static_cast<int64_t>(e) * B + b];
+    const auto c = moesim::pearson_corr(lm);
+    for (int i = 0; i < E; ++i)
+      for (int j = 0; j < E; ++j) corr[static_cast<int64_t>(i) * E + j] = c.corr(i, j);
+  });
+}
+
+// eval_balance (balance.cpp:153-165); out3 = max_load, avg_max_load, objective.
+int ref_eval_balance(const int* device_of, int E, int D, const double* loads, int B, double* out3) {
+  return guarded([&] {
+    moesim::Placement p;
+    p.num_devices = D;
+    p.device_of.assign(device_of, device_of + E);
+    moesim::LoadMatrix lm;
+    lm.share = Eigen::MatrixXd::Zero(E, B);
+    for (int e = 0; e < E; ++e)
+      for (int b = 0; b < B; ++b) lm.share(e, b) = loads[static_cast<int64_t>(e) * B + b];
+    const auto r = moesim::eval_balance(p, lm);
+    out3[0] = r.max_load;
+    out3[1] = r.avg_max_load;
+    out3[2] = r.objective;
+  });
+}
+
 // ---- exchange (exchange.cpp:95-120) -------------------------------------
 // Returns the D x D "size" and "payload" byte matrices, row-major src->dst.
 int ref_plan_dynamic_exchange(const int* experts, int S, int k, int E, int D,

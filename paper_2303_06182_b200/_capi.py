@@ -44,7 +44,7 @@ EXPORTED = [
     "moe_layer_forward_host_batches", "moe_layer_repack",
     "moe_ep_create", "moe_ep_destroy", "moe_ep_get_handle", "moe_ep_connect", "moe_ep_forward",
     "moe_ep_forward_graph", "moe_ep_check_errors", "moe_ep_get_view", "moe_ep_enable_timing",
-    "moe_ep_stage_times",
+    "moe_ep_stage_times", "moe_cache_policy_access",
 ]
 
 
@@ -143,7 +143,7 @@ def load(path: str = LIB_PATH):
     _sig(lib.moe_layer_repack, I, P, P)
     _sig(lib.moe_layer_get_view, I, P, C.POINTER(LayerView))
     _sig(lib.moe_layer_set_weight_pool, I, P, P, P, I, P)
-    _sig(lib.moe_exchange_counts_host, I, P, P, I, I, I, P, I, P)
+    _sig(lib.moe_exchange_counts_host, I, P, P, I, I, I, P, I, I, P)
     _sig(lib.moe_layer_enable_timing, I, P, I)
     _sig(lib.moe_layer_stage_times, I, P, I, P)
     _sig(lib.moe_ffn_create, I, P, C.POINTER(FfnDesc), P, P, C.POINTER(P))
@@ -157,6 +157,7 @@ def load(path: str = LIB_PATH):
     _sig(lib.moe_cache_forward_routed, I, P, P, P, P, I, P, P)
     _sig(lib.moe_cache_stats, I, P, P, P)
     _sig(lib.moe_cache_resident, I, P, P, P)
+    _sig(lib.moe_cache_policy_access, I, P, P, I, I, P, I, P, C.c_int64, P)
     _sig(lib.moe_layer_forward_routed, I, P, P, P, P, I, P, P)
     if not hasattr(lib, "moe_ep_create"):  # an older build (A/B runs via MOE_LIB_PATH)
         _lib = lib

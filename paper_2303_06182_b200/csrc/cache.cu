@@ -20,6 +20,7 @@
 // cache needs to know the active set, shared with the EP count exchange in
 // the paper's design).
 #include <algorithm>
+#include <cstdint>
 
 #include "capi_state.h"
 
@@ -69,15 +70,92 @@ int ensure_events(moe_cache* C, size_t n) {
   return MOE_OK;
 }
 
-// access_batch (buffer.cpp:57-130) over `active` (sorted, unique), emitting
-// the GPU schedule.  Returns the waves.
+// One cache decision, in access order: victim -2 = hit, -1 = miss into a free
+// slot, >= 0 = miss that evicts `victim`.
+struct CacheStep {
+  int expert;
+  int victim;
+};
+
+// The expert-buffering controller, access_batch semantics
+// (proj/src/buffer.cpp:57-130, include/moesim/buffer.hpp:45-55): the sorted,
+// distinct active experts are accessed serially; a miss inserts at the back
+// of `order` (residents oldest first) and, when the cache is full, evicts
+//   LIFO / FIFO: the most recently inserted resident inactive in this batch,
+//                else the newest (LIFO) / oldest (FIFO) resident;
+//   MIN:         the resident whose next use -- later in this batch, then in
+//                `future` -- is farthest; never-used-again first, ties to
+//                the lowest id.
+// Shared by the GPU cache (plan_batch below) and the moesim::access_batch
+// drop-in (through moe_cache_policy_access), so both make the same decisions.
+void cache_policy_run(std::vector<int>& order, int cache_size, int policy,
+                      const std::vector<int>& active, const int32_t* future, int64_t n_future,
+                      std::vector<CacheStep>& steps) {
+  steps.clear();
+  const int top = active.empty() ? 0 : active.back();
+  int hi = top;
+  for (int r : order) hi = std::max(hi, r);
+  std::vector<char> live((size_t)hi + 1, 0), here((size_t)hi + 1, 0);
+  for (int x : active) live[x] = 1;
+  for (int r : order) here[r] = 1;
+  // MIN: index of each expert's next access.  Within the batch the access
+  // sequence is `active` itself; the future stream follows it.
+  std::vector<int64_t> next_future;
+  if (policy == 2) {
+    next_future.assign((size_t)hi + 1, INT64_MAX);
+    for (int64_t i = n_future - 1; i >= 0; --i) {
+      const int e = future[i];
+      if (e >= 0 && e <= hi) next_future[e] = i;
+    }
+  }
+  for (size_t ai = 0; ai < active.size(); ++ai) {
+    const int x = active[ai];
+    if (here[x]) {
+      steps.push_back({x, -2});
+      continue;
+    }
+    int victim = -1;
+    if ((int)order.size() >= cache_size) {
+      if (policy == 2) {
+        int64_t far = -1;
+        for (int r : order) {
+          int64_t when;
+          const auto it = std::lower_bound(active.begin() + ai + 1, active.end(), r);
+          if (it != active.end() && *it == r)
+            when = it - active.begin();
+          else if (next_future[r] != INT64_MAX)
+            when = (int64_t)active.size() + next_future[r];
+          else
+            when = INT64_MAX;
+          if (when > far || (when == far && r < victim)) {
+            far = when;
+            victim = r;
+          }
+        }
+      } else {
+        for (auto it = order.rbegin(); it != order.rend() && victim < 0; ++it)
+          if (!live[*it]) victim = *it;
+        if (victim < 0) victim = policy == 0 ? order.back() : order.front();
+      }
+      order.erase(std::find(order.begin(), order.end(), victim));
+      here[victim] = 0;
+    }
+    order.push_back(x);
+    here[x] = 1;
+    steps.push_back({x, victim});
+  }
+}
+
+// The GPU schedule of one batch from the controller's decisions: slots for
+// the misses and the waves (a wave closes right before a miss would evict an
+// expert the wave itself still has to run).
 std::vector<Wave> plan_batch(moe_cache* C, const std::vector<int>& active, int* stats) {
+  std::vector<CacheStep> steps;
+  cache_policy_run(C->order, C->n_slots, C->policy, active, nullptr, 0, steps);
   std::vector<Wave> waves;
   Wave cur;
   cur.e_lo = -1;
   std::vector<char> in_wave(C->slot_of.size(), 0);
-  std::vector<char> is_active(C->slot_of.size(), 0);
-  for (int x : active) is_active[x] = 1;
   auto close_wave = [&]() {
     if (cur.e_lo >= 0) {
       for (auto& es : cur.table) in_wave[es.first] = 0;
@@ -86,33 +164,23 @@ std::vector<Wave> plan_batch(moe_cache* C, const std::vector<int>& active, int* 
     cur = Wave();
     cur.e_lo = -1;
   };
-  for (int x : active) {
+  for (const CacheStep& st : steps) {
+    const int x = st.expert;
     ++stats[0];
-    const bool resident = C->slot_of[x] >= 0;
-    if (resident) {
+    if (st.victim == -2) {
       ++stats[1];
     } else {
       ++stats[2];
       int slot;
-      if ((int)C->order.size() == C->n_slots) {
-        int victim = -1;
-        for (auto it = C->order.rbegin(); it != C->order.rend(); ++it)
-          if (!is_active[*it]) {
-            victim = *it;
-            break;
-          }
-        if (victim < 0) victim = C->policy == 0 ? C->order.back() : C->order.front();
-        // the victim's weights are still needed by the current wave: close it
-        if (in_wave[victim]) close_wave();
-        C->order.erase(std::find(C->order.begin(), C->order.end(), victim));
-        slot = C->slot_of[victim];
-        C->slot_of[victim] = -1;
+      if (st.victim >= 0) {
+        if (in_wave[st.victim]) close_wave();  // its weights are still needed by this wave
+        slot = C->slot_of[st.victim];
+        C->slot_of[st.victim] = -1;
         ++stats[3];
       } else {
         slot = C->free_slots.back();
         C->free_slots.pop_back();
       }
-      C->order.push_back(x);
       C->slot_of[x] = slot;
       if (cur.e_lo < 0) cur.e_lo = x;
       cur.loads.emplace_back(x, slot);
@@ -261,6 +329,40 @@ int moe_cache_stats(const moe_cache* C, int64_t* totals5, int* last5) {
   }
   if (last5)
     for (int i = 0; i < 5; ++i) last5[i] = C->last_stats[i];
+  return MOE_OK;
+}
+
+int moe_cache_policy_access(int32_t* resident, int* n_resident, int cache_size, int policy,
+                            const int32_t* active, int n_active, const int32_t* future,
+                            int64_t n_future, int32_t* stats4) {
+  if (!resident || !n_resident || (!active && n_active > 0) || !stats4)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (cache_size < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "cache_size must be >= 1");
+  if (policy < 0 || policy > 2) return fail(MOE_ERR_INVALID_ARGUMENT, "unknown cache policy");
+  if (policy == 2 && n_future < 0)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "MIN policy requires the future access sequence");
+  if (n_future > 0 && !future) return fail(MOE_ERR_INVALID_ARGUMENT, "null future");
+  if (*n_resident < 0 || *n_resident > cache_size)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "resident set larger than the cache");
+  std::vector<int> act(active, active + std::max(n_active, 0));
+  for (int e : act)
+    if (e < 0) return fail(MOE_ERR_INVALID_ARGUMENT, "negative expert id");
+  std::sort(act.begin(), act.end());
+  act.erase(std::unique(act.begin(), act.end()), act.end());
+  std::vector<int> order(resident, resident + *n_resident);
+  std::vector<CacheStep> steps;
+  cache_policy_run(order, cache_size, policy, act, future, std::max<int64_t>(n_future, 0), steps);
+  stats4[0] = stats4[1] = stats4[2] = stats4[3] = 0;
+  for (const CacheStep& st : steps) {
+    ++stats4[0];
+    if (st.victim == -2)
+      ++stats4[1];
+    else
+      ++stats4[2];
+    if (st.victim >= 0) ++stats4[3];
+  }
+  *n_resident = (int)order.size();
+  std::copy(order.begin(), order.end(), resident);
   return MOE_OK;
 }
 

@@ -15,7 +15,10 @@ __global__ void inverse_order_kernel(const int32_t* order, int64_t n, int32_t* p
   }
 }
 
-__global__ void exchange_counts_kernel(const int32_t* experts, int S, int k, int D,
+// counts[src * D + dst]: slots of tokens resident on src (token t on t % n_src:
+// round robin with n_src = D, single source with n_src = 1) routed to an
+// expert placed on dst.
+__global__ void exchange_counts_kernel(const int32_t* experts, int S, int k, int n_src, int D,
                                        const int32_t* device_of, int E,
                                        unsigned long long* counts, int32_t* err) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)S * k;
@@ -25,7 +28,7 @@ __global__ void exchange_counts_kernel(const int32_t* experts, int S, int k, int
       atomicOr(err, 1);
       continue;
     }
-    const int src = (int)((i / k) % D);
+    const int src = (int)((i / k) % n_src);
     atomicAdd(&counts[(int64_t)src * D + device_of[e]], 1ull);
   }
 }
@@ -342,37 +345,40 @@ int moe_inverse_order_host(moe_ctx* ctx, const int32_t* order, int64_t n, int32_
 }
 
 int moe_exchange_counts_host(moe_ctx* ctx, const int32_t* experts, int S, int k, int D,
-                             const int32_t* device_of, int E, int64_t* counts) {
+                             const int32_t* device_of, int E, int residency, int64_t* counts) {
   if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
   int st = check_batch(S, k, E);
   if (st) return st;
   if (D < 1 || E % D != 0)
     return fail(MOE_ERR_INVALID_ARGUMENT, "num_experts must divide evenly across devices");
+  if (residency != 0 && residency != 1) return fail(MOE_ERR_INVALID_ARGUMENT, "unknown residency");
   for (int e = 0; e < E; ++e)
     if (device_of[e] < 0 || device_of[e] >= D)
       return fail(MOE_ERR_INVALID_ARGUMENT, "device_of out of range");
   MOE_CUDA(cudaSetDevice(ctx->device));
   st = ctx->prepare_route(E);
   if (st) return st;
-  int32_t *d_e = nullptr, *d_dev = nullptr;
-  unsigned long long* d_c = nullptr;
-  MOE_CUDA(cudaMalloc(&d_e, (size_t)S * k * 4));
-  MOE_CUDA(cudaMalloc(&d_dev, (size_t)E * 4));
-  MOE_CUDA(cudaMalloc(&d_c, (size_t)D * D * 8));
-  cudaMemcpy(d_e, experts, (size_t)S * k * 4, cudaMemcpyHostToDevice);
-  cudaMemcpy(d_dev, device_of, (size_t)E * 4, cudaMemcpyHostToDevice);
-  cudaMemset(d_c, 0, (size_t)D * D * 8);
+  // scratch freed on every path
+  struct Scratch {
+    DevBuf<int32_t> ids, dev;
+    DevBuf<unsigned long long> c;
+    ~Scratch() {
+      ids.release();
+      dev.release();
+      c.release();
+    }
+  } w;
+  if ((st = w.ids.reserve((size_t)S * k)) || (st = w.dev.reserve(E)) || (st = w.c.reserve((size_t)D * D)))
+    return st;
+  MOE_CUDA(cudaMemcpy(w.ids.p, experts, (size_t)S * k * 4, cudaMemcpyHostToDevice));
+  MOE_CUDA(cudaMemcpy(w.dev.p, device_of, (size_t)E * 4, cudaMemcpyHostToDevice));
+  MOE_CUDA(cudaMemset(w.c.p, 0, (size_t)D * D * 8));
   exchange_counts_kernel<<<std::max(1, std::min(4096, (S * k + 255) / 256)), 256>>>(
-      d_e, S, k, D, d_dev, E, d_c, ctx->err_flag.p);
-  int rc = moe_check_errors(ctx, 0);
-  if (!rc) {
-    cudaError_t e = cudaMemcpy(counts, d_c, (size_t)D * D * 8, cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) rc = cuda_fail(e, "D2H counts");
-  }
-  cudaFree(d_e);
-  cudaFree(d_dev);
-  cudaFree(d_c);
-  return rc;
+      w.ids.p, S, k, residency == 1 ? 1 : D, D, w.dev.p, E, w.c.p, ctx->err_flag.p);
+  MOE_CUDA(cudaGetLastError());
+  if ((st = moe_check_errors(ctx, 0))) return st;
+  MOE_CUDA(cudaMemcpy(counts, w.c.p, (size_t)D * D * 8, cudaMemcpyDeviceToHost));
+  return MOE_OK;
 }
 
 int moe_gate_topk(moe_ctx* ctx, const void* X, const void* Wg, int S, int TD, int E, int k,

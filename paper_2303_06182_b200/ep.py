@@ -33,7 +33,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import _capi
+from . import _capi, placement
 from ._capi import check
 
 
@@ -75,10 +75,12 @@ class Placement:
             key[loc] = d * El + np.arange(len(loc), dtype=np.int32)
         return key
 
+    # The policies are the C++ host library's (host/balance.cpp, the drop-in
+    # of balance.cpp:59-151), bound through include/moesim/placement_c.h.
     @staticmethod
     def contiguous(E: int, D: int) -> "Placement":
         """balance.cpp:59-67: expert m on device floor(m / (E/D))."""
-        p = Placement((np.arange(E) // (E // D)).astype(np.int32), D)
+        p = Placement(placement.contiguous_place(E, D), D)
         p.validate()
         return p
 
@@ -87,29 +89,21 @@ class Placement:
         """balance.cpp:92-115: experts by mean historical load descending (ties:
         lower id) go to the open device with the least accumulated load (ties:
         lower device id); a device closes at E/D experts."""
-        loads = np.asarray(loads, dtype=np.float64)
-        E = loads.shape[0]
-        if E % D:
-            raise ValueError("num_experts must divide evenly across devices")
-        mean = loads.mean(axis=1)
-        order = sorted(range(E), key=lambda e: (-mean[e], e))
-        cap = E // D
-        dev_load = [0.0] * D
-        held = [0] * D
-        out = np.empty(E, np.int32)
-        for e in order:
-            best = -1
-            for d in range(D):
-                if held[d] >= cap:
-                    continue
-                if best < 0 or dev_load[d] < dev_load[best]:
-                    best = d
-            out[e] = best
-            held[best] += 1
-            dev_load[best] += mean[e]
-        p = Placement(out, D)
+        p = Placement(placement.greedy_place(loads, D), D)
         p.validate()
         return p
+
+    @staticmethod
+    def anticorr(loads: np.ndarray, D: int, weight: float = 0.5) -> "Placement":
+        """balance.cpp:117-151: the greedy loop scored by sum over the
+        device's experts of mean load + weight * Pearson correlation."""
+        p = Placement(placement.anticorr_place(loads, D, weight), D)
+        p.validate()
+        return p
+
+    def balance(self, loads: np.ndarray) -> dict:
+        """eval_balance (balance.cpp:153-165) of this placement on a load history."""
+        return placement.eval_balance(self.device_of, self.num_devices, loads)
 
 
 # ------------------------------------------------------------------ transport

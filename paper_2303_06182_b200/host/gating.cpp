@@ -16,33 +16,14 @@
 #include <vector>
 
 #include "moe_capi.h"
+#include "device_context.hpp"
 #include "moesim/gating.hpp"
 
 namespace moesim {
 
 namespace {
 
-std::mutex g_mu;
-moe_ctx* g_ctx = nullptr;
-
-// Process-wide context on device 0 (the C ABI context is not thread-safe, so
-// every use below holds g_mu).
-moe_ctx* context_locked() {
-  if (!g_ctx) {
-    const int st = moe_ctx_create(0, &g_ctx);
-    if (st != MOE_OK) {
-      g_ctx = nullptr;
-      throw std::runtime_error(std::string("moesim: no usable B200 (") + moe_last_error() + ")");
-    }
-  }
-  return g_ctx;
-}
-
-[[noreturn]] void rethrow(int status) {
-  const std::string msg = moe_last_error();
-  if (status == MOE_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
-  throw std::runtime_error("moesim: " + msg);
-}
+using detail::with_context;
 
 void check_batch(const Batch& batch, const GatingConfig& cfg) {
   if (cfg.num_experts < 1) throw std::invalid_argument("num_experts must be positive");
@@ -65,9 +46,7 @@ namespace detail {
 
 std::vector<int> inverse_order(const int* order, std::int64_t n, std::int64_t n_slots) {
   std::vector<int> pos(static_cast<std::size_t>(std::max<std::int64_t>(n_slots, 1)), -1);
-  std::lock_guard<std::mutex> lock(g_mu);
-  const int st = moe_inverse_order_host(context_locked(), order, n, pos.data(), n_slots);
-  if (st != MOE_OK) rethrow(st);
+  with_context([&](moe_ctx* c) { return moe_inverse_order_host(c, order, n, pos.data(), n_slots); });
   pos.resize(static_cast<std::size_t>(n_slots));
   return pos;
 }
@@ -90,11 +69,10 @@ DynamicDispatchPlan dynamic_dispatch(const Batch& batch, const GatingConfig& cfg
   plan.order.resize(ids.size());
   plan.counts.resize(static_cast<std::size_t>(cfg.num_experts));
   plan.splits.resize(static_cast<std::size_t>(cfg.num_experts) + 1);
-  std::lock_guard<std::mutex> lock(g_mu);
-  const int st = moe_dynamic_dispatch_host(context_locked(), ids.data(), plan.seq_len, plan.top_k,
-                                           plan.num_experts, plan.order.data(), plan.counts.data(),
-                                           plan.splits.data());
-  if (st != MOE_OK) rethrow(st);
+  with_context([&](moe_ctx* c) {
+    return moe_dynamic_dispatch_host(c, ids.data(), plan.seq_len, plan.top_k, plan.num_experts,
+                                     plan.order.data(), plan.counts.data(), plan.splits.data());
+  });
   return plan;
 }
 
@@ -115,13 +93,11 @@ StaticDispatchPlan static_dispatch(const Batch& batch, const GatingConfig& cfg) 
   std::vector<std::int32_t> slots(static_cast<std::size_t>(cells));
   std::vector<std::int32_t> dropped(2 * ids.size() + 2);
   std::int32_t cap = 0, n_dropped = 0;
-  {
-    std::lock_guard<std::mutex> lock(g_mu);
-    const int st = moe_static_dispatch_host(context_locked(), ids.data(), plan.seq_len,
-                                            plan.top_k, plan.num_experts, cfg.capacity_factor,
-                                            &cap, slots.data(), cells, dropped.data(), &n_dropped);
-    if (st != MOE_OK) rethrow(st);
-  }
+  with_context([&](moe_ctx* c) {
+    return moe_static_dispatch_host(c, ids.data(), plan.seq_len, plan.top_k, plan.num_experts,
+                                    cfg.capacity_factor, &cap, slots.data(), cells, dropped.data(),
+                                    &n_dropped);
+  });
   // the C ABI returns the table expert-major; Eigen's storage is column-major
   plan.slots = Eigen::MatrixXi::Constant(plan.num_experts, plan.capacity, kPlaceholder);
   for (int e = 0; e < plan.num_experts; ++e)

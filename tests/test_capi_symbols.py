@@ -40,7 +40,20 @@ def test_cxx_dropin_library_exports_reference_api():
                 "moesim::dispatch_mask_elements(int, int, double)",
                 "moesim::dispatch_cost_counts(moesim::DynamicDispatchPlan const&, int)",
                 "moesim::debug_json[abi:cxx11](moesim::StaticDispatchPlan const&)",
-                "moesim::debug_json[abi:cxx11](moesim::DynamicDispatchPlan const&)"]:
+                "moesim::debug_json[abi:cxx11](moesim::DynamicDispatchPlan const&)",
+                # adjacent API: exchange.hpp, balance.hpp, buffer.hpp
+                "moesim::make_topology(int, int, long, long, moesim::Residency)",
+                "moesim::plan_dynamic_exchange(moesim::DynamicDispatchPlan const&, moesim::Topology const&, "
+                "moesim::Placement const&)",
+                "moesim::plan_static_exchange(moesim::StaticDispatchPlan const&, moesim::Topology const&, "
+                "moesim::Placement const&)",
+                "moesim::greedy_place(moesim::LoadMatrix const&, int)",
+                "moesim::anticorr_place(moesim::LoadMatrix const&, int, double)",
+                "moesim::pearson_corr(moesim::LoadMatrix const&)",
+                "moesim::eval_balance(moesim::Placement const&, moesim::LoadMatrix const&)",
+                "moesim::run_cache_sim(moesim::LoadMatrix const&, moesim::Placement const&, "
+                "moesim::CacheConfig const&)",
+                "moesim::split_trace(moesim::LoadMatrix const&, double)"]:
         assert sym in out, sym
 
 
