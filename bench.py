@@ -188,6 +188,8 @@ def dist_setup():
     if world > 1:
         import torch.distributed as dist
 
+        if os.environ.get("MOE_BENCH_ONE_GPU_TEST") != "1" and torch.cuda.device_count() < world:
+            raise SystemExit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} GPU(s) visible")
         torch.cuda.set_device(local)
         if os.environ.get("MOE_BENCH_ONE_GPU_TEST") == "1":
             dist.init_process_group("gloo")
@@ -256,72 +258,103 @@ def run_reference(args):
 
 def run_ep(args, world, rank, local):
     """N > 1: expert parallelism.  E/N experts per GPU (placement: the
-    reference's greedy policy on a calibration routing histogram, or
-    contiguous), S tokens per GPU (weak scaling).  Exchange (--ep-transport):
-      p2p   (default) the layer's own kernels over NVLink peer memory
-            (moe_ep_*): counts published into every peer's window, token rows
-            gathered straight into the owner's receive buffer, outputs read
-            back by the combine -- no host sync, the step is one CUDA graph
-      nccl  count all-to-all + host sync + variable payload all-to-all over
-            NCCL (torch.distributed), the comparison path"""
+    reference's greedy policy -- the C++ host library's greedy_place -- on a
+    calibration routing histogram, or contiguous).  --scaling weak: S tokens
+    per GPU; strong: the S tokens of one batch split over the GPUs, token t on
+    GPU t % N (exchange.cpp:35-37).  Exchange (--ep-transport), both in the C
+    ABI (moe_ep_*):
+      p2p   (default) the layer's own kernels over NVLink peer memory:
+            counts published into every peer's window, token rows gathered
+            straight into the owner's receive buffer, outputs read back by the
+            combine -- no host sync, the step is one CUDA graph
+      nccl  NCCL count all-gather + host sync + grouped ncclSend/ncclRecv of
+            the rows and back (csrc/ep_nccl.cu), the comparison path"""
     import numpy as np
     import torch
+    import torch.distributed as dist
 
-    from paper_2303_06182_b200.ep import (ExpertParallelMoE, KernelBackend, PeerExpertParallelMoE,
-                                          Placement, Transport)
+    from paper_2303_06182_b200 import placement as PL
+    from paper_2303_06182_b200.ep import PeerExpertParallelMoE, Placement
     from paper_2303_06182_b200.layer import Context, LayerShape, make_tokens, make_weights
 
-    S, TD, HD, E, k, mode, C, desc = WORKLOADS[args.workload]
+    S_job, TD, HD, E, k, mode, C, desc = WORKLOADS[args.workload]
     if mode != "dynamic":
         raise SystemExit("expert parallelism is implemented for dynamic gating")
     hbm_gbs, tflops, peak_kind = measured_peaks()
     ctx = Context.get(local)
     shape = LayerShape(TD, HD, E, k)
     Wg, W1, W2 = make_weights(shape, seed=2303061820, ctx=ctx)
-    x = make_tokens(S, TD, seed=2303061820 + rank, ctx=ctx)
+    strong = args.scaling == "strong"
+    if strong:
+        # one global batch; this rank holds tokens t = rank, rank + N, ...
+        xg = make_tokens(S_job, TD, seed=2303061820, ctx=ctx)
+        x = xg[rank::world].contiguous()
+        del xg
+        S = x.shape[0]
+        S_total = S_job
+        S_max = (S_job + world - 1) // world
+    else:
+        x = make_tokens(S_job, TD, seed=2303061820 + rank, ctx=ctx)
+        S = S_job
+        S_max = S_job
+        S_total = S_job * world
+    # calibration history for the placement: one gate pass over a DIFFERENT
+    # batch (the two-half protocol of the reference CLI, tools/moesim.cpp:
+    # 451-492: place on one half of the trace, run on the other)
+    import ctypes
+
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    cur = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def expert_hist(tokens):
+        n = tokens.shape[0]
+        idx = torch.empty(n, k, dtype=torch.int32, device="cuda")
+        w = torch.empty(n, k, dtype=torch.float32, device="cuda")
+        ctx.lib.moe_gate_topk(ctx.h, P(tokens), P(Wg), n, TD, E, k, P(idx), P(w), None, cur)
+        h = torch.bincount(idx.view(-1).long(), minlength=E).double()
+        dist.all_reduce(h)
+        return h.cpu().numpy()
+
+    x_cal = make_tokens(S, TD, seed=2303061820 + 7919 + rank, ctx=ctx)
+    hist = expert_hist(x_cal)[:, None] / (S * k * world)
+    del x_cal
+    hist_run = expert_hist(x)[:, None] / (S * k * world)
     if args.placement == "greedy":
-        # calibration: per-expert load share of one gate pass over this rank's
-        # tokens, summed over ranks (the "history" greedy_place consumes)
-        idx = torch.empty(S, k, dtype=torch.int32, device="cuda")
-        w = torch.empty(S, k, dtype=torch.float32, device="cuda")
-        import ctypes
-
-        P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
-        ctx.lib.moe_gate_topk(ctx.h, P(x), P(Wg), S, TD, E, k, P(idx), P(w), None,
-                              ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
-        hist = torch.bincount(idx.view(-1).long(), minlength=E).double()
-        import torch.distributed as dist
-
-        dist.all_reduce(hist)
-        pl = Placement.greedy(hist.cpu().numpy()[:, None] / (S * k * world), world)
+        pl = Placement.greedy(hist, world)
     else:
         pl = Placement.contiguous(E, world)
+    contig = PL.contiguous_place(E, world)
+    balance = {
+        "placement": args.placement, "history": "gate routing of a separate calibration batch",
+        "ideal_load": 1.0 / world,
+        "max_load_calibration": pl.balance(hist)["max_load"],
+        "max_load_run_batch": pl.balance(hist_run)["max_load"],
+        "contiguous_max_load_run_batch": PL.eval_balance(contig, world, hist_run)["max_load"],
+    }
     loc = torch.from_numpy(pl.local_experts(rank)).long().cuda()
     W1l, W2l = W1[loc].contiguous(), W2[loc].contiguous()
     del W1, W2
     torch.cuda.empty_cache()
     p2p = args.ep_transport == "p2p"
     transport_note = ""
+    layer = None
     if p2p:
         from paper_2303_06182_b200.ep import PeerMemoryUnavailable
 
         try:
-            layer = PeerExpertParallelMoE(ctx, pl, shape, Wg, W1l, W2l, S, rank)
+            layer = PeerExpertParallelMoE(ctx, pl, shape, Wg, W1l, W2l, S_max, rank)
         except PeerMemoryUnavailable as e:  # raised on every rank: fall back together
             p2p = False
             transport_note = f"p2p unavailable ({e}); NCCL fallback"
-    if p2p:
-        be = None
-        fwd = lambda xx, st, out=None: layer.forward(xx, st, out=out, graph=not args.no_graph)  # noqa: E731
-        check = layer.check_errors
-        n_launch = 8  # gate, route, publish, dispatch, recv, FFN, done, combine
-    else:
-        be = KernelBackend(ctx, shape, Wg, W1l, W2l, S, S * k * world, tile_n=args.tile_n)
-        layer = ExpertParallelMoE(pl, k, be, Transport(), rank)
-        fwd = lambda xx, st, out=None: layer.forward(xx, st)  # noqa: E731
-        check = be.check_errors
-        n_launch = 9
-    del W1l, W2l  # each EP form keeps what it needs (packed copy / tensor references)
+    if layer is None:
+        layer = PeerExpertParallelMoE(ctx, pl, shape, Wg, W1l, W2l, S_max, rank, transport="nccl")
+    use_graph = p2p and not args.no_graph  # NCCL forwards have a host sync: eager
+    fwd = lambda xx, st, out=None: layer.forward(xx, st, out=out, graph=use_graph)  # noqa: E731
+    check = layer.check_errors
+    # p2p: gate, route, publish, dispatch, recv, FFN, done, combine;
+    # nccl: gate, route, gather, regroup, recv, FFN, regroup, combine (+ NCCL's own)
+    n_launch = 8
+    del W1l, W2l  # the EP layer keeps its tile-packed copy
     torch.cuda.empty_cache()
     stream = torch.cuda.Stream()
     stream.wait_stream(torch.cuda.current_stream())  # inputs were written on the current stream
@@ -359,25 +392,28 @@ def run_ep(args, world, rank, local):
     if sampler:
         sampler.stop()
     check(stream)
-    ep_stage = None
-    if p2p:
-        v = layer.view(S)
-        cnt = v["counts"].cpu().numpy().reshape(world, E // world).sum(1)
-        recv_rows = v["recv_rows"]
-        sent_off = int(cnt.sum() - cnt[rank])
-        # per-stage events from a separate untimed pass of eager forwards
-        # (collective: every rank runs it); median per stage, max over ranks
-        layer.enable_timing(True)
-        per = []
-        with torch.cuda.stream(stream):
-            for _ in range(5):
-                layer.forward(x, stream, out=out_buf, graph=False)
-                per.append(layer.stage_times())
-        layer.enable_timing(False)
-        ep_stage = {kk: max_over_ranks(float(np.median([p_[kk] for p_ in per])), world) for kk in per[0]}
-    else:
-        recv_rows = layer.last["recv_rows"]
-        sent_off = int(layer.last["send_counts"].sum()) - int(layer.last["send_counts"][rank].sum())
+    v = layer.view(S)
+    cnt = v["counts"].cpu().numpy().reshape(world, E // world).sum(1)
+    recv_rows = v["recv_rows"]
+    sent_off = int(cnt.sum() - cnt[rank])
+    # measured per-GPU load: rows each GPU's experts received this step
+    rr = torch.tensor([recv_rows], dtype=torch.int64, device="cuda")
+    all_rr = [torch.zeros_like(rr) for _ in range(world)]
+    dist.all_gather(all_rr, rr)
+    rows_per_gpu = [int(t.item()) for t in all_rr]
+    balance["measured_rows_per_gpu"] = rows_per_gpu
+    balance["measured_max_load"] = max(rows_per_gpu) / max(sum(rows_per_gpu), 1)
+    balance["measured_max_over_mean"] = max(rows_per_gpu) / max(np.mean(rows_per_gpu), 1e-9)
+    # per-stage events from a separate untimed pass of eager forwards
+    # (collective: every rank runs it); median per stage, max over ranks
+    layer.enable_timing(True)
+    per = []
+    with torch.cuda.stream(stream):
+        for _ in range(5):
+            layer.forward(x, stream, out=out_buf, graph=False)
+            per.append(layer.stage_times())
+    layer.enable_timing(False)
+    ep_stage = {kk: max_over_ranks(float(np.median([p_[kk] for p_ in per])), world) for kk in per[0]}
     # e2e: pinned host tokens in, host output out, copies inside the timed region
     xh = x.cpu().pin_memory()
     oh = torch.empty_like(xh).pin_memory()
@@ -399,7 +435,7 @@ def run_ep(args, world, rank, local):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / Ke, world)
     check(stream)
     if rank != 0:
-        (layer if p2p else be).close()
+        layer.close()
         return
     ms = elapsed / K
     El = E // world
@@ -408,13 +444,14 @@ def run_ep(args, world, rank, local):
     xbytes = 2 * sent_off * TD * 2  # token rows out + expert outputs back, off-GPU
     transport = ("NVLink peer memory: count publish + gather fused with the payload all-to-all + "
                  "return fused with the combine, one CUDA graph per step" if p2p else
-                 "NCCL all-to-all over NVLink, count exchange + host sync + payload")
+                 "NCCL (C ABI): count all-gather + host sync + grouped send/recv of the rows and back")
     line = {
-        "metric": "MoE-layer tokens/s (dynamic gating)", "value": world * S / (ms * 1e-3), "unit": "tokens/s",
+        "metric": "MoE-layer tokens/s (dynamic gating)", "value": S_total / (ms * 1e-3), "unit": "tokens/s",
         "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms, "p50_ms": p50,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (counter-hash uniform tokens; random-init experts, std 1/sqrt(fan-in))",
-        "config": {"workload": desc + " -- expert parallel", "S_per_gpu": S, "TD": TD, "HD": HD, "E": E,
+        "config": {"workload": desc + " -- expert parallel" + (", one batch split over the GPUs" if strong else ""),
+                   "S_total": S_total, "S_per_gpu": S, "TD": TD, "HD": HD, "E": E,
                    "top_k": k, "gating": mode, "experts_per_gpu": El, "placement": args.placement,
                    "parallelism": f"ep{world} ({transport})",
                    "ep_transport": ("p2p" if p2p else "nccl") + (f" -- {transport_note}" if transport_note else ""),
@@ -431,20 +468,25 @@ def run_ep(args, world, rank, local):
                 **({"dispatch_ms": ep_stage["dispatch"], "combine_ms": ep_stage["combine"],
                     "dispatch_gbs_offrank": sent_off * TD * 2 / (ep_stage["dispatch"] * 1e-3) / 1e9,
                     "combine_gbs_offrank": sent_off * TD * 2 / (ep_stage["combine"] * 1e-3) / 1e9,
-                    "note": "dispatch / combine kernel times include the wait for the slowest peer"}
+                    "note": ("dispatch / combine kernel times include the wait for the slowest peer" if p2p else
+                             "nccl: dispatch = gather + payload send/recv, combine = weighted combine; "
+                             "the return send/recv is in stage 'done'")}
                    if ep_stage else {})},
         "stage_ms": ep_stage,
+        "balance": balance,
         "gpu_launches": n_launch * K,
-        "e2e": {"value": world * S / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
-                "h2d_bytes_per_step": S * TD * 2, "d2h_bytes_per_step": S * TD * 2,
+        "e2e": {"value": S_total / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": S_total * TD * 2, "d2h_bytes_per_step": S_total * TD * 2,
+                "bytes_note": "whole job: every rank uploads its tokens and reads back its outputs",
                 "api": ("PeerExpertParallelMoE.forward (moe_ep_forward_graph)" if p2p else
-                        "ExpertParallelMoE.forward over the C ABI") + " (pinned host in/out)"},
+                        "PeerExpertParallelMoE(transport='nccl').forward (moe_ep_forward, NCCL)")
+                       + " (pinned host in/out)"},
         "cpu_baseline": None,
         "clocks": sampler.summary() if sampler else None,
         "gpu": torch.cuda.get_device_name(local),
     }
     print(json.dumps(line), flush=True)
-    (layer if p2p else be).close()
+    layer.close()
 
 
 def run_cache(args):
@@ -771,8 +813,31 @@ def main():
     ap.add_argument("--split-ffn", action="store_true", help="GEMM1/GEMM2 as two launches (A/B)")
     ap.add_argument("--fuse-front", action="store_true", help="gate+dispatch+gather in one launch (A/B)")
     ap.add_argument("--no-graph", action="store_true", help="timed steps as eager launches")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak = S tokens per GPU; strong = S tokens in total, split over the GPUs "
+                         "(configs[3]: the LM batch of 16384 tokens across 2/4/8 GPUs)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch / rendezvous check only: every rank prints its world and rank, no GPU work")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.impl != "reference" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `bench.py --gpus N` outside torchrun: relaunch as N ranks (one process per GPU)
+        import socket
+
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl != "reference" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        print(json.dumps({"dry_run": True, "impl": args.impl, "n_gpus": args.gpus, "world": world,
+                          "rank": int(os.environ.get("RANK", "0")), "scaling": args.scaling}), flush=True)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

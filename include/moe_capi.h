@@ -380,7 +380,11 @@ typedef struct moe_ep_desc {
   int num_experts;   /* global E <= 512 */
   int top_k;         /* k <= 8 */
   int max_recv_rows; /* receive capacity; 0 = world_size * max_tokens * top_k (worst case) */
+  int transport;     /* MOE_EP_TRANSPORT_P2P (0, default) or MOE_EP_TRANSPORT_NCCL */
 } moe_ep_desc;
+
+#define MOE_EP_TRANSPORT_P2P 0  /* NVLink peer memory (CUDA IPC windows), moe_ep_connect */
+#define MOE_EP_TRANSPORT_NCCL 1 /* NCCL count all-gather + grouped send/recv, moe_ep_connect_nccl */
 
 /* Wg [E, TD] (all experts, replicated), W1_local [E/D, HD, TD], W2_local
  * [E/D, TD, HD]: this rank's experts in increasing global id (bf16, device;
@@ -394,6 +398,21 @@ int moe_ep_destroy(moe_ep* ep);
 int moe_ep_get_handle(moe_ep* ep, void* handle);
 /* handles: world_size * MOE_EP_HANDLE_BYTES, in rank order. */
 int moe_ep_connect(moe_ep* ep, const void* handles);
+/* NCCL transport (desc.transport = MOE_EP_TRANSPORT_NCCL), north_star's
+ * "variable-count token all-to-all uses NCCL over NVLink, preceded by a count
+ * exchange": per forward an ncclAllGather of the per-key slot counts (the
+ * size phase, exchange.cpp:100-104), one host sync, then grouped
+ * ncclSend/ncclRecv of exactly the assigned token rows and gate weights (the
+ * payload phase, exchange.cpp:106-114), the same fused FFN, and the reverse
+ * send/recv before the weighted combine.  Setup: rank 0 calls
+ * moe_nccl_get_unique_id, the MOE_NCCL_ID_BYTES bytes reach every rank over
+ * any host transport, then every rank calls moe_ep_connect_nccl (collective)
+ * instead of moe_ep_connect.  NCCL is loaded at run time (libnccl.so.2);
+ * without it these calls return MOE_ERR_UNSUPPORTED.  Forwards have a host
+ * sync, so moe_ep_forward_graph runs them eagerly. */
+#define MOE_NCCL_ID_BYTES 128
+int moe_nccl_get_unique_id(void* id);
+int moe_ep_connect_nccl(moe_ep* ep, const void* nccl_id);
 /* X [S, TD] bf16 (this rank's tokens) -> out [S, TD] bf16. */
 int moe_ep_forward(moe_ep* ep, const void* X, int S, void* out, void* stream);
 int moe_ep_forward_graph(moe_ep* ep, const void* X, int S, void* out, void* stream);

@@ -21,6 +21,9 @@ MOE_ERR_EXPERT_RANGE = 5
 MOE_ERR_PEER_TIMEOUT = 6
 MOE_EP_MAX_RANKS = 8
 MOE_EP_HANDLE_BYTES = 64
+MOE_NCCL_ID_BYTES = 128
+MOE_EP_TRANSPORT_P2P = 0
+MOE_EP_TRANSPORT_NCCL = 1
 MOE_EP_NUM_STAGES = 7
 EP_STAGES = ["gate_route", "publish", "dispatch", "recv", "ffn", "done", "combine"]
 
@@ -44,7 +47,7 @@ EXPORTED = [
     "moe_layer_forward_host_batches", "moe_layer_repack",
     "moe_ep_create", "moe_ep_destroy", "moe_ep_get_handle", "moe_ep_connect", "moe_ep_forward",
     "moe_ep_forward_graph", "moe_ep_check_errors", "moe_ep_get_view", "moe_ep_enable_timing",
-    "moe_ep_stage_times", "moe_cache_policy_access",
+    "moe_ep_stage_times", "moe_cache_policy_access", "moe_nccl_get_unique_id", "moe_ep_connect_nccl",
 ]
 
 
@@ -89,7 +92,7 @@ class LayerView(C.Structure):
 class EpDesc(C.Structure):
     _fields_ = [("rank", C.c_int), ("world_size", C.c_int), ("max_tokens", C.c_int),
                 ("token_dim", C.c_int), ("hidden_dim", C.c_int), ("num_experts", C.c_int),
-                ("top_k", C.c_int), ("max_recv_rows", C.c_int)]
+                ("top_k", C.c_int), ("max_recv_rows", C.c_int), ("transport", C.c_int)]
 
 
 class EpView(C.Structure):
@@ -172,6 +175,8 @@ def load(path: str = LIB_PATH):
     _sig(lib.moe_ep_get_view, I, P, C.POINTER(EpView))
     _sig(lib.moe_ep_enable_timing, I, P, I)
     _sig(lib.moe_ep_stage_times, I, P, P)
+    _sig(lib.moe_nccl_get_unique_id, I, P)
+    _sig(lib.moe_ep_connect_nccl, I, P, P)
     _lib = lib
     return lib
 

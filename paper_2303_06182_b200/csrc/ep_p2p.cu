@@ -38,33 +38,12 @@
 // peer's done(e), which follows that peer's dispatch(e)/recv(e)/FFN(e) in its
 // stream; and a peer's FFN(e+1) overwrites recv_y only after recv(e+1), i.e.
 // after every sender finished combine(e).
-#include "capi_state.h"
+#include "ep_state.h"
 
 #include <algorithm>
 
 namespace moe {
 namespace {
-
-constexpr int kMaxRanks = MOE_EP_MAX_RANKS;
-constexpr int kRowBits = 28;
-
-struct EpHdr {
-  unsigned long long sig_counts[kMaxRanks];
-  unsigned long long sig_data;
-  unsigned long long pad0[7];
-  unsigned long long sig_ydone[kMaxRanks];
-  unsigned long long epoch;  // local step counter (only the owner touches it)
-  unsigned long long pad1[7];
-};
-static_assert(sizeof(EpHdr) <= 512, "header");
-
-struct EpLayout {
-  size_t counts_all, arrived, recv_w, recv_x, recv_y, total;
-};
-
-struct EpPeers {
-  char* base[kMaxRanks];
-};
 
 __device__ __forceinline__ EpHdr* hdr(char* base) { return reinterpret_cast<EpHdr*>(base); }
 
@@ -322,31 +301,32 @@ __global__ void __launch_bounds__(512) ep_recv_kernel(EpRecvArgs a) {
     const volatile int32_t* call = reinterpret_cast<const int32_t*>(a.mine + a.lay.counts_all);
     for (int s = 0; s < a.D; ++s) n += call[s * a.E + a.rank * a.El + q];
   }
-  const int ni = (n + a.tile_n - 1) / a.tile_n;
   if (q < a.El) {
     s_rows[q] = n;
-    s_items[q] = ni;
     if (a.expect) a.expect[q] = n;
   }
   __syncthreads();
   segmented_scan(s_rows, a.El, a.El);
+  // Rows past the receive capacity were never stored (the sender flagged
+  // them and dropped them from its combine): the work list covers exactly the
+  // rows that fit, so every row that did arrive is still computed.
+  int fit = 0;
+  if (q < a.El) fit = max(0, min(n, a.max_recv - (s_rows[q] - n)));
+  const int ni = (fit + a.tile_n - 1) / a.tile_n;
+  if (q < a.El) s_items[q] = ni;
+  __syncthreads();
   segmented_scan(s_items, a.El, a.El);
   if (q < a.El && ni) {
     const int row0 = s_rows[q] - n;
     const int it0 = s_items[q] - ni;
     for (int j = 0; j < ni; ++j) {
       const int r = row0 + j * a.tile_n;
-      a.items[it0 + j] = FfnItem{q, r, min(a.tile_n, n - j * a.tile_n), 0};
+      a.items[it0 + j] = FfnItem{q, r, min(a.tile_n, fit - j * a.tile_n), 0};
     }
   }
   if (q == 0) {
-    const int total_rows = s_rows[a.El - 1];
-    if (total_rows > a.max_recv) {
-      atomicExch(a.err + 1, 1);
-      *a.n_items = 0;  // rows past the capacity were never written
-    } else {
-      *a.n_items = s_ok ? s_items[a.El - 1] : 0;
-    }
+    if (s_rows[a.El - 1] > a.max_recv) atomicExch(a.err + 1, 1);
+    *a.n_items = s_ok ? s_items[a.El - 1] : 0;
   }
 }
 
@@ -357,6 +337,7 @@ __global__ void ep_done_kernel(EpPeers peers, EpLayout lay, int rank, int D, int
   // counts before any sender may start the next step (it waits for this flag)
   unsigned* arrived = reinterpret_cast<unsigned*>(peers.base[rank] + lay.arrived);
   for (int i = threadIdx.x; i < El; i += blockDim.x) arrived[i] = 0;
+  __syncwarp();  // every lane's reset is ordered before the releases below
   __threadfence_system();
   if (threadIdx.x < D) st_release_sys(&hdr(peers.base[threadIdx.x])->sig_ydone[rank], e);
 }
@@ -446,48 +427,70 @@ size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 }  // namespace
 }  // namespace moe
 
-struct moe_ep {
-  moe_ctx* ctx = nullptr;
-  moe_ep_desc d{};
-  int El = 0;
-  int tile_n = 128;
-  int max_recv = 0;
-  int items_max = 0;
-  moe::EpLayout lay{};
-  char* window = nullptr;
-  moe::EpPeers peers{};
-  bool opened[MOE_EP_MAX_RANKS] = {};
-  bool connected = false;
-  const void* Wg = nullptr;
-  CUtensorMap tmWg, tmX, tmW1p, tmW2p;
-  const void* tmX_ptr = nullptr;
-  int tmX_rows = 0;
-  moe::RowMaps xpm, hm;
-  DevBuf<int32_t> key_map, idx, counts, splits, order, pos, dest, n_items, done, err;
-  DevBuf<float> w, wpos;
-  DevBuf<FfnItem> items;
-  DevBuf<__nv_bfloat16> h, w1p, w2p;
-  unsigned long long timeout_ns = 20ull * 1000 * 1000 * 1000;
-  // CTAs of the dispatch kernel: every rank must use the same count (the
-  // receivers wait for D * dispatch_ctas arrivals); MOE_EP_DISPATCH_CTAS
-  int dispatch_ctas = 256;
-  int full_fence = 0;
-  // MOE_EP_OVERLAP=1: expert-ordered dispatch with per-expert arrival counts,
-  // GEMM1 tiles wait only for their expert's rows (the FFN starts while later
-  // rows are in flight).  Off by default: at world size 1 the per-row
-  // system-scope release costs 41 -> 140 us in the dispatch and the per-tile
-  // readiness check +15-19 us in the FFN, and the gain (hiding the
-  // all-to-all behind the FFN at D > 1) could not be measured on one GPU.
-  int overlap = 0;
-  DevBuf<int32_t> expect;
-  cudaEvent_t tev[MOE_EP_NUM_STAGES + 1] = {};  // per-stage timing (eager forwards)
-  bool timing = false;
-  cudaGraphExec_t graph = nullptr;
-  const void* g_x = nullptr;
-  void* g_out = nullptr;
-  int g_S = -1;
-  cudaStream_t g_stream = nullptr;
-};
+
+// Receive side of both transports: FFN work list (items over the received
+// rows, grouped by local expert) from the count matrix in the window, and the
+// fused FFN's counters zeroed.  wait_for_arrivals: spin until every sender's
+// dispatch CTAs arrived (peer-memory transport); the NCCL transport's rows
+// are in place when its receive completes in stream order.
+int ep_launch_recv(moe_ep* P, cudaStream_t s, bool wait_for_arrivals) {
+  const moe_ep_desc& d = P->d;
+  const int D = d.world_size, E = d.num_experts;
+  EpRecvArgs ra{};
+  ra.mine = P->window;
+  ra.lay = P->lay;
+  ra.rank = d.rank;
+  ra.D = D;
+  ra.E = E;
+  ra.El = P->El;
+  ra.tile_n = P->tile_n;
+  ra.max_recv = P->max_recv;
+  ra.dispatch_ctas = P->dispatch_ctas;
+  ra.overlap = wait_for_arrivals ? 0 : 1;
+  ra.expect = P->overlap ? P->expect.p : nullptr;
+  ra.items = P->items.p;
+  ra.n_items = P->n_items.p;
+  ra.done = P->done.p;
+  ra.done_n = 2 * P->items_max + 1;
+  ra.err = P->err.p;
+  ra.timeout_ns = P->timeout_ns;
+  cudaError_t ce = launch_chain(ep_recv_kernel, dim3(1), dim3(512), 0, s, false, ra);
+  if (ce != cudaSuccess) return cuda_fail(ce, "EP receive launch");
+  return MOE_OK;
+}
+
+// The fused tcgen05 FFN over the received rows (recv_x -> recv_y, gate weight
+// applied in the GEMM2 epilogue).
+int ep_launch_ffn(moe_ep* P, cudaStream_t s) {
+  const moe_ep_desc& d = P->d;
+  const int D = d.world_size, E = d.num_experts, TD = d.token_dim, HD = d.hidden_dim;
+  FusedFfnArgs fa{};
+  fa.items = P->items.p;
+  fa.n_items = P->n_items.p;
+  fa.TD = TD;
+  fa.HD = HD;
+  fa.H = P->h.p;
+  fa.Yw = reinterpret_cast<__nv_bfloat16*>(P->window + P->lay.recv_y);
+  fa.wpos = reinterpret_cast<const float*>(P->window + P->lay.recv_w);
+  fa.done1 = P->done.p;
+  fa.done2 = P->done.p + P->items_max;
+  fa.tile_ctr = P->done.p + 2 * P->items_max;
+  if (P->overlap && !P->nccl_comm) {  // GEMM1 tiles wait for their expert's rows, not for every row
+    fa.arrived = reinterpret_cast<const unsigned*>(P->window + P->lay.arrived);
+    fa.arrived_expect = P->expect.p;
+    fa.arrive_err = P->err.p;
+    fa.arrive_timeout_ns = P->timeout_ns;
+  }
+  const int per_item = HD / 128 + TD / 128;
+  fa.lag = std::max(2, (8 * P->ctx->sms + per_item - 1) / per_item);
+  fa.discard_h = 1;
+  fa.packed = 1;
+  fa.pair_hint = auto_pair((double)D * d.max_tokens * d.top_k / E, P->El, TD, HD, P->tile_n,
+                           P->ctx->sms);
+  cudaError_t ce = launch_fused_ffn(P->tmW1p, P->xpm, P->tmW2p, P->hm, fa, P->tile_n, P->ctx->sms, s);
+  if (ce != cudaSuccess) return cuda_fail(ce, "EP fused ffn launch");
+  return MOE_OK;
+}
 
 extern "C" {
 
@@ -589,6 +592,9 @@ int moe_ep_create(moe_ctx* ctx, const moe_ep_desc* desc, const void* Wg, const v
   if (const char* v = getenv("MOE_EP_FENCE")) P->full_fence = atoi(v);
   if (const char* v = getenv("MOE_EP_OVERLAP")) P->overlap = atoi(v);
   if ((st = P->expect.reserve(El))) return bail(st);
+  if (d.transport != MOE_EP_TRANSPORT_P2P && d.transport != MOE_EP_TRANSPORT_NCCL)
+    return bail(fail(MOE_ERR_INVALID_ARGUMENT, "unknown EP transport"));
+  if (d.transport == MOE_EP_TRANSPORT_NCCL) P->overlap = 0;  // arrivals are whole NCCL messages
   *out = P;
   return MOE_OK;
 }
@@ -601,6 +607,7 @@ int moe_ep_destroy(moe_ep* P) {
     if (e) cudaEventDestroy(e);
   for (int r = 0; r < MOE_EP_MAX_RANKS; ++r)
     if (P->opened[r]) cudaIpcCloseMemHandle(P->peers.base[r]);
+  ep_nccl_release(P);
   if (P->window) cudaFree(P->window);
   P->key_map.release();
   P->idx.release();
@@ -637,6 +644,8 @@ int moe_ep_get_handle(moe_ep* P, void* handle) {
 int moe_ep_connect(moe_ep* P, const void* handles) {
   if (!P || !handles) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   if (P->connected) return fail(MOE_ERR_INVALID_ARGUMENT, "already connected");
+  if (P->d.transport != MOE_EP_TRANSPORT_P2P)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "NCCL-transport layer: use moe_ep_connect_nccl");
   cudaSetDevice(P->ctx->device);
   const char* hb = static_cast<const char*>(handles);
   for (int r = 0; r < P->d.world_size; ++r) {
@@ -666,7 +675,8 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   if (!P->connected) return fail(MOE_ERR_INVALID_ARGUMENT, "moe_ep_connect has not been called");
   if (S < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "empty batch");
   if (S > d.max_tokens) return fail(MOE_ERR_INVALID_ARGUMENT, "S exceeds max_tokens");
-  const int k = d.top_k, E = d.num_experts, TD = d.token_dim, HD = d.hidden_dim, D = d.world_size;
+  if (P->nccl_comm) return ep_forward_nccl(P, X, S, out, s, timed);
+  const int k = d.top_k, E = d.num_experts, TD = d.token_dim, D = d.world_size;
   int st;
   if (X != P->tmX_ptr || S != P->tmX_rows) {
     if ((st = encode_bf16(&P->tmX, X, (uint64_t)S, TD, 128, moe::gate_box_cols(P->d.num_experts)))) return st;
@@ -711,54 +721,11 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   ce = launch_chain(ep_dispatch_kernel, dim3(P->dispatch_ctas), dim3(512), 0, s, false, da);
   if (ce != cudaSuccess) return cuda_fail(ce, "EP dispatch launch");
   // 4. receive side: work list from the count matrix
-  EpRecvArgs ra{};
-  ra.mine = P->window;
-  ra.lay = P->lay;
-  ra.rank = d.rank;
-  ra.D = D;
-  ra.E = E;
-  ra.El = P->El;
-  ra.tile_n = P->tile_n;
-  ra.max_recv = P->max_recv;
-  ra.dispatch_ctas = P->dispatch_ctas;
-  ra.overlap = P->overlap;
-  ra.expect = P->overlap ? P->expect.p : nullptr;
-  ra.items = P->items.p;
-  ra.n_items = P->n_items.p;
-  ra.done = P->done.p;
-  ra.done_n = 2 * P->items_max + 1;
-  ra.err = P->err.p;
-  ra.timeout_ns = P->timeout_ns;
   mark(3);
-  ce = launch_chain(ep_recv_kernel, dim3(1), dim3(512), 0, s, false, ra);
-  if (ce != cudaSuccess) return cuda_fail(ce, "EP receive launch");
+  if ((st = ep_launch_recv(P, s, !P->overlap))) return st;
   // 5. the fused FFN over the received rows (gate weight applied in GEMM2)
-  FusedFfnArgs fa{};
-  fa.items = P->items.p;
-  fa.n_items = P->n_items.p;
-  fa.TD = TD;
-  fa.HD = HD;
-  fa.H = P->h.p;
-  fa.Yw = reinterpret_cast<__nv_bfloat16*>(P->window + P->lay.recv_y);
-  fa.wpos = reinterpret_cast<const float*>(P->window + P->lay.recv_w);
-  fa.done1 = P->done.p;
-  fa.done2 = P->done.p + P->items_max;
-  fa.tile_ctr = P->done.p + 2 * P->items_max;
-  if (P->overlap) {  // GEMM1 tiles wait for their expert's rows, not for every row
-    fa.arrived = reinterpret_cast<const unsigned*>(P->window + P->lay.arrived);
-    fa.arrived_expect = P->expect.p;
-    fa.arrive_err = P->err.p;
-    fa.arrive_timeout_ns = P->timeout_ns;
-  }
-  const int per_item = HD / 128 + TD / 128;
-  fa.lag = std::max(2, (8 * P->ctx->sms + per_item - 1) / per_item);
-  fa.discard_h = 1;
-  fa.packed = 1;
-  fa.pair_hint = auto_pair((double)D * d.max_tokens * d.top_k / E, P->El, TD, HD, P->tile_n,
-                           P->ctx->sms);
   mark(4);
-  ce = launch_fused_ffn(P->tmW1p, P->xpm, P->tmW2p, P->hm, fa, P->tile_n, P->ctx->sms, s);
-  if (ce != cudaSuccess) return cuda_fail(ce, "EP fused ffn launch");
+  if ((st = ep_launch_ffn(P, s))) return st;
   // 6. outputs ready -> every peer
   mark(5);
   ce = launch_chain(ep_done_kernel, dim3(1), dim3(32), 0, s, false, P->peers, P->lay, d.rank, D,
@@ -816,6 +783,7 @@ int moe_ep_forward_graph(moe_ep* P, const void* X, int S, void* out, void* strea
   if (!P || !X || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
   cudaSetDevice(P->ctx->device);
+  if (P->nccl_comm) return ep_forward_impl(P, X, S, out, s);  // host sync inside: not capturable
   if (!(P->graph && P->g_x == X && P->g_out == out && P->g_S == S && P->g_stream == s)) {
     if (s == nullptr) return fail(MOE_ERR_INVALID_ARGUMENT, "graph capture needs a non-default stream");
     if (P->graph) cudaGraphExecDestroy(P->graph);

@@ -284,27 +284,49 @@ class PeerExpertParallelMoE:
 
     ``torch.distributed`` is used only at construction to exchange the
     64-byte CUDA IPC handles of the ranks' windows (any backend).
+
+    ``transport="nccl"`` selects the C ABI's NCCL transport instead
+    (csrc/ep_nccl.cu): count all-gather + one host sync + grouped
+    ncclSend/ncclRecv of the rows, same routing, FFN and combine; the NCCL
+    communicator is created inside the library from a unique id that rank 0
+    broadcasts over torch.distributed.
     """
 
     def __init__(self, ctx, placement: Placement, shape, Wg, W1_local, W2_local, max_tokens: int,
-                 rank: int, group=None, max_recv_rows: int = 0):
+                 rank: int, group=None, max_recv_rows: int = 0, transport: str = "p2p"):
         placement.validate()
         self.ctx, self.lib = ctx, ctx.lib
         self.placement, self.shape, self.rank = placement, shape, rank
         self.D = placement.num_devices
         self.max_tokens = max_tokens
+        if transport not in ("p2p", "nccl"):
+            raise ValueError("transport must be 'p2p' or 'nccl'")
+        self.transport = transport
         d = _capi.EpDesc(rank, self.D, max_tokens, shape.token_dim, shape.hidden_dim,
-                         shape.num_experts, shape.top_k, max_recv_rows)
+                         shape.num_experts, shape.top_k, max_recv_rows,
+                         _capi.MOE_EP_TRANSPORT_NCCL if transport == "nccl" else _capi.MOE_EP_TRANSPORT_P2P)
         dev_of = np.ascontiguousarray(placement.device_of, dtype=np.int32)
         h = C.c_void_p()
         check(self.lib.moe_ep_create(ctx.h, C.byref(d), _p(Wg), _p(W1_local), _p(W2_local),
                                      dev_of.ctypes.data_as(C.c_void_p), C.byref(h)))
         self.h = h
         self.Wg = Wg  # the gate's TMA descriptor holds Wg's raw pointer
+        self.group = group
+        if transport == "nccl":
+            # the C ABI owns the NCCL communicator; torch.distributed only
+            # carries the 128-byte unique id from rank 0
+            uid = C.create_string_buffer(_capi.MOE_NCCL_ID_BYTES)
+            if rank == 0:
+                check(self.lib.moe_nccl_get_unique_id(uid))
+            if self.D > 1:
+                obj = [bytes(uid.raw)]
+                dist.broadcast_object_list(obj, src=0, group=group)
+                uid = C.create_string_buffer(obj[0], _capi.MOE_NCCL_ID_BYTES)
+            check(self.lib.moe_ep_connect_nccl(self.h, uid))
+            return
         buf = C.create_string_buffer(_capi.MOE_EP_HANDLE_BYTES)
         check(self.lib.moe_ep_get_handle(self.h, buf))
         mine = bytes(buf.raw)
-        self.group = group
         if self.D > 1:
             handles = [None] * self.D
             dist.all_gather_object(handles, mine, group=group)
@@ -358,6 +380,7 @@ class PeerExpertParallelMoE:
         ca = _from_ptr(v.counts_all, self.D * E, torch.int32, dev).view(self.D, E)
         El = E // self.D
         R = int(ca[:, self.rank * El:(self.rank + 1) * El].sum())
+        R_stored = min(R, int(v.max_recv_rows))  # rows past the receive capacity were never stored
         out = {
             "idx": _from_ptr(v.idx, S * k, torch.int32, dev).view(S, k),
             "w": _from_ptr(v.w, S * k, torch.float32, dev).view(S, k),
@@ -368,10 +391,10 @@ class PeerExpertParallelMoE:
             "n_items": int(_from_ptr(v.n_items, 1, torch.int32, dev)[0]),
             "recv_rows": R,
         }
-        if R:
-            out["recv_x"] = _from_ptr(v.recv_x, R * TD, torch.bfloat16, dev).view(R, TD)
-            out["recv_y"] = _from_ptr(v.recv_y, R * TD, torch.bfloat16, dev).view(R, TD)
-            out["recv_w"] = _from_ptr(v.recv_w, R, torch.float32, dev)
+        if R_stored:
+            out["recv_x"] = _from_ptr(v.recv_x, R_stored * TD, torch.bfloat16, dev).view(R_stored, TD)
+            out["recv_y"] = _from_ptr(v.recv_y, R_stored * TD, torch.bfloat16, dev).view(R_stored, TD)
+            out["recv_w"] = _from_ptr(v.recv_w, R_stored, torch.float32, dev)
         return out
 
     def close(self):

@@ -46,3 +46,23 @@ def test_reference_arm_under_torchrun_prints_once():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["impl"] == "reference"
+
+
+@pytest.mark.timeout(200)
+@pytest.mark.parametrize("scaling", ["weak", "strong"])
+def test_gpus_flag_relaunches_one_rank_per_gpu(scaling):
+    """`bench.py --gpus 2` outside torchrun relaunches itself as 2 ranks (the
+    form the driver may use); --dry-run stops before any GPU work."""
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--dry-run", "--scaling", scaling],
+                       cwd=ROOT, capture_output=True, text=True, timeout=180)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert sorted(d["rank"] for d in lines) == [0, 1]
+    assert all(d["world"] == 2 and d["n_gpus"] == 2 and d["scaling"] == scaling for d in lines)
+
+
+def test_gpus_flag_must_match_world_size():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--dry-run"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=120, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE=1" in (r.stderr + r.stdout)

@@ -46,7 +46,7 @@ def _single_gpu_reference(S, TD, HD, E, k):
     return out
 
 
-def _build(rank, world, S, TD, HD, E, k, placement, max_recv_rows=0):
+def _build(rank, world, S, TD, HD, E, k, placement, max_recv_rows=0, transport="p2p"):
     from paper_2303_06182_b200.ep import PeerExpertParallelMoE
     from paper_2303_06182_b200.layer import Context, LayerShape, make_tokens, make_weights
 
@@ -58,7 +58,7 @@ def _build(rank, world, S, TD, HD, E, k, placement, max_recv_rows=0):
     mine = torch.arange(rank, S, world, device="cuda")  # token t lives on t % D (exchange.cpp:35-37)
     xl = x[mine].contiguous()
     ep = PeerExpertParallelMoE(ctx, placement, shape, Wg, W1[loc].contiguous(), W2[loc].contiguous(),
-                               xl.shape[0], rank, max_recv_rows=max_recv_rows)
+                               xl.shape[0], rank, max_recv_rows=max_recv_rows, transport=transport)
     return ep, x, xl, mine
 
 
@@ -100,6 +100,76 @@ def test_peer_ep_capacity_overflow_is_reported():
     ep.forward(xl)
     with pytest.raises(MoeError, match="receive capacity"):
         ep.check_errors()
+    ep.close()
+
+
+@pytest.mark.parametrize("S,TD,HD,E,k", [(1024, 256, 512, 16, 2), (333, 256, 512, 12, 3),
+                                         (16384, 1024, 4096, 512, 2)])
+def test_nccl_ep_one_rank_bitwise_equals_layer(S, TD, HD, E, k):
+    """The C ABI's NCCL transport (csrc/ep_nccl.cu: count all-gather, host
+    sync, grouped ncclSend/ncclRecv of the rows and weights, regroup by local
+    expert, fused FFN, reverse send/recv, combine) at world size 1 -- the
+    rank's sends go to itself through NCCL -- reproduces the single-GPU layer
+    bit for bit, eagerly and through the graph entry point (which runs NCCL
+    forwards eagerly)."""
+    from paper_2303_06182_b200.ep import Placement
+
+    ref_bits, ref_idx = _single_gpu_reference(S, TD, HD, E, k)
+    ep, x, xl, mine = _build(0, 1, S, TD, HD, E, k, Placement.contiguous(E, 1), transport="nccl")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        outs = [ep.forward(xl, s).clone() for _ in range(2)]
+        outs.append(ep.forward(xl, s, graph=True).clone())
+        ep.enable_timing(True)
+        outs.append(ep.forward(xl, s).clone())
+        st = ep.stage_times()
+    s.synchronize()
+    ep.check_errors(s)
+    for o in outs:
+        assert (o.view(torch.int16).cpu().numpy() == ref_bits).all()
+    v = ep.view(S)
+    assert (v["idx"].cpu().numpy() == ref_idx).all()
+    assert v["recv_rows"] == S * k
+    assert all(t >= 0 for t in st.values()) and st["ffn"] > 0
+    ep.close()
+
+
+def test_nccl_ep_capacity_overflow_fails_the_forward():
+    from paper_2303_06182_b200._capi import MoeError
+    from paper_2303_06182_b200.ep import Placement
+
+    S, TD, HD, E, k = 512, 256, 512, 8, 2
+    ep, x, xl, mine = _build(0, 1, S, TD, HD, E, k, Placement.contiguous(E, 1), max_recv_rows=100,
+                             transport="nccl")
+    with pytest.raises(MoeError, match="receive capacity"):
+        ep.forward(xl)
+    ep.close()
+
+
+def test_peer_ep_overflow_still_computes_the_rows_that_fit():
+    """A receive capacity below the batch: the rows that fit are computed
+    (the work list is clamped, not dropped), the overflow is reported, and a
+    forward with enough capacity afterwards is exact."""
+    from paper_2303_06182_b200._capi import MoeError
+    from paper_2303_06182_b200.ep import Placement
+
+    S, TD, HD, E, k = 512, 256, 512, 8, 2
+    ref_bits, _ = _single_gpu_reference(S, TD, HD, E, k)
+    ep, x, xl, mine = _build(0, 1, S, TD, HD, E, k, Placement.contiguous(E, 1), max_recv_rows=600)
+    out = ep.forward(xl)
+    with pytest.raises(MoeError, match="receive capacity"):
+        ep.check_errors()
+    v = ep.view(S)
+    assert v["n_items"] > 0
+    ok = v["dest"].cpu().numpy() >= 0  # sorted rows that were stored
+    assert 0 < ok.sum() < S * k
+    # tokens whose every row was stored are exact
+    pos = np.empty(S * k, np.int64)
+    pos[v["order"].cpu().numpy()] = np.arange(S * k)
+    full = ok[pos.reshape(S, k)].all(axis=1)
+    assert full.any()
+    assert (out.view(torch.int16).cpu().numpy()[full] == ref_bits[full]).all()
     ep.close()
 
 
