@@ -505,25 +505,38 @@ def run_cache(args):
     S = args.tokens or S
     shape = LayerShape(TD, HD, E, k)
     w = make_weights(shape, seed=2303061820)
+    Wg = w[0]
     x = make_tokens(S, TD, seed=2303061821)
     K, W = args.steps, args.warmup
     ex, wt = skewed_routing(E, k, W + K, S, 1.2, 0.9, 0.75, seed=7)
     idx = torch.from_numpy(ex).cuda()
     gw = torch.from_numpy(wt.astype(np.float32)).cuda()
     slots = args.cache_slots or E // 4
-    full = MoeLayer(shape, S, weights=w)
     W1h, W2h = w[1].cpu().pin_memory(), w[2].cpu().pin_memory()
-    layer = MoeLayer(shape, S, weights=w)
-    cache = ExpertCache(layer, slots, "lifo", W1h, W2h)
     stream = torch.cuda.Stream()
     stream.wait_stream(torch.cuda.current_stream())  # inputs were written on the current stream
     out = torch.empty_like(x)
-
-    def timed(fn):
+    # measured host->device peak of this box: pinned 1 GiB copy, best of 5
+    hbuf = torch.empty(1 << 29, dtype=torch.bfloat16).pin_memory()
+    dbuf = torch.empty_like(hbuf, device="cuda")
+    best = 0.0
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            dbuf.copy_(hbuf, non_blocking=True)
+            e1.record(stream)
+        stream.synchronize()
+        best = max(best, hbuf.numel() * 2 / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    h2d_peak = best
+    del hbuf, dbuf
+    def timed(fn, after_warmup=None):
         with torch.cuda.stream(stream):
             for b in range(W):
                 fn(b)
         stream.synchronize()
+        if after_warmup:
+            after_warmup()
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
         with torch.cuda.stream(stream):
             for i in range(K):
@@ -533,9 +546,23 @@ def run_cache(args):
         stream.synchronize()
         return [evs[i].elapsed_time(evs[i + 1]) for i in range(K)]
 
+    # fully resident layer on the same batches (all E experts in HBM), then
+    # freed: the cached layer holds only the slot pool
+    full = MoeLayer(shape, S, weights=w)
     t_full = timed(lambda b: full.forward_routed(x, idx[b], gw[b], out, stream))
-    s0 = cache.stats()
-    t_cache = timed(lambda b: cache.forward_routed(x, idx[b], gw[b], out, stream))
+    full.close()
+    del full, w
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    used0 = torch.cuda.mem_get_info()[1] - torch.cuda.mem_get_info()[0]
+    layer = MoeLayer(shape, S, weights=(Wg, None, None), pool_only=True)
+    cache = ExpertCache(layer, slots, "lifo", W1h, W2h)
+    torch.cuda.synchronize()
+    used1 = torch.cuda.mem_get_info()[1] - torch.cuda.mem_get_info()[0]
+    stats0 = {}
+    t_cache = timed(lambda b: cache.forward_routed(x, idx[b], gw[b], out, stream),
+                    after_warmup=lambda: stats0.update(cache.stats()))  # timed steps only
+    s0 = stats0
     s1 = cache.stats()
     acc = s1["accesses"] - s0["accesses"]
     miss = s1["misses"] - s0["misses"]
@@ -552,7 +579,11 @@ def run_cache(args):
         "cache": {"accesses": acc, "misses": miss, "miss_rate": miss / max(acc, 1),
                   "active_per_step": acc / K, "h2d_gb_per_step": copied / K / 1e9,
                   "h2d_gbs_achieved": copied / (sum(t_cache) * 1e-3) / 1e9,
+                  "h2d_peak_gbs_measured": h2d_peak,
+                  "pcie_frac": copied / (sum(t_cache) * 1e-3) / 1e9 / h2d_peak,
+                  "copy_bound_ms_per_step": copied / K / (h2d_peak * 1e9) * 1e3,
                   "gpu_expert_memory_gb": slots * expert_bytes / 1e9,
+                  "device_memory_of_cached_layer_gb": (used1 - used0) / 1e9,
                   "resident_expert_memory_gb": E * expert_bytes / 1e9},
         "fully_resident": {"ms_per_step": float(np.mean(t_full)), "value": S / (np.mean(t_full) * 1e-3)},
         "gpu": torch.cuda.get_device_name(0),
@@ -585,9 +616,21 @@ def run_b200(args):
     shape = LayerShape(TD, HD, E, k)
     seed = 2303061820 + rank
     weights = make_weights(shape, seed=2303061820)
+    # expert weights held ONCE: the dynamic-gating layer streams them tile-packed
+    # in place (no second copy); static gating streams them row-major
+    in_place = mode == "dynamic" and not (args.split_ffn or args.fuse_combine)
+    torch.cuda.synchronize()
+    free0, total_mem = torch.cuda.mem_get_info()
     layer = MoeLayer(shape, S, mode=mode, capacity_factor=C if mode == "static" else 1.0, weights=weights,
                      tile_n=args.tile_n, fuse_combine=args.fuse_combine,
-                     split_ffn=args.split_ffn, fuse_front=args.fuse_front)
+                     split_ffn=args.split_ffn, fuse_front=args.fuse_front, pack_in_place=in_place)
+    del weights
+    torch.cuda.synchronize()
+    expert_bytes = E * 2 * TD * HD * 2
+    mem = {"expert_weight_bytes": expert_bytes,
+           "expert_weight_copies_in_hbm": 1 if (in_place or mode == "static") else 2,
+           "layer_extra_device_bytes": free0 - torch.cuda.mem_get_info()[0],
+           "device_used_gb": (total_mem - torch.cuda.mem_get_info()[0]) / 1e9}
     x = make_tokens(S, TD, seed=seed)
     out = torch.empty_like(x)
     stream = torch.cuda.Stream()
@@ -766,6 +809,7 @@ def run_b200(args):
         "layer_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms_per_step, "flops": F,
                            "bytes": B, "peaks": {"hbm_gbs": hbm_gbs, "bf16_tflops": tflops}},
         "stage_ms": {n: float(m) for n, m in zip(STAGES, mean_stage)},
+        "memory": mem,
         "timed_path": "CUDA graph replay of moe_layer_forward (PDL edges)" if use_graph else "eager launches",
         "gpu_launches": launches_per_step * K,
         "e2e": {"value": world * S / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,

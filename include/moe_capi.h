@@ -179,13 +179,37 @@ typedef struct moe_layer_desc {
                              tiles (+1x expert-weight memory; weights are
                              snapshotted at create, see moe_layer_repack);
                              1: stream the caller's row-major weights */
+  int weights_packed;     /* 1: W1/W2 are already in the tile-packed layout
+                             (moe_pack_expert_weights, e.g. packed in place):
+                             the FFN streams them directly and the layer keeps
+                             NO copy -- expert weights are held once.  Dynamic
+                             gating, fused FFN only (split_ffn / keep_layout 0) */
 } moe_layer_desc;
 
 /* Weights are caller-owned device buffers (bf16, row-major):
- *   Wg [E, TD], W1 [E, HD, TD] (H = relu(x W1_e^T)), W2 [E, TD, HD]. */
+ *   Wg [E, TD], W1 [E, HD, TD] (H = relu(x W1_e^T)), W2 [E, TD, HD].
+ * Expert-weight memory:
+ *   - default: the layer streams its own tile-packed copy; after create the
+ *     caller's W1/W2 are read again only by moe_layer_repack (or by the
+ *     split / keep_layout / static forms), so a caller that does not need
+ *     those may free them -- or avoid the copy altogether with
+ *   - weights_packed = 1: W1/W2 were packed by moe_pack_expert_weights
+ *     (in place is fine) and are streamed as they are: one copy in HBM;
+ *   - W1 = W2 = NULL: a pool-only layer for expert buffering (dynamic
+ *     gating): no expert weights on the device at all until moe_cache_create
+ *     attaches its slot pool; a forward without a cache fails. */
 int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, const void* W1,
                      const void* W2, moe_layer** out);
 int moe_layer_destroy(moe_layer* layer);
+
+/* Expert weights, row-major [rows, K] bf16 (rows = E * HD for W1 with K = TD,
+ * rows = E * TD for W2 with K = HD), -> the tile-packed layout the fused FFN
+ * streams (128 x 64 tiles, 16 KB contiguous; every expert's tiles stay inside
+ * its own row range).  dst == src packs IN PLACE (expert-block-wise through a
+ * 64 MB scratch); otherwise the buffers must not overlap.  rows % 128 == 0,
+ * K % 64 == 0.  Synchronous on `stream`. */
+int moe_pack_expert_weights(moe_ctx* ctx, const void* src, void* dst, int64_t rows, int K,
+                            void* stream);
 
 /* Refresh the layer's packed weight copy after the caller changed W1/W2 in
  * place (no-op when the layer streams the caller's weights). */

@@ -48,6 +48,7 @@ EXPORTED = [
     "moe_ep_create", "moe_ep_destroy", "moe_ep_get_handle", "moe_ep_connect", "moe_ep_forward",
     "moe_ep_forward_graph", "moe_ep_check_errors", "moe_ep_get_view", "moe_ep_enable_timing",
     "moe_ep_stage_times", "moe_cache_policy_access", "moe_nccl_get_unique_id", "moe_ep_connect_nccl",
+    "moe_pack_expert_weights",
 ]
 
 
@@ -70,7 +71,7 @@ class LayerDesc(C.Structure):
         ("num_experts", C.c_int), ("top_k", C.c_int), ("mode", C.c_int),
         ("capacity_factor", C.c_double), ("tile_n", C.c_int), ("keep_logits", C.c_int),
         ("fuse_combine", C.c_int), ("split_ffn", C.c_int),
-        ("fuse_front", C.c_int), ("keep_layout", C.c_int),
+        ("fuse_front", C.c_int), ("keep_layout", C.c_int), ("weights_packed", C.c_int),
     ]
 
 
@@ -144,6 +145,7 @@ def load(path: str = LIB_PATH):
     _sig(lib.moe_layer_forward_host, I, P, P, I, P, P)
     _sig(lib.moe_layer_forward_host_batches, I, P, P, P, P, I, P)
     _sig(lib.moe_layer_repack, I, P, P)
+    _sig(lib.moe_pack_expert_weights, I, P, P, P, I64, I, P)
     _sig(lib.moe_layer_get_view, I, P, C.POINTER(LayerView))
     _sig(lib.moe_layer_set_weight_pool, I, P, P, P, I, P)
     _sig(lib.moe_exchange_counts_host, I, P, P, I, I, I, P, I, I, P)

@@ -12,10 +12,10 @@
 // must not be overwritten before that wave finishes.  The batch is therefore
 // split into waves (contiguous expert-id ranges, hence contiguous rows and
 // FFN items): a wave closes right before a miss would evict one of its own
-// experts.  Per wave:
-//   copy stream:    wait(previous wave's FFN) -> H2D copies of its misses
-//   compute stream: wait(its copies) -> slot table H2D -> GEMM1/GEMM2 over
-//                   the items of its expert range
+// experts.  Copies run on a side stream with per-slot readiness: a copy
+// waits only for the FFN of the wave that last read its slot (none for free
+// slots and inactive victims, which are all issued up front); each wave's
+// FFN waits for its own copies.
 // The routing counts reach the host once per layer call (the host sync the
 // cache needs to know the active set, shared with the EP count exchange in
 // the paper's design).
@@ -211,21 +211,56 @@ int cache_forward(moe_cache* C, const void* X, int S, const int32_t* idx, const 
   int stats[4] = {0, 0, 0, 0};
   const std::vector<Wave> waves = plan_batch(C, active, stats);
   if ((st = ensure_events(C, waves.size()))) return st;
+  // Per-slot readiness: a copy into slot q must wait only for the FFN of the
+  // last wave of THIS batch that read q (earlier batches' FFNs finished
+  // before the host sync above).  Copies whose slot no wave of this batch has
+  // used yet (free slots, victims inactive in this batch) wait for nothing:
+  // they are all issued first, so they stream over PCIe while earlier waves
+  // compute; the dependent ones follow wave by wave.
+  std::vector<int> slot_wave((size_t)C->n_slots, -1), dep_of_load, wave_dep(waves.size(), -1);
+  std::vector<char> wave_has_dep(waves.size(), 0);
+  for (size_t wv = 0; wv < waves.size(); ++wv) {
+    for (auto& es : waves[wv].loads) {
+      const int dep = slot_wave[(size_t)es.second];
+      dep_of_load.push_back(dep);
+      if (dep >= 0) {
+        wave_has_dep[wv] = 1;
+        wave_dep[wv] = std::max(wave_dep[wv], dep);
+      }
+    }
+    for (auto& es : waves[wv].table) slot_wave[(size_t)es.second] = (int)wv;
+  }
+  auto copy_in = [&](const std::pair<int, int>& es) -> int {
+    const size_t e = (size_t)es.first, slot = (size_t)es.second;
+    MOE_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(C->pool1.p) + slot * C->w1_bytes,
+                             C->w1h + e * C->w1_bytes, C->w1_bytes, cudaMemcpyHostToDevice,
+                             C->copy_stream));
+    MOE_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(C->pool2.p) + slot * C->w2_bytes,
+                             C->w2h + e * C->w2_bytes, C->w2_bytes, cudaMemcpyHostToDevice,
+                             C->copy_stream));
+    C->copies_bytes += (int64_t)(C->w1_bytes + C->w2_bytes);
+    return MOE_OK;
+  };
+  // pass 1: every independent copy, in wave order
+  size_t li = 0;
+  for (size_t wv = 0; wv < waves.size(); ++wv) {
+    for (auto& es : waves[wv].loads)
+      if (dep_of_load[li++] < 0 && (st = copy_in(es))) return st;
+    if (!wave_has_dep[wv]) MOE_CUDA(cudaEventRecord(C->ev_copy[wv], C->copy_stream));
+  }
+  // pass 2: per wave, its dependent copies (after the FFN that last read their
+  // slots), then its FFN
+  li = 0;
   for (size_t wv = 0; wv < waves.size(); ++wv) {
     const Wave& W = waves[wv];
-    // copies: after the previous wave's FFN (its slots may be overwritten)
-    if (wv > 0) MOE_CUDA(cudaStreamWaitEvent(C->copy_stream, C->ev_ffn[wv - 1], 0));
-    for (auto& es : W.loads) {
-      const size_t e = (size_t)es.first, slot = (size_t)es.second;
-      MOE_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(C->pool1.p) + slot * C->w1_bytes,
-                               C->w1h + e * C->w1_bytes, C->w1_bytes, cudaMemcpyHostToDevice,
-                               C->copy_stream));
-      MOE_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(C->pool2.p) + slot * C->w2_bytes,
-                               C->w2h + e * C->w2_bytes, C->w2_bytes, cudaMemcpyHostToDevice,
-                               C->copy_stream));
-      C->copies_bytes += (int64_t)(C->w1_bytes + C->w2_bytes);
+    const size_t l0 = li;
+    li += W.loads.size();
+    if (wave_has_dep[wv]) {
+      MOE_CUDA(cudaStreamWaitEvent(C->copy_stream, C->ev_ffn[(size_t)wave_dep[wv]], 0));
+      for (size_t j = 0; j < W.loads.size(); ++j)
+        if (dep_of_load[l0 + j] >= 0 && (st = copy_in(W.loads[j]))) return st;
+      MOE_CUDA(cudaEventRecord(C->ev_copy[wv], C->copy_stream));
     }
-    MOE_CUDA(cudaEventRecord(C->ev_copy[wv], C->copy_stream));
     // compute: the wave's slot table, then its experts' FFN items
     int32_t* tab = C->slot_host[wv];
     for (auto& es : W.table) tab[es.first] = es.second;

@@ -89,6 +89,7 @@ int moe_ctx_destroy(moe_ctx* ctx) {
   ctx->block_hist.release();
   ctx->err_flag.release();
   ctx->drop_mark.release();
+  ctx->static_splits.release();
   delete ctx;
   return MOE_OK;
 }
@@ -230,11 +231,11 @@ int moe_route_static(moe_ctx* ctx, const int32_t* expert_idx, int S, int k, int 
     return fail(MOE_ERR_INVALID_ARGUMENT, "null buffer");
   st = ctx->prepare_route(E);
   if (st) return st;
-  // splits scratch lives in block_hist's tail-free area: use a small buffer
-  static thread_local DevBuf<int32_t> splits;
-  st = splits.reserve((size_t)E + 1);
+  // the splits are not an output of this entry point: context-owned scratch
+  // (on the context's device, released with it)
+  st = ctx->static_splits.reserve((size_t)E + 1);
   if (st) return st;
-  return route_common(ctx, expert_idx, S, k, E, capacity, counts, splits.p, slots, pos, nullptr,
+  return route_common(ctx, expert_idx, S, k, E, capacity, counts, ctx->static_splits.p, slots, pos, nullptr,
                       nullptr, dropped, n_dropped, nullptr, nullptr, 128, nullptr, 0,
                       (cudaStream_t)stream);
 }
@@ -458,7 +459,14 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
     return fail(MOE_ERR_INVALID_ARGUMENT, "unknown gating mode");
   if (d.mode == MOE_GATING_STATIC && d.capacity_factor <= 0.0)
     return fail(MOE_ERR_INVALID_ARGUMENT, "capacity factor must be positive in static mode");
-  if (!Wg || !W1 || !W2) return fail(MOE_ERR_INVALID_ARGUMENT, "null weight pointer");
+  if (!Wg) return fail(MOE_ERR_INVALID_ARGUMENT, "null gate weight pointer");
+  if (!W1 != !W2) return fail(MOE_ERR_INVALID_ARGUMENT, "W1 and W2 must both be given or both be NULL");
+  const bool pool_only = !W1;
+  if (pool_only && (d.mode != MOE_GATING_DYNAMIC || d.weights_packed))
+    return fail(MOE_ERR_INVALID_ARGUMENT, "a pool-only layer (no W1/W2) needs dynamic gating, row-major pools");
+  if (d.weights_packed && (d.mode != MOE_GATING_DYNAMIC || d.split_ffn || d.keep_layout || d.fuse_combine))
+    return fail(MOE_ERR_INVALID_ARGUMENT,
+                "pre-packed weights need dynamic gating and the fused FFN (split_ffn, keep_layout, fuse_combine 0)");
   MOE_CUDA(cudaSetDevice(ctx->device));
   cudaError_t ce = gate_prepare(d.num_experts);
   if (ce != cudaSuccess) return cuda_fail(ce, "gate_prepare");
@@ -525,8 +533,9 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
   cudaMemset(L->comb_cnt.p, 0, sizeof(int32_t) * (size_t)S * (d.token_dim / 128));
   cudaMemset(L->h.p, 0, Rp * HD * 2);
   if ((st = encode_bf16(&L->tmWg, Wg, E, TD, moe::gate_box_rows(E), moe::gate_box_cols(E, d.fuse_front))) ||
-      (st = encode_bf16(&L->tmW1, W1, (uint64_t)E * HD, TD, 128)) ||
-      (st = encode_bf16(&L->tmW2, W2, (uint64_t)E * TD, HD, 128)) ||
+      (!pool_only && !d.weights_packed &&
+       ((st = encode_bf16(&L->tmW1, W1, (uint64_t)E * HD, TD, 128)) ||
+        (st = encode_bf16(&L->tmW2, W2, (uint64_t)E * TD, HD, 128)))) ||
       (st = encode_bf16(&L->tmXp, L->xp.p, Rp, TD, 16)) ||
       (st = encode_bf16(&L->tmH, L->h.p, Rp, HD, 16)) ||
       (st = encode_rows(&L->xpm, L->xp.p, Rp, TD)) || (st = encode_rows(&L->hm, L->h.p, Rp, HD))) {
@@ -544,8 +553,18 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
     const char* v = getenv("MOE_PACK");
     return v ? atoi(v) : 1;
   }();
-  if (!d.keep_layout && pack_env && !d.split_ffn && !d.fuse_combine &&
-      d.mode == MOE_GATING_DYNAMIC && (L->tile_n == 128 || fused256_enabled())) {
+  L->no_weights = pool_only;
+  if (d.weights_packed) {
+    // the caller's buffers are the packed tiles: stream them, keep no copy
+    const size_t n1 = (size_t)E * HD * TD;
+    if ((st = encode_bf16(&L->tmW1p, W1, n1 / 64, 64, 128)) || (st = encode_bf16(&L->tmW2p, W2, n1 / 64, 64, 128))) {
+      moe_layer_destroy(L);
+      return st;
+    }
+    L->packed = true;
+    L->caller_packed = true;
+  } else if (!pool_only && !d.keep_layout && pack_env && !d.split_ffn && !d.fuse_combine &&
+             d.mode == MOE_GATING_DYNAMIC && (L->tile_n == 128 || fused256_enabled())) {
     const size_t n1 = (size_t)E * HD * TD;
     if (L->w1p.reserve(n1) == MOE_OK && L->w2p.reserve(n1) == MOE_OK &&
         encode_bf16(&L->tmW1p, L->w1p.p, n1 / 64, 64, 128) == MOE_OK &&
@@ -572,7 +591,7 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
 
 int moe_layer_repack(moe_layer* L, void* stream) {
   if (!L) return fail(MOE_ERR_INVALID_ARGUMENT, "null layer");
-  if (!L->packed) return MOE_OK;
+  if (!L->packed || L->caller_packed) return MOE_OK;  // nothing copied: nothing to refresh
   cudaSetDevice(L->ctx->device);
   const moe_layer_desc& d = L->d;
   cudaStream_t s = (cudaStream_t)stream;
@@ -583,6 +602,42 @@ int moe_layer_repack(moe_layer* L, void* stream) {
                           (long)d.num_experts * d.token_dim, d.hidden_dim, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(e, "weight prepack");
+  return MOE_OK;
+}
+
+int moe_pack_expert_weights(moe_ctx* ctx, const void* src, void* dst, int64_t rows, int K,
+                            void* stream) {
+  if (!ctx || !src || !dst) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (rows <= 0 || rows % 128 || K <= 0 || K % 64)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "rows must be a multiple of 128 and K a multiple of 64");
+  MOE_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const auto* in = static_cast<const __nv_bfloat16*>(src);
+  auto* outp = static_cast<__nv_bfloat16*>(dst);
+  cudaError_t e = cudaSuccess;
+  if (src != dst) {
+    const char *a = static_cast<const char*>(src), *b = static_cast<const char*>(dst);
+    const size_t bytes = (size_t)rows * K * 2;
+    if (a < b + bytes && b < a + bytes) return fail(MOE_ERR_INVALID_ARGUMENT, "src and dst overlap");
+    e = launch_pack_tiles(in, outp, (long)rows, K, s);
+  } else {
+    // in place: a tile row-block occupies exactly the bytes of its 128 source
+    // rows, so blocks of rows pack into a scratch and copy straight back
+    const long block = std::max<long>(128, ((64L << 20) / ((long)K * 2)) / 128 * 128);
+    DevBuf<__nv_bfloat16> tmp;
+    int st = tmp.reserve((size_t)std::min<long>(block, (long)rows) * K);
+    if (st) return st;
+    for (long r0 = 0; r0 < rows && e == cudaSuccess; r0 += block) {
+      const long n = std::min<long>(block, (long)rows - r0);
+      e = launch_pack_tiles(in + (size_t)r0 * K, tmp.p, n, K, s);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(outp + (size_t)r0 * K, tmp.p, (size_t)n * K * 2, cudaMemcpyDeviceToDevice, s);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    tmp.release();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "pack expert weights");
   return MOE_OK;
 }
 
@@ -714,6 +769,8 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
   auto mark = [&](int i) {
     if (ev) cudaEventRecord(ev[i], s);
   };
+  if (L->no_weights && !L->slot_of)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "layer has no expert weights: attach an expert cache (moe_cache_create)");
   const int32_t* off = e_lo >= 0 ? L->item_off.p : nullptr;
   const bool fcomb = layer_fused_combine(L);
   mark(3);
@@ -1210,8 +1267,10 @@ int moe_layer_set_weight_pool(moe_layer* L, const void* W1_pool, const void* W2_
   const moe_layer_desc& d = L->d;
   int st;
   if (!W1_pool || !W2_pool) {
-    if ((st = encode_bf16(&L->tmW1, L->W1, (uint64_t)d.num_experts * d.hidden_dim, d.token_dim, 128)) ||
-        (st = encode_bf16(&L->tmW2, L->W2, (uint64_t)d.num_experts * d.token_dim, d.hidden_dim, 128)))
+    // back to the layer's own weights (row-major map only where they are row-major)
+    if (!L->no_weights && !L->caller_packed &&
+        ((st = encode_bf16(&L->tmW1, L->W1, (uint64_t)d.num_experts * d.hidden_dim, d.token_dim, 128)) ||
+         (st = encode_bf16(&L->tmW2, L->W2, (uint64_t)d.num_experts * d.token_dim, d.hidden_dim, 128))))
       return st;
     L->slot_of = nullptr;
   } else {

@@ -158,6 +158,7 @@ struct moe_ctx {
   int route_max_blocks = 0;
   int route_prepared_E = -1;
   DevBuf<int32_t> block_hist, err_flag, drop_mark;
+  DevBuf<int32_t> static_splits;  // moe_route_static's splits scratch (per device)
   cudaStream_t scratch_stream = nullptr;
 
   int prepare_route(int E) {
@@ -193,6 +194,8 @@ struct moe_layer {
   moe::RowMaps xpm, hm;  // Xp / H at 8/16/32/64-row boxes (fused FFN)
   // prepacked weights: 128 x 64 tiles, 16 KB contiguous (launch_pack_tiles)
   bool packed = false;
+  bool caller_packed = false;  // tmW1p/tmW2p address the caller's pre-packed W1/W2 (no copy)
+  bool no_weights = false;     // pool-only layer: expert weights come from an attached cache
   DevBuf<__nv_bfloat16> w1p, w2p;
   CUtensorMap tmW1p, tmW2p;
   CUtensorMap tmX;  // X for the gate (box 64 x 128)

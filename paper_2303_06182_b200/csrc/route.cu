@@ -261,6 +261,11 @@ __global__ void __launch_bounds__(kSingle ? kSingleThreads : kMultiThreads)
           }
           a.drop_mark[slot] = r < cap ? 0 : 1;
         }
+      } else if (slot < w_hi) {
+        // a rejected (out-of-range) id: the slot has no row, so no stale row
+        // index from an earlier forward reaches the gather / combine
+        if (a.pos) a.pos[slot] = -1;
+        if (cap != 0) a.drop_mark[slot] = 0;
       }
       __syncwarp();
       if (e >= 0 && (peers & lanemask_lt()) == 0) my_cnt[e] += __popc(peers);

@@ -82,7 +82,13 @@ class MoeLayer:
     def __init__(self, shape: LayerShape, max_tokens: int, mode: str = "dynamic",
                  capacity_factor: float = 1.0, weights=None, keep_logits: bool = False,
                  tile_n: int = 0, device: int | None = None, seed: int = SEED, fuse_combine: bool = False,
-                 split_ffn: bool = False, fuse_front: bool = False, keep_layout: bool = False):
+                 split_ffn: bool = False, fuse_front: bool = False, keep_layout: bool = False,
+                 pack_in_place: bool = False, pool_only: bool = False):
+        """pack_in_place: the caller's W1/W2 tensors are repacked IN PLACE into
+        the tile layout the fused FFN streams and the layer keeps no copy
+        (expert weights held once; the tensors are no longer row-major
+        afterwards).  pool_only: no expert weights on the device (W1/W2 may
+        be None) -- attach an ExpertCache before forwarding."""
         self.ctx = Context.get(device)
         dev = torch.device("cuda", self.ctx.device)
         TD, HD, E, k = shape.token_dim, shape.hidden_dim, shape.num_experts, shape.top_k
@@ -93,13 +99,22 @@ class MoeLayer:
         if weights is None:
             weights = make_weights(shape, ctx=self.ctx, seed=seed)
         self.Wg, self.W1, self.W2 = weights
+        if pool_only:
+            self.W1 = self.W2 = None
         for t, sh in ((self.Wg, (E, TD)), (self.W1, (E, HD, TD)), (self.W2, (E, TD, HD))):
+            if t is None:
+                continue
             assert t.dtype == torch.bfloat16 and t.is_contiguous() and tuple(t.shape) == sh, sh
             assert t.device == dev
+        self.weights_packed = bool(pack_in_place) and not pool_only
+        if self.weights_packed:
+            pack_expert_weights_(self.W1, self.ctx)
+            pack_expert_weights_(self.W2, self.ctx)
         d = _capi.LayerDesc(max_tokens, TD, HD, E, k,
                             _capi.MOE_GATING_DYNAMIC if mode == "dynamic" else _capi.MOE_GATING_STATIC,
                             float(capacity_factor), int(tile_n), int(bool(keep_logits)), int(bool(fuse_combine)),
-                            int(bool(split_ffn)), int(bool(fuse_front)), int(bool(keep_layout)))
+                            int(bool(split_ffn)), int(bool(fuse_front)), int(bool(keep_layout)),
+                            int(self.weights_packed))
         h = C.c_void_p()
         check(self.ctx.lib.moe_layer_create(self.ctx.h, C.byref(d), _p(self.Wg), _p(self.W1),
                                             _p(self.W2), C.byref(h)))
@@ -239,6 +254,16 @@ def make_weights(shape: LayerShape, device=None, seed: int = SEED, ctx=None):
     return Wg, W1, W2
 
 
+def pack_expert_weights_(W: torch.Tensor, ctx=None, stream=None) -> torch.Tensor:
+    """Repack expert weights [E, rows, K] (bf16, device) IN PLACE into the
+    tile layout of the fused FFN (moe_pack_expert_weights); returns W."""
+    assert W.dtype == torch.bfloat16 and W.is_cuda and W.is_contiguous() and W.dim() == 3
+    ctx = ctx or Context.get(W.device.index)
+    check(ctx.lib.moe_pack_expert_weights(ctx.h, _p(W), _p(W), W.shape[0] * W.shape[1], W.shape[2],
+                                          _stream_ptr(stream)))
+    return W
+
+
 def make_tokens(S: int, TD: int, device=None, seed: int = SEED, ctx=None):
     import math
 
@@ -257,6 +282,8 @@ class ExpertCache:
     def __init__(self, layer: MoeLayer, n_slots: int, policy: str = "lifo", W1_host=None, W2_host=None):
         self.layer = layer
         self.ctx = layer.ctx
+        if (W1_host is None or W2_host is None) and (layer.W1 is None or layer.weights_packed):
+            raise ValueError("pass the row-major pinned host weights (W1_host, W2_host)")
         self.W1_host = W1_host if W1_host is not None else layer.W1.cpu().pin_memory()
         self.W2_host = W2_host if W2_host is not None else layer.W2.cpu().pin_memory()
         for t in (self.W1_host, self.W2_host):

@@ -418,3 +418,43 @@ def test_invalid_expert_ids_fail_cleanly_and_layer_recovers():
     layer.check_errors()
     ref = OL.layer_forward(_f32(x), _f32(w[1]), _f32(w[2]), ex, gw.astype(np.float64), E)
     assert OL.rel_fro(_f32(out), ref) < TOL_OUT
+
+
+@pytest.mark.parametrize("S,TD,HD,E,k", [(1024, 256, 512, 16, 2), (2048, 1024, 4096, 8, 1),
+                                         (16384, 1024, 4096, 512, 2), (12288, 2048, 8192, 128, 2)])
+def test_pack_in_place_holds_expert_weights_once(S, TD, HD, E, k):
+    """moe_pack_expert_weights in place + weights_packed: the layer streams the
+    caller's (repacked) buffers and allocates no expert-weight copy; outputs
+    bitwise equal to the default layer (which streams its own packed copy)."""
+    shape = LayerShape(TD, HD, E, k)
+    x = make_tokens(S, TD, seed=SEED)
+    ref_layer = MoeLayer(shape, S, weights=make_weights(shape, seed=SEED))
+    ref = ref_layer(x)
+    torch.cuda.synchronize()
+    ref_layer.close()
+    del ref_layer
+    torch.cuda.empty_cache()
+    w = make_weights(shape, seed=SEED)
+
+    def allocated_by(make):
+        torch.cuda.synchronize()
+        free0 = torch.cuda.mem_get_info()[0]
+        obj = make()
+        torch.cuda.synchronize()
+        return obj, free0 - torch.cuda.mem_get_info()[0]
+
+    copy_layer, extra_copy = allocated_by(lambda: MoeLayer(shape, S, weights=w))
+    copy_layer.close()
+    del copy_layer
+    torch.cuda.empty_cache()
+    layer, extra = allocated_by(lambda: MoeLayer(shape, S, weights=w, pack_in_place=True))
+    expert_bytes = E * 2 * TD * HD * 2
+    print(f"layer allocations {extra / 1e6:.1f} MB (default layer {extra_copy / 1e6:.1f} MB) "
+          f"for {expert_bytes / 1e6:.1f} MB of experts")
+    assert extra_copy - extra >= 0.9 * expert_bytes
+    out = layer(x)
+    out2 = layer(x)
+    torch.cuda.synchronize()
+    layer.check_errors()
+    assert torch.equal(out, ref) and torch.equal(out2, ref)
+    assert layer.view()["ffn_kernel"] in (1, 2)
