@@ -618,12 +618,12 @@ def run_b200(args):
     weights = make_weights(shape, seed=2303061820)
     # expert weights held ONCE: the dynamic-gating layer streams them tile-packed
     # in place (no second copy); static gating streams them row-major
-    in_place = mode == "dynamic" and not (args.split_ffn or args.fuse_combine)
+    in_place = mode == "dynamic" and not args.split_ffn
     torch.cuda.synchronize()
     free0, total_mem = torch.cuda.mem_get_info()
     layer = MoeLayer(shape, S, mode=mode, capacity_factor=C if mode == "static" else 1.0, weights=weights,
                      tile_n=args.tile_n, fuse_combine=args.fuse_combine,
-                     split_ffn=args.split_ffn, fuse_front=args.fuse_front, pack_in_place=in_place)
+                     split_ffn=args.split_ffn, pack_in_place=in_place)
     del weights
     torch.cuda.synchronize()
     expert_bytes = E * 2 * TD * HD * 2
@@ -760,7 +760,7 @@ def run_b200(args):
     one_launch = ((mode == "dynamic" or os.environ.get("MOE_FUSED_STATIC", "1") != "0")
                   and int(v["tile_n"]) in (128, 256) and not args.split_ffn
                   and (int(v["tile_n"]) == 128 or os.environ.get("MOE_FUSED_256", "1") != "0"))
-    launches_per_step = ((1 if args.fuse_front else 3) + (1 if one_launch else 2)
+    launches_per_step = (3 + (1 if one_launch else 2)
                          + (0 if args.fuse_combine else 1))
     ffn_b = ffn_bytes(rows, active, TD, HD, one_launch)
     ffn_ms = mean_stage[3] + mean_stage[4]
@@ -855,7 +855,6 @@ def main():
     ap.add_argument("--tokens", type=int, default=0, help="override tokens per step (mt-cache)")
     ap.add_argument("--fuse-combine", action="store_true", help="combine in the GEMM2 epilogue (A/B)")
     ap.add_argument("--split-ffn", action="store_true", help="GEMM1/GEMM2 as two launches (A/B)")
-    ap.add_argument("--fuse-front", action="store_true", help="gate+dispatch+gather in one launch (A/B)")
     ap.add_argument("--no-graph", action="store_true", help="timed steps as eager launches")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N>1: weak = S tokens per GPU; strong = S tokens in total, split over the GPUs "

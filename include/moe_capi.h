@@ -163,17 +163,15 @@ typedef struct moe_layer_desc {
   double capacity_factor; /* static mode only */
   int tile_n;             /* grouped-FFN item width: 0 = auto, 128 or 256 */
   int keep_logits;        /* 1: keep fp32 gate logits [S,E] for parity checks */
-  int fuse_combine;       /* 1: dynamic gating combines inside the GEMM2
-                             epilogue (last-arrival sums the k partials);
-                             0 (default): separate combine kernel -- measured
-                             equal speed, profiles/r01_fusion_ab.md */
+  int fuse_combine;       /* top-1 layers only: 1 = GEMM2 stores each token's
+                             output row itself (gate weight applied), no
+                             combine kernel; 0 (default): separate combine.
+                             (The k >= 2 last-arrival form measured no faster
+                             than the combine kernel in round 1 and was
+                             removed, profiles/r01_fusion_ab.md.) */
   int split_ffn;          /* 1: GEMM1 and GEMM2 as two launches (H through HBM);
                              0 (default): one fused persistent launch with H
                              kept in L2 */
-  int fuse_front;         /* 1: gate + dispatch + gather in one cooperative
-                             launch (dynamic gating, batch <= one 128-token
-                             tile per SM); 0 (default): three launches --
-                             measured faster, profiles/r01_fusion_ab.md */
   int keep_layout;        /* 0 (default): when the fused FFN runs, the layer keeps
                              a copy of W1/W2 repacked into contiguous 128x64
                              tiles (+1x expert-weight memory; weights are

@@ -71,7 +71,7 @@ class LayerDesc(C.Structure):
         ("num_experts", C.c_int), ("top_k", C.c_int), ("mode", C.c_int),
         ("capacity_factor", C.c_double), ("tile_n", C.c_int), ("keep_logits", C.c_int),
         ("fuse_combine", C.c_int), ("split_ffn", C.c_int),
-        ("fuse_front", C.c_int), ("keep_layout", C.c_int), ("weights_packed", C.c_int),
+        ("keep_layout", C.c_int), ("weights_packed", C.c_int),
     ]
 
 

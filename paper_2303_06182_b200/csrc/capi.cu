@@ -464,9 +464,11 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
   const bool pool_only = !W1;
   if (pool_only && (d.mode != MOE_GATING_DYNAMIC || d.weights_packed))
     return fail(MOE_ERR_INVALID_ARGUMENT, "a pool-only layer (no W1/W2) needs dynamic gating, row-major pools");
-  if (d.weights_packed && (d.mode != MOE_GATING_DYNAMIC || d.split_ffn || d.keep_layout || d.fuse_combine))
+  if (d.weights_packed && (d.mode != MOE_GATING_DYNAMIC || d.split_ffn || d.keep_layout))
     return fail(MOE_ERR_INVALID_ARGUMENT,
-                "pre-packed weights need dynamic gating and the fused FFN (split_ffn, keep_layout, fuse_combine 0)");
+                "pre-packed weights need dynamic gating and the fused FFN (split_ffn, keep_layout 0)");
+  if (d.fuse_combine && d.top_k != 1)
+    return fail(MOE_ERR_UNSUPPORTED, "fuse_combine (GEMM2 stores the output rows) applies to top-1 layers");
   MOE_CUDA(cudaSetDevice(ctx->device));
   cudaError_t ce = gate_prepare(d.num_experts);
   if (ce != cudaSuccess) return cuda_fail(ce, "gate_prepare");
@@ -509,7 +511,6 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
       (st = L->wpos.reserve(R)) || (st = L->items.reserve(L->items_max)) ||
       (st = L->n_items.reserve(1)) || (st = L->err.reserve(1)) ||
       (st = L->item_off.reserve((size_t)E + 1)) ||
-      (st = L->comb_cnt.reserve((size_t)S * (d.token_dim / 128))) ||
       (st = L->done.reserve(2 * (size_t)L->items_max + 1)) ||
       (st = L->xp.reserve(Rp * TD)) || (st = L->h.reserve(Rp * HD)) ||
       (st = L->yw.reserve(R * TD))) {
@@ -530,9 +531,8 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
   // rejected (error flag) keeps pos = -1 and is skipped by the gather
   cudaMemset(L->pos.p, 0xff, sizeof(int32_t) * (size_t)S * k);
   cudaMemset(L->order.p, 0xff, sizeof(int32_t) * R);
-  cudaMemset(L->comb_cnt.p, 0, sizeof(int32_t) * (size_t)S * (d.token_dim / 128));
   cudaMemset(L->h.p, 0, Rp * HD * 2);
-  if ((st = encode_bf16(&L->tmWg, Wg, E, TD, moe::gate_box_rows(E), moe::gate_box_cols(E, d.fuse_front))) ||
+  if ((st = encode_bf16(&L->tmWg, Wg, E, TD, moe::gate_box_rows(E), moe::gate_box_cols(E))) ||
       (!pool_only && !d.weights_packed &&
        ((st = encode_bf16(&L->tmW1, W1, (uint64_t)E * HD, TD, 128)) ||
         (st = encode_bf16(&L->tmW2, W2, (uint64_t)E * TD, HD, 128)))) ||
@@ -563,7 +563,7 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
     }
     L->packed = true;
     L->caller_packed = true;
-  } else if (!pool_only && !d.keep_layout && pack_env && !d.split_ffn && !d.fuse_combine &&
+  } else if (!pool_only && !d.keep_layout && pack_env && !d.split_ffn &&
              d.mode == MOE_GATING_DYNAMIC && (L->tile_n == 128 || fused256_enabled())) {
     const size_t n1 = (size_t)E * HD * TD;
     if (L->w1p.reserve(n1) == MOE_OK && L->w2p.reserve(n1) == MOE_OK &&
@@ -666,7 +666,6 @@ int moe_layer_destroy(moe_layer* L) {
   L->n_items.release();
   L->err.release();
   L->item_off.release();
-  L->comb_cnt.release();
   L->w1p.release();
   L->w2p.release();
   L->done.release();
@@ -701,36 +700,10 @@ int moe::capi::layer_front(moe_layer* L, const void* X, int S, const int32_t* id
   // 1. gate
   mark(0);
   if (X != L->tmX_ptr || S != L->tmX_rows) {
-    if ((st = encode_bf16(&L->tmX, X, (uint64_t)S, TD, 128,
-                          moe::gate_box_cols(L->d.num_experts, L->d.fuse_front))))
+    if ((st = encode_bf16(&L->tmX, X, (uint64_t)S, TD, 128, moe::gate_box_cols(L->d.num_experts))))
       return st;
     L->tmX_ptr = X;
     L->tmX_rows = S;
-  }
-  if (!idx_in && d.mode == MOE_GATING_DYNAMIC && d.fuse_front &&
-      gate_dispatch_supported(S, E, k, TD, L->ctx->sms)) {
-    // gate + dispatch + gather in one cooperative launch
-    GateArgs ga{S, TD, E, k, L->idx.p, L->w.p, d.keep_logits ? L->logits.p : nullptr};
-    DispatchArgs da{};
-    da.X = X;
-    da.Xp = L->xp.p;
-    da.counts = L->counts.p;
-    da.splits = L->splits.p;
-    da.order = L->order.p;
-    da.pos = L->pos.p;
-    da.wpos = L->wpos.p;
-    da.block_hist = L->ctx->block_hist.p;
-    da.items = L->items.p;
-    da.n_items = L->n_items.p;
-    da.item_off = L->item_off.p;
-    da.tile_n = L->tile_n;
-    L->last_rows = S * k;
-    L->last_cap = 0;
-    cudaError_t e = launch_gate_dispatch(L->tmX, L->tmWg, ga, da, s);
-    if (e != cudaSuccess) return cuda_fail(e, "gate+dispatch launch");
-    mark(1);
-    mark(2);
-    return MOE_OK;
   }
   if (!idx_in) {
     GateArgs ga{S, TD, E, k, L->idx.p, L->w.p, d.keep_logits ? L->logits.p : nullptr};
@@ -829,16 +802,10 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
     fa.packed = L->packed && !L->slot_of;
     fa.pair_hint = auto_pair((double)L->rows_max / L->d.num_experts, L->d.num_experts, TD, HD,
                              L->tile_n, L->ctx->sms);
-    if (fcomb && L->d.top_k == 1) {
-      // one contribution per token: GEMM2 writes the layer output row directly
+    if (fcomb) {
+      // top-1: one contribution per token, GEMM2 writes the layer output row directly
       fa.Yw = static_cast<__nv_bfloat16*>(L->fwd_out);
       fa.out_rows = L->order.p;
-    } else if (fcomb) {
-      fa.top_k = L->d.top_k;
-      fa.comb_order = L->order.p;
-      fa.comb_pos = L->pos.p;
-      fa.comb_cnt = L->comb_cnt.p;
-      fa.comb_out = static_cast<__nv_bfloat16*>(L->fwd_out);
     }
     L->last_ffn_kernel = fused_ffn_uses_pair(fa, L->tile_n) ? 2 : 1;
     cudaError_t e = launch_fused_ffn(fa.packed ? L->tmW1p : L->tmW1, L->xpm,
@@ -856,17 +823,10 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
   mark(4);
   GemmArgs g2{L->items.p, L->n_items.p, L->slot_of, TD, HD, kEpiScaleBf16, L->yw.p, L->wpos.p,
               nullptr, off, e_lo, e_hi};
-  if (fcomb && L->d.top_k == 1) {
-    // one contribution per token: write the layer output directly (row -> token)
+  if (fcomb) {
+    // top-1: one contribution per token, write the layer output directly (row -> token)
     g2.out = static_cast<__nv_bfloat16*>(L->fwd_out);
     g2.out_rows = L->order.p;
-  } else if (fcomb) {
-    g2.mode = kEpiScaleCombine;
-    g2.top_k = L->d.top_k;
-    g2.comb_order = L->order.p;
-    g2.comb_pos = L->pos.p;
-    g2.comb_cnt = L->comb_cnt.p;
-    g2.comb_out = static_cast<__nv_bfloat16*>(L->fwd_out);
   }
   e = launch_grouped_gemm(L->tmW2, L->tmH, g2, L->tile_n, L->ctx->sms, s);
   if (e != cudaSuccess) return cuda_fail(e, "grouped gemm 2 launch");

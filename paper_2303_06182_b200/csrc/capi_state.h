@@ -18,9 +18,8 @@
 
 namespace moe {
 int gate_box_rows(int E);
-// inner (K) extent of the gate's X / Wg TMA boxes (64 or 32; 32 for the
-// cooperative gate + dispatch kernel)
-int gate_box_cols(int E, bool fused_front = false);
+// inner (K) extent of the gate's X / Wg TMA boxes (64 for E <= 128, else 32)
+int gate_box_cols(int E);
 
 namespace capi {
 
@@ -201,7 +200,6 @@ struct moe_layer {
   CUtensorMap tmX;  // X for the gate (box 64 x 128)
   const void* tmX_ptr = nullptr;
   int tmX_rows = 0;
-  DevBuf<int32_t> comb_cnt;  // fused-combine counters [S_max * TD/128], self-resetting
   DevBuf<int32_t> done;      // fused-FFN per-item counters [2 * items_max]
   void* fwd_out = nullptr;   // output of the forward in flight (fused combine target)
   // optional expert-cache weight pool
@@ -272,9 +270,10 @@ int layer_front(moe_layer* L, const void* X, int S, const int32_t* idx_in, const
                 cudaStream_t s, cudaEvent_t* ev);
 int layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaEvent_t* ev);
 int layer_back(moe_layer* L, int S, void* out, cudaStream_t s, cudaEvent_t* ev);
-// dynamic gating with fuse_combine: the combine runs inside the GEMM2 epilogue
+// dynamic top-1 gating with fuse_combine: GEMM2 stores each token's output row
+// itself (one contribution per token, weight applied), no combine kernel
 inline bool layer_fused_combine(const moe_layer* L) {
-  return L->d.mode == MOE_GATING_DYNAMIC && L->d.fuse_combine;
+  return L->d.mode == MOE_GATING_DYNAMIC && L->d.fuse_combine && L->d.top_k == 1;
 }
 }  // namespace capi
 }  // namespace moe

@@ -18,7 +18,6 @@
 // Two TMEM accumulators (2 x tile_n columns) let the epilogue of tile i
 // overlap the MMAs of tile i+1.  Tiles = (work item, 128-row m-block); the
 // work list comes from the route kernel, so no host sync is needed.
-#include "combine_epi.cuh"
 #include "moe_internal.h"
 #include "ptx.cuh"
 
@@ -40,14 +39,6 @@ struct GemmCfg {
                                (2 * STAGES + 4) * 8 + 16;
   static constexpr int kTmemCols = 2 * BN;
 };
-
-// Fused combine for one GEMM2 tile (combine_epi.cuh).
-__device__ __forceinline__ void combine_tile(const GemmArgs& g, const FfnItem& it, int m, int MT,
-                                             int tid, int* fin_tok, int* fin_cnt) {
-  (void)MT;
-  combine_rows_epilogue(g.out, g.m_total, g.top_k, g.comb_order, g.comb_pos, g.comb_cnt,
-                        g.comb_out, it.row0, it.len, m, tid, fin_tok, fin_cnt);
-}
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(256, 1)
@@ -164,8 +155,6 @@ __global__ void __launch_bounds__(256, 1)
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;  // TMEM lane quadrant owned by this warp
     __nv_bfloat16* stg = sEpi + q * 32 * 32;
-    __shared__ int fin_tok[256];  // tokens whose last contribution is in this tile
-    __shared__ int fin_cnt[1];
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -182,7 +171,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i)
             stg[i * 32 + lane] = __float2bfloat16_rn(fmaxf(__uint_as_float(r[i]), 0.f));
-        } else {  // kEpiScaleBf16 / kEpiScaleCombine: gate weight of the row
+        } else {  // kEpiScaleBf16: gate weight of the row
           const float wv = (c0 + lane < it.len) ? g.wpos[it.row0 + c0 + lane] : 0.f;
 #pragma unroll
           for (int i = 0; i < 32; ++i)
@@ -204,13 +193,12 @@ __global__ void __launch_bounds__(256, 1)
         }
         __syncwarp();
       }
-      // TMEM of this tile is no longer needed: release it before the combine
+      // TMEM of this tile is no longer needed
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-      if (g.mode == kEpiScaleCombine) combine_tile(g, it, m, MT, threadIdx.x - 128, fin_tok, fin_cnt);
     }
   }
 

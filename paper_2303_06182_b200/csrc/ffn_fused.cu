@@ -25,7 +25,6 @@
 #include <cstdio>
 #include <cstdlib>
 
-#include "combine_epi.cuh"
 #include "moe_internal.h"
 #include "ptx.cuh"
 
@@ -129,7 +128,6 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ int last_consumer;
-  __shared__ int fin_tok[256], fin_cnt;  // combine epilogue (g.comb_out)
   // dynamic tail: tiles [t_dyn, total) are claimed from a global counter by
   // the producer and handed to the MMA / epilogue warps through this ring
   constexpr int kRing = 4;
@@ -353,7 +351,6 @@ __global__ void __launch_bounds__(256, 1)
     const int q = warp & 3;
     const int tid = threadIdx.x - 128;
     __nv_bfloat16* stg = sEpi + q * 32 * 32;
-    const uint64_t pol_keep = ptx::policy_evict_last();
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x < t_dyn ? blockIdx.x : take(true); t >= 0;
@@ -389,11 +386,7 @@ __global__ void __launch_bounds__(256, 1)
             const uint4 v = *reinterpret_cast<const uint4*>(stg + tok * 32 + ch * 8);
             int row = it.row0 + c0 + tok;
             if (tr.gemm && g.out_rows) row = g.out_rows[row];
-            __nv_bfloat16* dst = out + static_cast<size_t>(row) * m_total + col0 + ch * 8;
-            if (tr.gemm && g.yw_keep)
-              ptx::st_global_hint(dst, v, pol_keep);
-            else
-              *reinterpret_cast<uint4*>(dst) = v;
+            *reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * m_total + col0 + ch * 8) = v;
           }
         }
         __syncwarp();
@@ -417,9 +410,6 @@ __global__ void __launch_bounds__(256, 1)
           if (tid == 0) red_release_add(done1 + tr.item, 1);
         }
       } else {
-        if (g.comb_out)
-          combine_rows_epilogue(g.Yw, g.TD, g.top_k, g.comb_order, g.comb_pos, g.comb_cnt,
-                                g.comb_out, it.row0, it.len, tr.m, tid, fin_tok, &fin_cnt);
         // this tile's MMAs (hence its H reads) are complete; the last consumer
         // of the item drops the item's H lines from L2 without write-back
         asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -462,16 +452,6 @@ cudaError_t launch_fused(const CUtensorMap& w1, const RowMaps& xp, const CUtenso
 
 }  // namespace
 
-// MOE_FFN_KCH=1 selects the 64-deep stages (6 x 32 KB) for A/B experiments.
-int fused_kch() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("MOE_FFN_KCH");
-    v = (e && atoi(e) == 1) ? 1 : 2;
-  }
-  return v;
-}
-
 cudaError_t fused_ffn_pair_prepare();
 bool fused_ffn_pair_enabled(int hint);
 cudaError_t launch_fused_ffn_pair(const CUtensorMap& tmW1, const RowMaps& xp,
@@ -482,8 +462,8 @@ cudaError_t launch_fused_ffn_pair(const CUtensorMap& tmW1, const RowMaps& xp,
 cudaError_t fused_ffn_prepare() {
   cudaError_t e = fused_ffn_pair_prepare();
   if (e != cudaSuccess) return e;
-  e = prepare_fused<128, 6, 1>();
-  if (e != cudaSuccess) return e;
+  // 128-token items: 3 stages of two 64-wide k chunks (round 1 A/B against
+  // 6 x 64-deep stages, since removed)
   if ((e = prepare_fused<128, 3, 2>()) != cudaSuccess) return e;
   return prepare_fused<256, 4, 1>();
 }
@@ -502,9 +482,7 @@ cudaError_t launch_fused_ffn_impl(const CUtensorMap& tmW1, const RowMaps& xp, co
     cudaError_t e = launch_fused_ffn_pair(tmW1, xp, tmW2, h, args, tile_n, grid, stream);
     if (e != cudaErrorNotSupported) return e;
   }
-  if (tile_n == 128 && fused_kch() == 2)
-    return launch_fused<128, 3, 2>(tmW1, xp, tmW2, h, args, grid, stream);
-  if (tile_n == 128) return launch_fused<128, 6, 1>(tmW1, xp, tmW2, h, args, grid, stream);
+  if (tile_n == 128) return launch_fused<128, 3, 2>(tmW1, xp, tmW2, h, args, grid, stream);
   if (tile_n == 256) return launch_fused<256, 4, 1>(tmW1, xp, tmW2, h, args, grid, stream);
   return cudaErrorInvalidValue;
 }
@@ -531,13 +509,8 @@ cudaError_t launch_fused_ffn(const CUtensorMap& tmW1, const RowMaps& xp, const C
     const char* v = getenv("MOE_FFN_DYN_TAIL");  // tiles claimed dynamically; 0 = lag * MT2, <0 = off
     return v ? atoi(v) : 0;
   }();
-  static const int yw_keep = [] {
-    const char* v = getenv("MOE_FFN_YW_KEEP");
-    return v ? atoi(v) : 0;
-  }();
   FusedFfnArgs args = args_in;
   args.full_fence = full_fence;
-  args.yw_keep = yw_keep;
   args.dyn_tail = dyn_tail;
   if (dyn_tail < 0) args.tile_ctr = nullptr;
   args.late_trigger = late;

@@ -22,7 +22,6 @@
 #include <cstdio>
 #include <cstdlib>
 
-#include "combine_epi.cuh"
 #include "moe_internal.h"
 #include "ptx.cuh"
 
@@ -174,7 +173,6 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ int last_consumer;
-  __shared__ int fin_tok[256], fin_cnt;  // combine epilogue (g.comb_out)
   // dynamic tail (as ffn_fused.cu): the leader's producer claims the tail's
   // pair-tiles from a global counter and hands them to its MMA / epilogue
   // warps and to the peer's producer / epilogue warps through this ring
@@ -371,7 +369,6 @@ __global__ void __launch_bounds__(256, 1)
     const int q = warp & 3;
     const int tid = threadIdx.x - 128;
     __nv_bfloat16* stg = sEpi + q * 32 * 32;
-    const uint64_t pol_keep = ptx::policy_evict_last();
     const uint32_t tempty_l[2] = {leader_addr(&tempty[0]), leader_addr(&tempty[1])};
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -409,11 +406,7 @@ __global__ void __launch_bounds__(256, 1)
             const uint4 v = *reinterpret_cast<const uint4*>(stg + tok * 32 + ch * 8);
             int row = it.row0 + c0 + tok;
             if (tr.gemm && g.out_rows) row = g.out_rows[row];
-            __nv_bfloat16* dst = out + static_cast<size_t>(row) * m_total + col0 + ch * 8;
-            if (tr.gemm && g.yw_keep)
-              ptx::st_global_hint(dst, v, pol_keep);
-            else
-              *reinterpret_cast<uint4*>(dst) = v;
+            *reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * m_total + col0 + ch * 8) = v;
           }
         }
         __syncwarp();
@@ -432,9 +425,6 @@ __global__ void __launch_bounds__(256, 1)
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (tid == 0) atomicAdd(done1 + tr.item, 1);
       } else {
-        if (g.comb_out)
-          combine_rows_epilogue(g.Yw, g.TD, g.top_k, g.comb_order, g.comb_pos, g.comb_cnt,
-                                g.comb_out, it.row0, it.len, m, tid, fin_tok, &fin_cnt);
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (tid == 0) last_consumer = atomicAdd(done2 + tr.item, 1) == MT2 - 1;
         asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -461,18 +451,6 @@ __global__ void __launch_bounds__(256, 1)
                  "n"(kTmemCols)
                  : "memory");
   if (g.late_trigger) pdl_trigger();
-}
-
-// Pair stage shape: 4 stages of 128-deep k (two 64-wide chunks, default:
-// LM FFN 1.303 -> 1.284 ms, MT 1.384 -> 1.340 ms against 8 x 64-deep on the
-// same box) or MOE_FFN_PAIR_STAGES=8 for 8 x 64-deep.
-int pair_cfg() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("MOE_FFN_PAIR_STAGES");
-    v = (e && atoi(e) == 8) ? 8 : 4;
-  }
-  return v;
 }
 
 template <int BN, int STAGES, int KCH>
@@ -529,15 +507,13 @@ cudaError_t launch_pair(const CUtensorMap& tmW1, const RowMaps& xp, const CUtens
 
 }  // namespace
 
+// Stage shapes (round 1, same-box A/B, the losing shapes since removed):
+// 128-token items 4 stages of 128-deep k (two 64-wide chunks): LM FFN
+// 1.303 -> 1.284 ms, MT 1.384 -> 1.340 ms against 8 x 64-deep; 256-token items
+// 3 x 128-deep: MT seq 256 FFN 1.82 -> 1.78-1.80 ms, LM static 7.76 ->
+// 7.59-7.68 ms against 6 x 64.
 cudaError_t fused_ffn_pair_prepare() {
-  cudaError_t e = cudaFuncSetAttribute(fused_ffn_pair_kernel<128, 8, 1>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       PairCfg<128, 8, 1>::kSmem);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(fused_ffn_pair_kernel<256, 6, 1>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<256, 6, 1>::kSmem);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(fused_ffn_pair_kernel<256, 3, 2>,
+  cudaError_t e = cudaFuncSetAttribute(fused_ffn_pair_kernel<256, 3, 2>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<256, 3, 2>::kSmem);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(fused_ffn_pair_kernel<128, 4, 2>,
@@ -564,19 +540,8 @@ cudaError_t launch_fused_ffn_pair(const CUtensorMap& tmW1, const RowMaps& xp,
                                   const CUtensorMap& tmW2, const RowMaps& h,
                                   const FusedFfnArgs& args, int tile_n, int sms,
                                   cudaStream_t stream) {
-  if (tile_n == 256) {
-    // 3 x 128-deep k stages (default: MT seq 256 FFN 1.82 -> 1.78-1.80 ms,
-    // LM static 7.76 -> 7.59-7.68 ms against 6 x 64, same box);
-    // MOE_FFN_PAIR256_STAGES=6 restores 6 x 64
-    static const int s256 = [] {
-      const char* e = getenv("MOE_FFN_PAIR256_STAGES");
-      return e ? atoi(e) : 3;
-    }();
-    if (s256 == 3) return launch_pair<256, 3, 2>(tmW1, xp, tmW2, h, args, sms, stream);
-    return launch_pair<256, 6, 1>(tmW1, xp, tmW2, h, args, sms, stream);
-  }
-  if (pair_cfg() == 4) return launch_pair<128, 4, 2>(tmW1, xp, tmW2, h, args, sms, stream);
-  return launch_pair<128, 8, 1>(tmW1, xp, tmW2, h, args, sms, stream);
+  if (tile_n == 256) return launch_pair<256, 3, 2>(tmW1, xp, tmW2, h, args, sms, stream);
+  return launch_pair<128, 4, 2>(tmW1, xp, tmW2, h, args, sms, stream);
 }
 
 }  // namespace moe

@@ -101,7 +101,7 @@ cudaError_t route_prepare(int E, int* max_blocks);
 cudaError_t launch_route(RouteArgs a, int max_blocks, cudaStream_t stream);
 
 // ---- grouped expert FFN (tcgen05)
-enum EpilogueMode { kEpiReluBf16 = 0, kEpiScaleBf16 = 1, kEpiScaleCombine = 2 };
+enum EpilogueMode { kEpiReluBf16 = 0, kEpiScaleBf16 = 1 };
 
 struct GemmArgs {
   const FfnItem* items;
@@ -115,14 +115,6 @@ struct GemmArgs {
   const int32_t* out_rows; // optional row remap of the output (row r -> out_rows[r])
   const int32_t* item_off; // optional: run only the items of experts [e_lo, e_hi)
   int e_lo, e_hi;
-  // fused combine (kEpiScaleCombine): the last of the k contributions of a
-  // token (per 128-feature block) sums the bf16 partials in slot order and
-  // writes the layer output; counters [S * m_total/128] self-reset to 0.
-  int top_k;
-  const int32_t* comb_order;
-  const int32_t* comb_pos;
-  int32_t* comb_cnt;
-  __nv_bfloat16* comb_out;
 };
 
 // Fused GEMM1 + GEMM2 (ffn_fused.cu): one persistent launch, H kept in L2.
@@ -157,13 +149,6 @@ struct FusedFfnArgs {
   const int32_t* arrived_expect;
   int32_t* arrive_err;
   unsigned long long arrive_timeout_ns;
-  int yw_keep;               // GEMM2 stores Yw with an L2 evict_last hint (read next by the combine)
-  // combine in the GEMM2 epilogue (combine_epi.cuh); comb_out null = off
-  int top_k;
-  const int32_t* comb_order;  // row -> slot (token * k + j)
-  const int32_t* comb_pos;    // slot -> row
-  int32_t* comb_cnt;          // [tokens, TD / 128], zero between forwards
-  __nv_bfloat16* comb_out;    // [tokens, TD]
 };
 // One activation matrix (Xp or H) seen by TMA at four box heights: a B tile
 // of n rows (n % 8 == 0) is n/64 boxes of 64 rows plus at most one each of 32,
@@ -192,24 +177,6 @@ struct GateArgs {
   float* logits;    // optional [S*E]
   unsigned long long* prof = nullptr;  // experiments (MOE_GATE_PROF): per-CTA phase times
 };
-// Gate + dynamic dispatch + gather in one cooperative launch (gate.cu).
-struct DispatchArgs {
-  const void* X;       // [S, TD] bf16 (the gate's input)
-  void* Xp;            // [kS, TD] bf16, expert-grouped rows
-  int32_t* counts;     // [E]
-  int32_t* splits;     // [E+1]
-  int32_t* order;      // [kS]
-  int32_t* pos;        // [kS]
-  float* wpos;         // [kS]
-  int32_t* block_hist; // scratch [E * (tiles + 4)]
-  FfnItem* items;
-  int32_t* n_items;
-  int32_t* item_off;   // optional [E+1]
-  int tile_n;
-};
-bool gate_dispatch_supported(int S, int E, int k, int TD, int sms);
-cudaError_t launch_gate_dispatch(const CUtensorMap& tmX, const CUtensorMap& tmWg,
-                                 const GateArgs& a, const DispatchArgs& d, cudaStream_t stream);
 cudaError_t gate_prepare(int E);
 cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateArgs& a,
                         cudaStream_t stream);

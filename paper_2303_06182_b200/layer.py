@@ -82,7 +82,7 @@ class MoeLayer:
     def __init__(self, shape: LayerShape, max_tokens: int, mode: str = "dynamic",
                  capacity_factor: float = 1.0, weights=None, keep_logits: bool = False,
                  tile_n: int = 0, device: int | None = None, seed: int = SEED, fuse_combine: bool = False,
-                 split_ffn: bool = False, fuse_front: bool = False, keep_layout: bool = False,
+                 split_ffn: bool = False, keep_layout: bool = False,
                  pack_in_place: bool = False, pool_only: bool = False):
         """pack_in_place: the caller's W1/W2 tensors are repacked IN PLACE into
         the tile layout the fused FFN streams and the layer keeps no copy
@@ -113,7 +113,7 @@ class MoeLayer:
         d = _capi.LayerDesc(max_tokens, TD, HD, E, k,
                             _capi.MOE_GATING_DYNAMIC if mode == "dynamic" else _capi.MOE_GATING_STATIC,
                             float(capacity_factor), int(tile_n), int(bool(keep_logits)), int(bool(fuse_combine)),
-                            int(bool(split_ffn)), int(bool(fuse_front)), int(bool(keep_layout)),
+                            int(bool(split_ffn)), int(bool(keep_layout)),
                             int(self.weights_packed))
         h = C.c_void_p()
         check(self.ctx.lib.moe_layer_create(self.ctx.h, C.byref(d), _p(self.Wg), _p(self.W1),

@@ -10,6 +10,7 @@ Tiers (north_star):
       accumulate, bf16 H and output), stated per test below.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -273,27 +274,33 @@ def test_repeat_forward_is_deterministic():
     assert torch.equal(out, out2)
 
 
-@pytest.mark.parametrize("S,TD,HD,E,k", [(300, 256, 512, 8, 2), (1000, 256, 384, 16, 1), (257, 128, 256, 33, 3),
-                                         (2048, 1024, 4096, 8, 1), (4096, 1024, 2048, 64, 2),
-                                         (16384, 1024, 4096, 512, 2), (6144, 2048, 8192, 128, 2)])
+@pytest.mark.parametrize("S,TD,HD,E,k", [(1000, 256, 384, 16, 1), (2048, 1024, 4096, 8, 1),
+                                         (4096, 1024, 2048, 64, 1), (16384, 1024, 4096, 512, 1)])
 @pytest.mark.parametrize("split", [False, True])
-def test_fused_combine_bitwise_equal_combine_kernel(S, TD, HD, E, k, split):
-    """The combine inside the GEMM2 epilogue computes exactly the arithmetic of
-    the separate combine kernel, whatever order the k contributions land in --
-    in the persistent fused FFN (1-SM or CTA-pair kernel) and in the two-launch
-    grouped GEMM."""
+def test_top1_direct_store_bitwise_equal_combine_kernel(S, TD, HD, E, k, split):
+    """fuse_combine on a top-1 layer: GEMM2 writes each token's output row
+    itself (in the persistent fused FFN -- 1-SM or CTA-pair kernel -- and in
+    the two-launch grouped GEMM); bitwise the combine kernel's result."""
     shape = LayerShape(TD, HD, E, k)
     w = make_weights(shape, seed=SEED)
     x = make_tokens(S, TD, seed=SEED)
     fused = MoeLayer(shape, S, weights=w, fuse_combine=True, split_ffn=split)
-    plain = MoeLayer(shape, S, weights=w)
+    plain = MoeLayer(shape, S, weights=w, split_ffn=split)
     a = fused(x)
     b = plain(x)
-    a2 = fused(x)  # counters self-reset: a second forward is identical
+    a2 = fused(x)
     torch.cuda.synchronize()
     fused.check_errors()
     assert torch.equal(a, b)
     assert torch.equal(a, a2)
+
+
+def test_fuse_combine_refused_for_top2():
+    from paper_2303_06182_b200._capi import MoeError
+
+    shape = LayerShape(256, 256, 8, 2)
+    with pytest.raises(MoeError, match="top-1"):
+        MoeLayer(shape, 64, weights=make_weights(shape, seed=SEED), fuse_combine=True)
 
 
 @pytest.mark.parametrize("S,TD,HD,E,k,mode,C", [(300, 256, 512, 8, 2, "dynamic", 1.0), (2048, 1024, 4096, 8, 1, "dynamic", 1.0),
@@ -317,25 +324,46 @@ def test_fused_ffn_bitwise_equal_two_launch_ffn(S, TD, HD, E, k, mode, C):
     assert torch.equal(a, a2)
 
 
-@pytest.mark.parametrize("S,TD,HD,E,k", [(300, 256, 512, 8, 2), (2048, 1024, 4096, 8, 1), (257, 128, 256, 33, 3),
-                                         (16384, 1024, 4096, 512, 2), (6144, 2048, 8192, 128, 2),
-                                         (18944, 256, 256, 64, 2)])
-def test_fused_gate_dispatch_matches_three_launches(S, TD, HD, E, k):
-    """Gate + dispatch + gather in one cooperative launch == gate, route and
-    gather kernels: identical routing arrays, Xp rows and layer output."""
-    shape = LayerShape(TD, HD, E, k)
-    w = make_weights(shape, seed=SEED)
-    x = make_tokens(S, TD, seed=SEED)
-    fused = MoeLayer(shape, S, weights=w, split_ffn=True, fuse_front=True)
-    split = MoeLayer(shape, S, weights=w, split_ffn=True)
-    a = fused(x)
-    b = split(x)
-    torch.cuda.synchronize()
-    fused.check_errors()
-    va, vb = fused.view(), split.view()
-    for key in ("idx", "w", "counts", "splits", "order", "pos", "n_items", "xp"):
-        assert torch.equal(va[key], vb[key]), key
-    assert torch.equal(a, b)
+_GATE_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2303_06182_b200.layer import LayerShape, MoeLayer, make_tokens, make_weights
+S, TD, HD, E, k = map(int, sys.argv[2:7])
+shape = LayerShape(TD, HD, E, k)
+layer = MoeLayer(shape, S, weights=make_weights(shape, seed=2303061820), keep_logits=True)
+layer(make_tokens(S, TD, seed=2303061820))
+torch.cuda.synchronize()
+np.save(sys.argv[7], layer.view()["logits"][:S * E].cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("S,TD,HD,E,k", [(2048, 1024, 4096, 8, 1), (6144, 2048, 8192, 128, 2),
+                                         (300, 256, 512, 40, 2)])
+def test_split_k_gate_matches_one_cta_gate(S, TD, HD, E, k, tmp_path):
+    """The split-K gate (a cluster of CTAs per token tile, partial logits
+    reduced over DSMEM: MT, cfg1 and small batches) against the one-CTA-per-
+    tile gate (MOE_GATE_SPLIT=0, a separate process since the choice is read
+    once): same logits up to fp32 summation order, both checked against the
+    fp32 oracle."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for split in ("8", "0"):
+        f = str(tmp_path / f"logits_{split}.npy")
+        env = dict(os.environ, MOE_GATE_SPLIT=split)
+        r = subprocess.run([sys.executable, "-c", _GATE_SCRIPT, root, str(S), str(TD), str(HD), str(E), str(k), f],
+                           env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[split] = np.load(f).reshape(S, E)
+    x = _f32(make_tokens(S, TD, seed=SEED))
+    Wg = _f32(make_weights(LayerShape(TD, HD, E, k), seed=SEED)[0])
+    ref = OL.gate_logits(x, Wg)
+    tol = 2e-5 * max(float(np.abs(ref).max()), 1.0) * math.sqrt(TD / 256)
+    for split, lg in outs.items():
+        assert np.abs(lg - ref).max() <= tol, split
+    assert np.abs(outs["8"] - outs["0"]).max() <= tol
 
 
 @pytest.mark.parametrize("S,TD,HD,E,k,mode,C", [
