@@ -175,6 +175,14 @@ def load_traffic(workload):
         return None
 
 
+def emit(line, args):
+    """The one JSON line on stdout (+ --json-out copy)."""
+    print(json.dumps(line), flush=True)
+    if getattr(args, "json_out", None):
+        with open(args.json_out, "w") as f:
+            json.dump(line, f, indent=1)
+
+
 def dist_setup():
     import torch
 
@@ -253,7 +261,7 @@ def run_reference(args):
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "breakdown_s": r["breakdown_s"],
     }
-    print(json.dumps(line), flush=True)
+    emit(line, args)
 
 
 def run_ep(args, world, rank, local):
@@ -485,7 +493,7 @@ def run_ep(args, world, rank, local):
         "clocks": sampler.summary() if sampler else None,
         "gpu": torch.cuda.get_device_name(local),
     }
-    print(json.dumps(line), flush=True)
+    emit(line, args)
     layer.close()
 
 
@@ -588,7 +596,7 @@ def run_cache(args):
         "fully_resident": {"ms_per_step": float(np.mean(t_full)), "value": S / (np.mean(t_full) * 1e-3)},
         "gpu": torch.cuda.get_device_name(0),
     }
-    print(json.dumps(line), flush=True)
+    emit(line, args)
     cache.close()
 
 
@@ -726,11 +734,15 @@ def run_b200(args):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    call_ms = []
     for _ in range(Ke):
-        layer.forward_host(xh, oh, stream=stream)
+        tc = time.perf_counter()
+        layer.forward_host(xh, oh, stream=stream)  # returns after the read-back
+        call_ms.append((time.perf_counter() - tc) * 1e3)
     e1.record(stream)
     e1.synchronize()
     e2e_sync_ms = max_over_ranks(e0.elapsed_time(e1) / Ke, world)
+    call_p50_ms = max_over_ranks(float(np.median(call_ms)), world)
     # serving queue: Ke batches, each uploaded from and read back to its own
     # pinned host buffers (ring of 3 distinct token sets), copies overlapped
     # with the neighbouring batches' compute (moe_layer_forward_host_batches)
@@ -781,9 +793,17 @@ def run_b200(args):
     if world == 1 and not args.no_cpu_baseline:
         from oracle.cpu_layer import cpu_layer_bench
 
+        from oracle.cpu_layer import cpu_layer_1thread, routing_1thread
+
         r = cpu_layer_bench(S, TD, HD, E, k, min_seconds=cpu_seconds())
         cpu = {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": r["cores"], "kind": "port",
                "sample": r["sample"], "breakdown_s": r["breakdown_s"]}
+        if os.environ.get("MOE_BENCH_CPU_DETAIL", "1") != "0":
+            # the 1-thread layer and the reference's routing
+            # alone (Batch prebuilt, no marshalling) beside the GPU route stage
+            cpu["one_thread"] = cpu_layer_1thread(S, TD, HD, E, k)
+            cpu["routing_1thread_s"] = routing_1thread(S, TD, E, k, C if mode == "static" else 0.0)
+            cpu["routing_1thread_s"]["gpu_route_stage_s"] = float(mean_stage[1]) * 1e-3
     line = {
         "metric": "MoE-layer tokens/s (dynamic gating)" if mode == "dynamic" else "MoE-layer tokens/s (static gating)",
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
@@ -819,15 +839,13 @@ def run_b200(args):
                         "host wall clock)" % Ke),
                 "device_ms_per_step": e2e_dev_ms, "wall_ms_per_step": wall_ms,
                 "per_call_sync": {"value": world * S / (e2e_sync_ms * 1e-3), "ms_per_step": e2e_sync_ms,
+                                  "p50_ms_wall": call_p50_ms,
                                   "api": "moe_layer_forward_host (one synchronous call per batch)"}},
         "cpu_baseline": cpu,
         "clocks": clocks,
         "gpu": torch.cuda.get_device_name(local),
     }
-    print(json.dumps(line), flush=True)
-    if args.json_out:
-        with open(args.json_out, "w") as f:
-            json.dump(line, f, indent=1)
+    emit(line, args)
     layer.close()
     if world > 1:
         import torch.distributed as dist

@@ -4,7 +4,8 @@
 // Declarations, struct layouts and exception behaviour match the reference so
 // code written against it -- including its own unit tests
 // (proj/tests/test_gating.cpp, compiled unmodified against this header, see
-// tests/test_reference_suite.py) -- builds and passes unchanged.  The work is
+// tests/test_route_gpu.py::test_reference_test_gating_compiled_against_dropin and
+// tests/test_dropin_suites.py) -- builds and passes unchanged.  The work is
 // done by the sm_100a kernels behind the C ABI (include/moe_capi.h):
 //
 //   dynamic_dispatch  -> moe_dynamic_dispatch_host  (stable counting sort)

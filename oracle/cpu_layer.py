@@ -136,3 +136,38 @@ def _cpu_layer_bench(S, TD, HD, E, k, min_seconds, max_passes, weight_pool, laye
                    f"gate/FFN numpy/OpenBLAS fp32 on {blas_threads()} threads ({os.cpu_count()} host "
                    f"cores); {t_all:.1f} s timed"),
     }
+
+
+def cpu_layer_1thread(S, TD, HD, E, k, tokens=2048, min_seconds=3.0, weight_pool=8):
+    """The same layer pass on ONE host thread (BLAS limited to 1) over the
+    first ``tokens`` tokens of the workload, repeated until ``min_seconds``;
+    median pass.  Reported beside the all-core number."""
+    from threadpoolctl import threadpool_limits
+
+    n = min(S, tokens)
+    with threadpool_limits(limits=1, user_api="blas"):
+        L = CpuLayer(n, TD, HD, E, k, weight_pool=weight_pool)
+        ts, t_all = [], 0.0
+        while t_all < min_seconds or not ts:
+            t = L.run()["total"]
+            ts.append(t)
+            t_all += t
+    ts.sort()
+    med = ts[len(ts) // 2]
+    return {"value": n / med, "unit": "tokens/s", "cores": 1, "seconds_per_pass": med,
+            "sample": f"{len(ts)} passes over {n} of the {S} tokens ({n * k} slots, {E} experts), "
+                      f"BLAS on 1 thread, median pass"}
+
+
+def routing_1thread(S, TD, E, k, C=0.0, seed=2303061820, reps=5):
+    """The reference's routing functions alone (dynamic_dispatch, combine<float>,
+    and static_dispatch + its combine when C > 0) on one thread, with the
+    reference Batch prebuilt outside the timed region (oracle/ref_capi.cpp
+    ref_time_routing): the CPU number the GPU route kernel replaces.  Routing
+    uses the workload's own top-k of the fp32 gate logits."""
+    sc = OL.init_scales(TD, 1)
+    X = OL.bf16_to_f32(OL.synth_bf16((S, TD), seed, OL.T_X, sc["x"]))
+    Wg = OL.bf16_to_f32(OL.synth_bf16((E, TD), seed, OL.T_WG, sc["wg"]))
+    idx, w = OL.topk_from_logits(OL.gate_logits(X, Wg), k)
+    r = N.ref_time_routing(idx, w.astype(np.float64), E, C, reps)
+    return {kk: float(v) for kk, v in r.items()}

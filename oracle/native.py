@@ -63,6 +63,7 @@ def ref_lib():
         _sig(lib.ref_save_synthetic_trace, _I, _I, _I, _I, _I, _D, _D, _D, C.c_uint64, C.c_char_p)
         _sig(lib.ref_trace_roundtrip, _I, C.c_char_p, C.c_char_p, _P)
         _sig(lib.ref_trace_loads, _I, C.c_char_p, _P, _I)
+        _sig(lib.ref_time_routing, _I, _P, _P, _I, _I, _I, _D, _I, _P)
         _ref = lib
     return _ref
 
@@ -107,6 +108,21 @@ def ref_dynamic_dispatch(experts: np.ndarray, E: int, weights=None, mode_static=
     if rc:
         raise OracleError(ref_lib().ref_last_error().decode())
     return order[:S * k], counts[:E], splits[:E + 1]
+
+
+def ref_time_routing(experts: np.ndarray, weights: np.ndarray, E: int, C_: float = 0.0, reps: int = 5):
+    """The reference's routing functions on one thread, Batch prebuilt (no
+    marshalling in the timed region); best of ``reps`` seconds per call."""
+    ex = np.ascontiguousarray(experts, dtype=np.int32)
+    S, k = ex.shape
+    wt = np.ascontiguousarray(weights, dtype=np.float64)
+    sec = np.zeros(4, np.float64)
+    if ref_lib().ref_time_routing(_ptr(ex), _ptr(wt), S, k, E, float(C_), reps, _ptr(sec)):
+        raise OracleError(ref_lib().ref_last_error().decode())
+    out = {"dynamic_dispatch": sec[0], "combine_dynamic": sec[1]}
+    if C_ > 0:
+        out.update({"static_dispatch": sec[2], "combine_static": sec[3]})
+    return out
 
 
 def ref_static_dispatch(experts: np.ndarray, E: int, C_: float, weights=None, mode_static=True):

@@ -8,6 +8,7 @@
 //
 // Because the whole translation unit is compiled with -Dmoesim=moesim_ref,
 // every `moesim::` below names the reference implementation.
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <optional>
@@ -352,6 +353,44 @@ int ref_trace_loads(const char* path, double* share, int cap) {
     if (n > cap) throw std::runtime_error("load buffer too small");
     for (long j = 0; j < L.share.cols(); ++j)
       for (long i = 0; i < L.share.rows(); ++i) share[j * L.share.rows() + i] = L.share(i, j);
+  });
+}
+
+// The reference's routing tier timed on one host thread WITHOUT marshalling:
+// the Batch (nested std::vector<TokenAssignment>) is built once, untimed, and
+// each call below is the reference's own function on it, best of `reps`:
+//   sec[0] dynamic_dispatch          gating.cpp:58-86
+//   sec[1] combine<float> (dynamic)   gating.hpp:107-141, payload = k*S floats
+//   sec[2] static_dispatch (C)       gating.cpp:30-56   (skipped when C <= 0)
+//   sec[3] combine<float> (static)   gating.hpp:147-184 (skipped when C <= 0)
+int ref_time_routing(const int* experts, const double* weights, int S, int k, int E, double C,
+                     int reps, double* sec) {
+  return guarded([&] {
+    using clk = std::chrono::steady_clock;
+    const moesim::Batch b = make_batch(experts, weights, S, k);
+    const std::vector<float> pay(static_cast<std::size_t>(S) * k, 1.0f);
+    for (int i = 0; i < 4; ++i) sec[i] = -1.0;
+    auto best = [&](int slot, auto&& fn) {
+      for (int r = 0; r < reps; ++r) {
+        const auto t0 = clk::now();
+        fn();
+        const double s = std::chrono::duration<double>(clk::now() - t0).count();
+        if (sec[slot] < 0 || s < sec[slot]) sec[slot] = s;
+      }
+    };
+    const auto dcfg = cfg_of(E, k, 0.0, false);
+    std::size_t sink = 0;
+    best(0, [&] { sink += moesim::dynamic_dispatch(b, dcfg).order.size(); });
+    const auto dplan = moesim::dynamic_dispatch(b, dcfg);
+    best(1, [&] { sink += moesim::combine(dplan, b, std::span<const float>(pay)).size(); });
+    if (C > 0) {
+      const auto scfg = cfg_of(E, k, C, true);
+      best(2, [&] { sink += moesim::static_dispatch(b, scfg).dropped.size(); });
+      const auto splan = moesim::static_dispatch(b, scfg);
+      const std::vector<float> spay(static_cast<std::size_t>(E) * splan.capacity, 1.0f);
+      best(3, [&] { sink += moesim::combine(splan, b, std::span<const float>(spay)).size(); });
+    }
+    if (sink == static_cast<std::size_t>(-1)) sec[0] = 0;  // keep the calls observable
   });
 }
 

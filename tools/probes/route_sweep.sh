@@ -2,7 +2,7 @@
 # ncu-timed route kernel for several per-block chunk sizes (units of 512 slots)
 for c in 1 2 4 8; do
   MOE_ROUTE_CHUNK_UNITS=$c ncu --metrics gpu__time_duration.sum --clock-control none -k regex:route_kernel --csv \
-    --log-file gpurun_out/route_sweep_$c.csv python tools/route_bench.py > /dev/null 2>&1
+    --log-file gpurun_out/route_sweep_$c.csv python tools/probes/route_bench.py > /dev/null 2>&1
   python3 - "$c" <<'PY'
 import csv, sys
 c = sys.argv[1]
