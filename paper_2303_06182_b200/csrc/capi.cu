@@ -397,6 +397,8 @@ int moe_gate_topk(moe_ctx* ctx, const void* X, const void* Wg, int S, int TD, in
   st = encode_bf16(&tmWg, Wg, E, TD, gate_box_rows(E), moe::gate_box_cols(E));
   if (st) return st;
   GateArgs a{S, TD, E, k, idx, w, logits};
+  a.X = X;
+  a.Wg = Wg;
   e = launch_gate(tmX, tmWg, a, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "gate launch");
   return MOE_OK;
@@ -707,6 +709,8 @@ int moe::capi::layer_front(moe_layer* L, const void* X, int S, const int32_t* id
   }
   if (!idx_in) {
     GateArgs ga{S, TD, E, k, L->idx.p, L->w.p, d.keep_logits ? L->logits.p : nullptr};
+    ga.X = X;
+    ga.Wg = L->Wg;
     cudaError_t e = launch_gate(L->tmX, L->tmWg, ga, s);
     if (e != cudaSuccess) return cuda_fail(e, "gate launch");
   }

@@ -215,6 +215,8 @@ int ep_forward_nccl(moe_ep* P, const void* X, int S, void* out, cudaStream_t s, 
   // 1. gate + route keyed by (device, local expert) -- local
   mark(0);
   GateArgs ga{S, TD, E, k, P->idx.p, P->w.p, nullptr};
+  ga.X = X;
+  ga.Wg = P->Wg;
   cudaError_t ce = launch_gate(P->tmX, P->tmWg, ga, s);
   if (ce != cudaSuccess) return cuda_fail(ce, "gate launch");
   st = route_common(P->ctx, P->idx.p, S, k, E, 0, P->counts.p, P->splits.p, P->order.p, P->pos.p,

@@ -685,6 +685,8 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   }
   // 1. gate + keyed route (local)
   GateArgs ga{S, TD, E, k, P->idx.p, P->w.p, nullptr};
+  ga.X = X;
+  ga.Wg = P->Wg;
   mark(0);
   cudaError_t ce = launch_gate(P->tmX, P->tmWg, ga, s);
   if (ce != cudaSuccess) return cuda_fail(ce, "gate launch");

@@ -260,14 +260,15 @@ __global__ void __launch_bounds__(256, 1)
         }
         fence_proxy_async_global();
       }
-      const uint32_t bytes = kABytes + ((g.dbg & 1) ? 0 : KCH * nrows * kChunkK * 2);
+      const uint32_t bytes = ((g.dbg & 16) ? 0 : kABytes) + ((g.dbg & 1) ? 0 : KCH * nrows * kChunkK * 2);
       for (int kb = 0; kb < KB; ++kb) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         ptx::mbar_arrive_expect_tx(&full[stage], bytes);
 #pragma unroll
         for (int c = 0; c < KCH; ++c) {
           const int k0 = kb * Cfg::kStageK + c * kChunkK;
-          if (g.packed)
+          if (g.dbg & 16) {
+          } else if (g.packed)
             ptx::tma_load_2d(sA + stage * kABytes + c * Cfg::kAChunk, tA, &full[stage], 0,
                              (a_tile + kb * KCH + c) * kBlockM, pol_w);
           else

@@ -217,6 +217,9 @@ __global__ void __launch_bounds__(256, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
   }
   ptx::tc_fence_before();
+  // the CTA barrier orders warp 2's TMEM-slot write before every warp's read
+  // (barrier.cluster alone is not a CTA-scope smem barrier to racecheck)
+  __syncthreads();
   ptx::cluster_sync();  // barriers and TMEM of both CTAs exist before any remote use
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;

@@ -62,6 +62,9 @@ constexpr int kPartOffset = 16 * 1024;
 #define MOE_GATE_MAX_STAGES 8
 #endif
 constexpr int kMaxStages = MOE_GATE_MAX_STAGES;
+// MOE_GATE_PROF stamps per CTA: entry, after griddepcontrol.wait, first stage
+// full (MMA thread), last MMA committed, accumulator ready (epilogue), end
+constexpr int kProf = 6;
 
 struct GateLayout {
   int e_pad;      // E rounded up to 16
@@ -134,7 +137,7 @@ __device__ __forceinline__ void gate_epilogue(const GateArgs& a, uint32_t tmem_b
   const int lane = threadIdx.x & 31;
   ptx::mbar_wait(tfull, 0);
   ptx::tc_fence_after();
-  if (a.prof && threadIdx.x == 0) a.prof[3 * blockIdx.x + 1] = gate_clock();
+  if (a.prof && threadIdx.x == 0) a.prof[kProf * blockIdx.x + 4] = gate_clock();
   const int q = warp & 3;
   const int half = warp >> 2;
   const int tl = q * 32 + lane;  // token within the tile
@@ -281,13 +284,14 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
   static_assert(SPLIT ? (C >= 2 && C <= 8) : (C == 1 || C == 2 || C == 4), "cluster shape");
   static_assert(BK == 32 || BK == 64, "32-deep (64-byte swizzle) or 64-deep (128-byte) k-blocks");
   constexpr int kABytes = kBlockM * BK * 2;
-  if (a.prof && threadIdx.x == 0) a.prof[3 * blockIdx.x] = gate_clock();
+  if (a.prof && threadIdx.x == 0) a.prof[kProf * blockIdx.x] = gate_clock();
   const GateLayout L = gate_layout(a.E, BK);
   const int stage_bytes = kABytes + L.b_rows * BK * 2;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.stages * stage_bytes);
   uint64_t* empty = full + L.stages;
   uint64_t* tfull = empty + L.stages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* pbar = tfull + 2;  // split-K: the followers' partials landed (leader)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -308,6 +312,7 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
       ptx::mbar_init(&empty[s], SPLIT ? 1 : C);  // one MMA commit from every CTA that reads the stage
     }
     ptx::mbar_init(tfull, 1);
+    if (SPLIT) ptx::mbar_init(pbar, 1);
     ptx::fence_barrier_init();
   }
   if (warp == 2) {
@@ -324,25 +329,39 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
   if (C > 1) ptx::cluster_sync();  // peers' barriers exist before any multicast lands
   pdl_trigger();
   pdl_wait();  // X and the routing buffers belong to the previous kernel until here
+  if (a.prof && threadIdx.x == 0) a.prof[kProf * blockIdx.x + 1] = gate_clock();
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ---------------------------------------------------- TMA producer
-      const uint64_t pol_x = ptx::policy_evict_first();
-      const uint64_t pol_w = ptx::policy_evict_last();
-      // this CTA's share of the Wg boxes (all of them without multicast)
-      constexpr int MC = SPLIT ? 1 : C;  // CTAs sharing each Wg box
-      const int per = L.n_box / MC;
-      const int b_lo = MC > 1 ? crank * per : 0;
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int kb = kb_lo; kb < kb_hi; ++kb) {
-        // free once every CTA of the cluster has consumed the stage
-        ptx::mbar_wait(&empty[stage], phase ^ 1);
-        ptx::mbar_arrive_expect_tx(&full[stage], stage_bytes);
+    // ------------------------------------------------------ TMA producer
+    // A thread's bulk-tensor requests complete one after another (~0.25-0.3
+    // us each for 8-64 KB, tools/probes/tma_l2_probe.cu: one issuing thread
+    // streams ~50 GB/s, four ~170 GB/s), so the stage's requests rotate over
+    // the 32 lanes of the warp: consecutive requests come from different
+    // threads and overlap.  The whole warp waits on the stage; one lane arms it.
+    const uint64_t pol_x = ptx::policy_evict_first();
+    const uint64_t pol_w = ptx::policy_evict_last();
+    // this CTA's share of the Wg boxes (all of them without multicast)
+    constexpr int MC = SPLIT ? 1 : C;  // CTAs sharing each Wg box
+    const int per = L.n_box / MC;
+    const int b_lo = MC > 1 ? crank * per : 0;
+    const int nreq = 1 + per;  // requests per stage
+    const int spread = a.tma_spread ? 32 : 1;
+    int stage = 0;
+    uint32_t phase = 0;
+    int slot = 0;  // request counter (lane = slot % spread)
+    for (int kb = kb_lo; kb < kb_hi; ++kb) {
+      // free once every CTA of the cluster has consumed the stage
+      ptx::mbar_wait(&empty[stage], phase ^ 1);
+      if (a.dbg & 2) {  // ablation: no loads at all
+        if (lane == 0) ptx::mbar_arrive(&full[stage]);
+      } else {
+        if (lane == 0)
+          ptx::mbar_arrive_expect_tx(&full[stage], stage_bytes - ((a.dbg & 4) ? L.b_rows * BK * 2 : 0) -
+                                                       ((a.dbg & 8) ? kABytes : 0));
         uint8_t* st = smem + stage * stage_bytes;
-        ptx::tma_load_2d(st, &tmX, &full[stage], kb * BK, tok0, pol_x);
-        for (int b = b_lo; b < b_lo + per; ++b) {
+        if (!(a.dbg & 8) && lane == slot % spread) ptx::tma_load_2d(st, &tmX, &full[stage], kb * BK, tok0, pol_x);
+        for (int b = b_lo; b < b_lo + per && !(a.dbg & 4); ++b) {
+          if (lane != (slot + 1 + b - b_lo) % spread) continue;
           const int r = b * L.box_rows;
           if (MC > 1)
             ptx::tma_load_2d_mc(st + kABytes + r * BK * 2, &tmWg, &full[stage], kb * BK, r,
@@ -350,10 +369,11 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
           else
             ptx::tma_load_2d(st + kABytes + r * BK * 2, &tmWg, &full[stage], kb * BK, r, pol_w);
         }
-        if (++stage == L.stages) {
-          stage = 0;
-          phase ^= 1;
-        }
+        slot += nreq;
+      }
+      if (++stage == L.stages) {
+        stage = 0;
+        phase ^= 1;
       }
     }
     __syncwarp();
@@ -369,10 +389,11 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
       for (int kb = kb_lo; kb < kb_hi; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
+        if (a.prof && kb == kb_lo) a.prof[kProf * blockIdx.x + 2] = gate_clock();
         const uint32_t a0 = ptx::smem_u32(smem + stage * stage_bytes);
         const uint32_t b0 = a0 + kABytes;
 #pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk) {
+        for (int kk = 0; kk < BK / 16 && !(a.dbg & 1); ++kk) {
           const uint32_t acc = (kb != kb_lo || kk != 0) ? 1u : 0u;
           ptx::mma_bf16(tmem_base, desc(a0 + kk * 32), desc(b0 + kk * 32), id0, acc);
           if (n1 > 0)
@@ -389,42 +410,56 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
         }
       }
       ptx::mma_commit(tfull);
+      if (a.prof) a.prof[kProf * blockIdx.x + 3] = gate_clock();
     }
     __syncwarp();
   }
 
   if constexpr (SPLIT) {
-    // every CTA's MMAs retired (tfull) before the cluster barrier, so the
-    // leader's stage buffers are free for the followers' partials
+    // Followers: TMEM partial logits -> own smem (their stage buffers are free
+    // once their tfull fired), then ONE bulk DSMEM copy into the leader's
+    // partial slot, counted on the leader's pbar.  The cluster barrier in
+    // between keeps the copies out of the leader's stage buffers until the
+    // leader's MMAs retired.  (Per-thread st.shared::cluster stores of the
+    // same 64 KB took ~4 us at MT; one bulk copy per follower streams it.)
+    const int pstride = (a.E + 31) / 32 * 32 + 4;  // floats per token row (+4: bank spread)
+    const uint32_t part_bytes = static_cast<uint32_t>(kBlockM * pstride * 4);
+    float* part = reinterpret_cast<float*>(smem + kPartOffset);
     ptx::mbar_wait(tfull, 0);
     ptx::tc_fence_after();
-    ptx::cluster_sync();
-    const int pstride = (a.E + 31) / 32 * 32 + 4;  // floats per token row (+4: bank spread)
-    float* part = reinterpret_cast<float*>(smem + kPartOffset);
     if (crank != 0) {
       const int q = warp & 3, half = warp >> 2, tl = q * 32 + lane;
       const int nchunk = (a.E + 31) / 32, split = (nchunk + 1) / 2;
       const int c_begin = half ? split * 32 : 0, c_end = half ? nchunk * 32 : split * 32;
-      const uint32_t row = ptx::smem_u32(part + (static_cast<size_t>(crank - 1) * kBlockM + tl) * pstride);
-      const uint32_t dst = ptx::cluster_map(row, 0);
+      float* row = reinterpret_cast<float*>(smem) + static_cast<size_t>(tl) * pstride;
       for (int c0 = c_begin; c0 < c_end; c0 += 32) {
         uint32_t r[32];
         ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + c0, r);
         ptx::tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-          ptx::st_cluster_v4(dst + (c0 + 4 * i) * 4, r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+          *reinterpret_cast<uint4*>(row + c0 + 4 * i) = make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
       }
+      ptx::fence_proxy_async_smem();
       ptx::tc_fence_before();
+    } else if (threadIdx.x == 0) {
+      ptx::mbar_arrive_expect_tx(pbar, (C - 1) * part_bytes);
     }
-    ptx::cluster_sync();  // partials visible in the leader
-    if (crank == 0) gate_epilogue<K>(a, tmem_base, tfull, tok0, smem, part, C - 1, pstride);
+    __syncthreads();
+    ptx::cluster_sync();  // leader's stage buffers free; every follower's rows staged
+    if (crank != 0 && threadIdx.x == 0)
+      ptx::bulk_copy_to_cluster(ptx::cluster_map(ptx::smem_u32(part) + (crank - 1) * part_bytes, 0), smem,
+                                part_bytes, ptx::cluster_map(ptx::smem_u32(pbar), 0));
+    if (crank == 0) {
+      ptx::mbar_wait(pbar, 0);
+      gate_epilogue<K>(a, tmem_base, tfull, tok0, smem, part, C - 1, pstride);
+    }
   } else {
     gate_epilogue<K>(a, tmem_base, tfull, tok0, smem);
   }
 
   __syncthreads();
-  if (a.prof && threadIdx.x == 0) a.prof[3 * blockIdx.x + 2] = gate_clock();
+  if (a.prof && threadIdx.x == 0) a.prof[kProf * blockIdx.x + 5] = gate_clock();
   ptx::tc_fence_after();
   if (warp == 2) {
     if (L.e_pad <= 32) ptx::tmem_dealloc<32>(tmem_base);
@@ -433,8 +468,10 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
     else if (L.e_pad <= 256) ptx::tmem_dealloc<256>(tmem_base);
     else ptx::tmem_dealloc<512>(tmem_base);
   }
-  // peers' last MMA commits arrive on this CTA's empty barriers: stay alive
-  if (!SPLIT && C > 1) ptx::cluster_sync();
+  // peers' last MMA commits arrive on this CTA's empty barriers, and the
+  // followers' smem is the source of bulk copies until the leader saw pbar:
+  // stay alive
+  if (C > 1) ptx::cluster_sync();
 }
 
 __device__ __forceinline__ uint8_t* aligned_smem() {
@@ -465,6 +502,111 @@ const void* split_fn(int C, int k) {
     case 4: return gate_fn<4, 64, true>(k);
     default: return gate_fn<8, 64, true>(k);
   }
+}
+
+// ---------------------------------------------------------------- small-E gate
+// Few experts (E <= 32: configs[0]'s E = 8): the gate is a bandwidth-bound
+// GEMV-like pass over X (2 * E flop per byte of X), so it runs on the CUDA
+// cores instead of tcgen05: no TMEM allocation, TMA pipeline or cluster
+// barriers (whose fixed costs were ~5 us of the 9 us tcgen05 gate at
+// configs[0]).  Wg [E, TD] is staged in shared memory BEFORE
+// griddepcontrol.wait (weights are never written by the previous kernel of
+// the chain); one warp per token then streams its X row with 16-byte loads,
+// keeps E fp32 partial sums per lane, all-reduces them with butterflies and
+// applies the same top-k / weight rule as the tcgen05 epilogue.
+constexpr int kSmallMaxE = 32;
+constexpr int kSmallThreads = 512;
+constexpr int kSmallMaxSmem = 64 * 1024;
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
+  const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(u[i] << 16);
+    f[2 * i + 1] = __uint_as_float(u[i] & 0xffff0000u);
+  }
+}
+
+template <int EM, int K>
+__global__ void __launch_bounds__(kSmallThreads) gate_small_kernel(GateArgs a) {
+  extern __shared__ uint4 swg[];  // Wg [E][TD] bf16
+  const int vpr = a.TD / 8;       // 16-byte vectors per row
+  const uint4* wg = reinterpret_cast<const uint4*>(a.Wg);
+  for (int i = threadIdx.x; i < a.E * vpr; i += blockDim.x) swg[i] = __ldg(wg + i);
+  __syncthreads();
+  pdl_trigger();
+  pdl_wait();  // X belongs to the previous kernel until here
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int t = blockIdx.x * wpb + (threadIdx.x >> 5); t < a.S; t += gridDim.x * wpb) {
+    const uint4* xr = reinterpret_cast<const uint4*>(a.X) + static_cast<size_t>(t) * vpr;
+    float acc[EM];
+#pragma unroll
+    for (int e = 0; e < EM; ++e) acc[e] = 0.f;
+#pragma unroll 4
+    for (int v = lane; v < vpr; v += 32) {
+      float xf[8];
+      bf16x8_to_f32(__ldcs(xr + v), xf);
+#pragma unroll
+      for (int e = 0; e < EM; ++e) {
+        if (e < a.E) {
+          float wf[8];
+          bf16x8_to_f32(swg[e * vpr + v], wf);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[e] = fmaf(xf[i], wf[i], acc[e]);
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < EM; ++e)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+    // every lane holds all E logits: same selection as gate_epilogue
+    float bv[K];
+    int bi[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      bv[j] = -INFINITY;
+      bi[j] = 0x7fffffff;
+    }
+#pragma unroll
+    for (int e = 0; e < EM; ++e)
+      if (e < a.E) topk_insert<K>(bv, bi, acc[e], e);
+    if (a.logits) {
+#pragma unroll
+      for (int e = 0; e < EM; ++e)
+        if (e == lane && e < a.E) a.logits[static_cast<size_t>(t) * a.E + e] = acc[e];
+    }
+    if (lane == 0) {
+      const int k = a.k;
+      float ex[K];
+      float sum = 0.f;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        ex[j] = (j < k) ? expf(bv[j] - bv[0]) : 0.f;
+        sum += ex[j];
+      }
+      float accw = 0.f;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if (j < k) {
+          const float wj = (j < k - 1) ? ex[j] / sum : 1.f - accw;
+          accw += wj;
+          a.idx[static_cast<size_t>(t) * k + j] = bi[j];
+          a.w[static_cast<size_t>(t) * k + j] = wj;
+        }
+      }
+    }
+  }
+}
+
+template <int EM>
+cudaError_t launch_gate_small_e(const GateArgs& a, int grid, int smem, cudaStream_t stream) {
+  const dim3 g(grid), b(kSmallThreads);
+  if (a.k == 1) return launch_chain(gate_small_kernel<EM, 1>, g, b, smem, stream, false, a);
+  if (a.k == 2) return launch_chain(gate_small_kernel<EM, 2>, g, b, smem, stream, false, a);
+  if (a.k <= 4) return launch_chain(gate_small_kernel<EM, 4>, g, b, smem, stream, false, a);
+  return launch_chain(gate_small_kernel<EM, 8>, g, b, smem, stream, false, a);
 }
 
 // every gate kernel may use up to the layout maximum (stages are sized to
@@ -501,6 +643,17 @@ cudaError_t gate_prepare(int E) {
     }
     for (const void* fn : fns) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAttr);
+      if (e != cudaSuccess && err == cudaSuccess) err = e;
+    }
+    const void* small[] = {
+        reinterpret_cast<const void*>(gate_small_kernel<8, 1>), reinterpret_cast<const void*>(gate_small_kernel<8, 2>),
+        reinterpret_cast<const void*>(gate_small_kernel<8, 4>), reinterpret_cast<const void*>(gate_small_kernel<8, 8>),
+        reinterpret_cast<const void*>(gate_small_kernel<16, 1>), reinterpret_cast<const void*>(gate_small_kernel<16, 2>),
+        reinterpret_cast<const void*>(gate_small_kernel<16, 4>), reinterpret_cast<const void*>(gate_small_kernel<16, 8>),
+        reinterpret_cast<const void*>(gate_small_kernel<32, 1>), reinterpret_cast<const void*>(gate_small_kernel<32, 2>),
+        reinterpret_cast<const void*>(gate_small_kernel<32, 4>), reinterpret_cast<const void*>(gate_small_kernel<32, 8>)};
+    for (const void* fn : small) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallMaxSmem);
       if (e != cudaSuccess && err == cudaSuccess) err = e;
     }
   });
@@ -617,8 +770,27 @@ cudaError_t launch_gate_bk(const CUtensorMap& tmX, const CUtensorMap& tmWg, cons
 
 }  // namespace
 
+bool gate_small(int E, int TD) {
+  static const int env = [] {
+    const char* v = getenv("MOE_GATE_SMALL");
+    return v ? atoi(v) : 1;
+  }();
+  return env != 0 && E <= kSmallMaxE && TD % 8 == 0 && E * TD * 2 <= kSmallMaxSmem;
+}
+
 cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateArgs& a,
                         cudaStream_t stream) {
+  if (a.X && a.Wg && a.k >= 1 && a.k <= kMaxK && a.E >= a.k && gate_small(a.E, a.TD)) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int wpb = kSmallThreads / 32;
+    const int grid = std::max(1, std::min((a.S + wpb - 1) / wpb, 2 * sms));
+    const int smem = a.E * a.TD * 2;
+    if (a.E <= 8) return launch_gate_small_e<8>(a, grid, smem, stream);
+    if (a.E <= 16) return launch_gate_small_e<16>(a, grid, smem, stream);
+    return launch_gate_small_e<32>(a, grid, smem, stream);
+  }
   const bool wide = gate_wide(a.E);
   if (a.k < 1 || a.k > kMaxK || a.E > 512 || a.E < a.k || (a.TD % (wide ? 64 : kBlockK)) != 0)
     return cudaErrorInvalidValue;
@@ -645,34 +817,52 @@ cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const G
   const int C = shape.first;
   const bool split = shape.second;
   static const bool prof = getenv("MOE_GATE_PROF") != nullptr;
+  static const int dbg = getenv("MOE_GATE_DBG") ? atoi(getenv("MOE_GATE_DBG")) : 0;
   GateArgs b = a;
+  b.dbg = dbg;
+  b.tma_spread = tma_spread_enabled();
   static unsigned long long* prof_buf = nullptr;
   const int ctas = split ? tiles * C : tiles;
   if (prof) {
-    if (!prof_buf) cudaMalloc(&prof_buf, 3 * 4096 * sizeof(unsigned long long));
+    if (!prof_buf) cudaMalloc(&prof_buf, kProf * 4096 * sizeof(unsigned long long));
+    if (prof_buf) cudaMemsetAsync(prof_buf, 0, kProf * 4096 * sizeof(unsigned long long), stream);
     b.prof = ctas <= 4096 ? prof_buf : nullptr;
   }
   const cudaError_t e = wide ? launch_gate_bk<64>(tmX, tmWg, b, C, split, tiles, L.smem, stream)
                              : launch_gate_bk<kBlockK>(tmX, tmWg, b, C, split, tiles, L.smem, stream);
   if (!b.prof || e != cudaSuccess) return e;
-  // experiments only: per-CTA mainloop / epilogue split of this launch (split
-  // followers record their mainloop only)
-  std::vector<unsigned long long> h(3 * (size_t)ctas);
+  // experiments only: mean per-CTA phase times of this launch (split
+  // followers have no epilogue stamps and are left out)
+  std::vector<unsigned long long> h(kProf * (size_t)ctas);
   cudaStreamSynchronize(stream);
   cudaMemcpy(h.data(), prof_buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-  unsigned long long t0 = ~0ull, t2 = 0;
-  double m = 0, ep = 0;
+  unsigned long long t0 = ~0ull, t5 = 0;
+  double ph[kProf - 1] = {0, 0, 0, 0, 0};
   int nl = 0;
   for (int i = 0; i < ctas; ++i) {
     if (split && i % C) continue;
+    const unsigned long long* p = &h[kProf * (size_t)i];
     ++nl;
-    t0 = std::min(t0, h[3 * i]);
-    t2 = std::max(t2, h[3 * i + 2]);
-    m += (double)(h[3 * i + 1] - h[3 * i]);
-    ep += (double)(h[3 * i + 2] - h[3 * i + 1]);
+    t0 = std::min(t0, p[0]);
+    t5 = std::max(t5, p[5]);
+    for (int j = 0; j < kProf - 1; ++j) ph[j] += (double)(p[j + 1] - p[j]);
   }
-  fprintf(stderr, "[gate prof] %d CTAs (cluster %d, %s): mean mainloop+reduce %.1f us, mean epilogue %.1f us, span %.1f us\n",
-          ctas, C, split ? "split-K" : "multicast", m / nl * 1e-3, ep / nl * 1e-3, (t2 - t0) * 1e-3);
+  if (const char* path = getenv("MOE_GATE_PROF_DUMP")) {  // raw stamps, one CTA per line
+    if (FILE* f = fopen(path, "a")) {
+      for (int i = 0; i < ctas; ++i) {
+        fprintf(f, "%d", i);
+        for (int j = 0; j < kProf; ++j) fprintf(f, " %llu", h[kProf * (size_t)i + j] - t0);
+        fprintf(f, "\n");
+      }
+      fprintf(f, "--\n");
+      fclose(f);
+    }
+  }
+  fprintf(stderr,
+          "[gate prof] %d CTAs (cluster %d, %s): mean us: pdl-wait %.1f | first stage %.1f | MMA loop %.1f | "
+          "to acc-ready %.1f | epilogue %.1f ; span %.1f\n",
+          ctas, C, split ? "split-K" : "multicast", ph[0] / nl * 1e-3, ph[1] / nl * 1e-3, ph[2] / nl * 1e-3,
+          ph[3] / nl * 1e-3, ph[4] / nl * 1e-3, (t5 - t0) * 1e-3);
   return e;
 }
 

@@ -38,6 +38,14 @@ class Context:
             cls._by_device[device] = Context(device)
         return cls._by_device[device]
 
+    @classmethod
+    def close_all(cls):
+        """Destroy every cached context (tools / sanitizer runs: no live
+        layer may still use them)."""
+        for c in cls._by_device.values():
+            c.lib.moe_ctx_destroy(c.h)
+        cls._by_device.clear()
+
     @property
     def sm_count(self) -> int:
         return self.lib.moe_ctx_sm_count(self.h)

@@ -19,6 +19,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="lm")
 ap.add_argument("--steps", type=int, default=4)
 ap.add_argument("--ep", action="store_true")
+ap.add_argument("--tile-n", type=int, default=0)
 a = ap.parse_args()
 S, TD, HD, E, k, mode, C, _ = WORKLOADS[a.workload]
 shape = LayerShape(TD, HD, E, k)
@@ -33,7 +34,7 @@ if a.ep:
         layer.forward(x, out=out)
     layer.check_errors()
 else:
-    layer = MoeLayer(shape, S, mode=mode, capacity_factor=C or 1.0, weights=w)
+    layer = MoeLayer(shape, S, mode=mode, capacity_factor=C or 1.0, weights=w, tile_n=a.tile_n)
     for _ in range(a.steps):
         layer.forward(x, out)
     layer.check_errors()

@@ -27,4 +27,5 @@ for tool in $TOOLS; do
   rc=$?
   echo "$tool ep2 rc=$rc $(grep -h 'ERROR SUMMARY\|RACECHECK SUMMARY' $out/${tool}_ep2.log | tail -1)" >> $out/summary.txt
 done
-cat $out/summary.txt
+python tools/sanitize_summary.py $out > $out/classified.txt
+cat $out/summary.txt $out/classified.txt
