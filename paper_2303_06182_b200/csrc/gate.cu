@@ -46,6 +46,11 @@ namespace moe {
 namespace {
 
 constexpr int kBlockM = 128;
+// 8 warps join the top-K epilogue, two per TMEM lane quadrant, each scanning
+// half of the expert columns (16 warps, a quarter each, measured equal: LM
+// epilogue 5.0 vs 5.1 us)
+constexpr int kThreads = 256;
+constexpr int kParts = kThreads / 128;
 // 32-deep k-blocks (64-byte rows, 64-byte swizzle): a stage is 8 KB of X +
 // b_rows x 64 B of Wg (40 KB at E = 512), so five stages fit and the loads of
 // four k-blocks are in flight while one is multiplied (at 64-deep stages only
@@ -54,7 +59,7 @@ constexpr int kBlockK = 32;
 constexpr int kMaxK = 8;
 constexpr int kMaxSmem = 220 * 1024;
 // split-K partial logits in the leader's smem start past the top-K merge
-// scratch of the epilogue (kBlockM x 8 x (4 + 4) bytes)
+// scratch of the epilogue ((kParts - 1) x kBlockM x 8 x (4 + 4) bytes)
 constexpr int kPartOffset = 16 * 1024;
 // more stages (16) measured equal at MT and cfg1 (same box): the gate is not
 // bound by loads in flight
@@ -121,13 +126,18 @@ __device__ __forceinline__ void topk_insert(float (&bv)[K], int (&bi)[K], float 
   }
 }
 
-// Top-K epilogue of one 128-token tile (all 8 warps of the CTA): TMEM lane =
-// token, columns = expert logits.  Warps q and q+4 share TMEM lane quadrant q
-// (tokens 32q..32q+31); warps 0-3 scan the first half of the expert columns,
-// warps 4-7 the second half, then the two partial top-K lists are merged
+// Top-K epilogue of one 128-token tile (all warps of the CTA): TMEM lane =
+// token, columns = expert logits.  Warps q, q+4, ... share TMEM lane quadrant
+// q (tokens 32q..32q+31), each scanning 1/kParts of the expert columns; the
+// partial top-K lists are then merged
 // through shared memory (the stage buffers, free once tfull fired).
 // Split-K: `part` holds nparts follower partials, [part][token lane][pstride]
 // floats; they are added to this CTA's TMEM logits in rank order.
+__device__ __forceinline__ void reg_fence32(uint32_t (&r)[32]) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) asm volatile("" : "+r"(r[i]));
+}
+
 template <int K>
 __device__ __forceinline__ void gate_epilogue(const GateArgs& a, uint32_t tmem_base,
                                               uint64_t* tfull, int tok0, uint8_t* smem,
@@ -139,13 +149,12 @@ __device__ __forceinline__ void gate_epilogue(const GateArgs& a, uint32_t tmem_b
   ptx::tc_fence_after();
   if (a.prof && threadIdx.x == 0) a.prof[kProf * blockIdx.x + 4] = gate_clock();
   const int q = warp & 3;
-  const int half = warp >> 2;
+  const int part_id = warp >> 2;  // column range of this warp
   const int tl = q * 32 + lane;  // token within the tile
   const int tok = tok0 + tl;
   const int nchunk = (a.E + 31) / 32;
-  const int split = (nchunk + 1) / 2;
-  const int c_begin = half ? split * 32 : 0;
-  const int c_end = half ? nchunk * 32 : split * 32;
+  const int c_begin = part_id * nchunk / kParts * 32;
+  const int c_end = (part_id + 1) * nchunk / kParts * 32;
   float bv[K];
   int bi[K];
 #pragma unroll
@@ -157,10 +166,12 @@ __device__ __forceinline__ void gate_epilogue(const GateArgs& a, uint32_t tmem_b
   // select chains instead of one vote-guarded insert per value)
   float ov0 = -INFINITY, ov1 = -INFINITY;
   int oi0 = 0x7fffffff, oi1 = 0x7fffffff;
-  for (int c0 = c_begin; c0 < c_end; c0 += 32) {
-    uint32_t r[32];
-    ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + c0, r);
-    ptx::tmem_ld_wait();
+  // TMEM loads are software-pipelined: the next 32 columns are in flight
+  // while this chunk is scanned (tcgen05.wait::ld waits for every load of the
+  // thread, so the load of chunk c+1 is issued right after chunk c's wait;
+  // the empty asm pins chunk c's registers behind the wait)
+  const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+  auto consume = [&](uint32_t (&r)[32], int c0) {
     for (int p = 0; p < nparts; ++p) {
       const float4* src = reinterpret_cast<const float4*>(part + (static_cast<size_t>(p) * kBlockM + tl) * pstride + c0);
 #pragma unroll
@@ -214,6 +225,22 @@ __device__ __forceinline__ void gate_epilogue(const GateArgs& a, uint32_t tmem_b
         }
       }
     }
+  };
+  uint32_t ra[32], rb[32];
+  int c0 = c_begin;
+  if (c0 < c_end) ptx::tmem_ld32(trow + c0, ra);
+  while (c0 < c_end) {
+    ptx::tmem_ld_wait();
+    reg_fence32(ra);
+    if (c0 + 32 < c_end) ptx::tmem_ld32(trow + c0 + 32, rb);
+    consume(ra, c0);
+    c0 += 32;
+    if (c0 >= c_end) break;
+    ptx::tmem_ld_wait();
+    reg_fence32(rb);
+    if (c0 + 32 < c_end) ptx::tmem_ld32(trow + c0 + 32, ra);
+    consume(rb, c0);
+    c0 += 32;
   }
   if constexpr (K == 2) {
     // merge the odd-column list: order by (value desc, id asc)
@@ -230,24 +257,26 @@ __device__ __forceinline__ void gate_epilogue(const GateArgs& a, uint32_t tmem_b
     }
   }
   ptx::tc_fence_before();
-  // partial lists of the upper half -> smem (stage buffers are free: all TMA
+  // partial lists of parts 1.. -> smem (stage buffers are free: all TMA
   // writes landed and all MMAs retired before tfull fired; split-K partials
   // start at kPartOffset, past this scratch)
   float* pv = reinterpret_cast<float*>(smem);
-  int* pi = reinterpret_cast<int*>(smem + kBlockM * K * sizeof(float));
-  if (half == 1) {
+  int* pi = reinterpret_cast<int*>(smem + (kParts - 1) * kBlockM * K * sizeof(float));
+  if (part_id > 0) {
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-      pv[j * kBlockM + tl] = bv[j];
-      pi[j * kBlockM + tl] = bi[j];
+      pv[((part_id - 1) * K + j) * kBlockM + tl] = bv[j];
+      pi[((part_id - 1) * K + j) * kBlockM + tl] = bi[j];
     }
   }
   __syncthreads();
-  if (half == 0 && tok < a.S) {
-    // upper-half ids are all larger, so inserting them in order keeps ties
-    // resolved toward the lower id
+  if (part_id == 0 && tok < a.S) {
+    // later parts hold larger ids, so inserting them part by part, each list
+    // in its (value desc, id asc) order, keeps ties resolved toward the lower id
+    for (int p = 0; p < kParts - 1; ++p)
 #pragma unroll
-    for (int j = 0; j < K; ++j) topk_insert<K>(bv, bi, pv[j * kBlockM + tl], pi[j * kBlockM + tl]);
+      for (int j = 0; j < K; ++j)
+        topk_insert<K>(bv, bi, pv[(p * K + j) * kBlockM + tl], pi[(p * K + j) * kBlockM + tl]);
     const int k = a.k;
     float ex[K];
     float sum = 0.f;
@@ -332,48 +361,41 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
   if (a.prof && threadIdx.x == 0) a.prof[kProf * blockIdx.x + 1] = gate_clock();
 
   if (warp == 0) {
-    // ------------------------------------------------------ TMA producer
-    // A thread's bulk-tensor requests complete one after another (~0.25-0.3
-    // us each for 8-64 KB, tools/probes/tma_l2_probe.cu: one issuing thread
-    // streams ~50 GB/s, four ~170 GB/s), so the stage's requests rotate over
-    // the 32 lanes of the warp: consecutive requests come from different
-    // threads and overlap.  The whole warp waits on the stage; one lane arms it.
-    const uint64_t pol_x = ptx::policy_evict_first();
-    const uint64_t pol_w = ptx::policy_evict_last();
-    // this CTA's share of the Wg boxes (all of them without multicast)
-    constexpr int MC = SPLIT ? 1 : C;  // CTAs sharing each Wg box
-    const int per = L.n_box / MC;
-    const int b_lo = MC > 1 ? crank * per : 0;
-    const int nreq = 1 + per;  // requests per stage
-    const int spread = a.tma_spread ? 32 : 1;
-    int stage = 0;
-    uint32_t phase = 0;
-    int slot = 0;  // request counter (lane = slot % spread)
-    for (int kb = kb_lo; kb < kb_hi; ++kb) {
-      // free once every CTA of the cluster has consumed the stage
-      ptx::mbar_wait(&empty[stage], phase ^ 1);
-      if (a.dbg & 2) {  // ablation: no loads at all
-        if (lane == 0) ptx::mbar_arrive(&full[stage]);
-      } else {
-        if (lane == 0)
+    if (lane == 0) {
+      // ---------------------------------------------------- TMA producer
+      // (one issuing thread: rotating the stage's requests over the warp's
+      // lanes measured equal, LM 13.3 vs 13.4 us mainloop, same box)
+      const uint64_t pol_x = ptx::policy_evict_first();
+      const uint64_t pol_w = ptx::policy_evict_last();
+      // this CTA's share of the Wg boxes (all of them without multicast)
+      constexpr int MC = SPLIT ? 1 : C;  // CTAs sharing each Wg box
+      const int per = L.n_box / MC;
+      const int b_lo = MC > 1 ? crank * per : 0;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = kb_lo; kb < kb_hi; ++kb) {
+        // free once every CTA of the cluster has consumed the stage
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        if (a.dbg & 2) {  // ablation: no loads at all
+          ptx::mbar_arrive(&full[stage]);
+        } else {
           ptx::mbar_arrive_expect_tx(&full[stage], stage_bytes - ((a.dbg & 4) ? L.b_rows * BK * 2 : 0) -
                                                        ((a.dbg & 8) ? kABytes : 0));
-        uint8_t* st = smem + stage * stage_bytes;
-        if (!(a.dbg & 8) && lane == slot % spread) ptx::tma_load_2d(st, &tmX, &full[stage], kb * BK, tok0, pol_x);
-        for (int b = b_lo; b < b_lo + per && !(a.dbg & 4); ++b) {
-          if (lane != (slot + 1 + b - b_lo) % spread) continue;
-          const int r = b * L.box_rows;
-          if (MC > 1)
-            ptx::tma_load_2d_mc(st + kABytes + r * BK * 2, &tmWg, &full[stage], kb * BK, r,
-                                static_cast<uint16_t>((1u << MC) - 1), pol_w);
-          else
-            ptx::tma_load_2d(st + kABytes + r * BK * 2, &tmWg, &full[stage], kb * BK, r, pol_w);
+          uint8_t* st = smem + stage * stage_bytes;
+          if (!(a.dbg & 8)) ptx::tma_load_2d(st, &tmX, &full[stage], kb * BK, tok0, pol_x);
+          for (int b = b_lo; b < b_lo + per && !(a.dbg & 4); ++b) {
+            const int r = b * L.box_rows;
+            if (MC > 1)
+              ptx::tma_load_2d_mc(st + kABytes + r * BK * 2, &tmWg, &full[stage], kb * BK, r,
+                                  static_cast<uint16_t>((1u << MC) - 1), pol_w);
+            else
+              ptx::tma_load_2d(st + kABytes + r * BK * 2, &tmWg, &full[stage], kb * BK, r, pol_w);
+          }
         }
-        slot += nreq;
-      }
-      if (++stage == L.stages) {
-        stage = 0;
-        phase ^= 1;
+        if (++stage == L.stages) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
     }
     __syncwarp();
@@ -428,9 +450,9 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
     ptx::mbar_wait(tfull, 0);
     ptx::tc_fence_after();
     if (crank != 0) {
-      const int q = warp & 3, half = warp >> 2, tl = q * 32 + lane;
-      const int nchunk = (a.E + 31) / 32, split = (nchunk + 1) / 2;
-      const int c_begin = half ? split * 32 : 0, c_end = half ? nchunk * 32 : split * 32;
+      const int q = warp & 3, part_id = warp >> 2, tl = q * 32 + lane;
+      const int nchunk = (a.E + 31) / 32;
+      const int c_begin = part_id * nchunk / kParts * 32, c_end = (part_id + 1) * nchunk / kParts * 32;
       float* row = reinterpret_cast<float*>(smem) + static_cast<size_t>(tl) * pstride;
       for (int c0 = c_begin; c0 < c_end; c0 += 32) {
         uint32_t r[32];
@@ -481,7 +503,7 @@ __device__ __forceinline__ uint8_t* aligned_smem() {
 }
 
 template <int K, int C, int BK, bool SPLIT>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     gate_topk_kernel(const __grid_constant__ CUtensorMap tmX,
                      const __grid_constant__ CUtensorMap tmWg, GateArgs a) {
   gate_tile<K, C, BK, SPLIT>(tmX, tmWg, a, aligned_smem());
@@ -665,7 +687,7 @@ namespace {
 bool clusters_fit(const void* fn, int C, int clusters, int smem) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * C);
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeClusterDimension;
@@ -726,7 +748,7 @@ cudaError_t launch_gate_k(const CUtensorMap& tmX, const CUtensorMap& tmWg, const
                           int C, bool split, int tiles, int smem, cudaStream_t stream) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(split ? tiles * C : (tiles + C - 1) / C * C);
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
@@ -820,7 +842,6 @@ cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const G
   static const int dbg = getenv("MOE_GATE_DBG") ? atoi(getenv("MOE_GATE_DBG")) : 0;
   GateArgs b = a;
   b.dbg = dbg;
-  b.tma_spread = tma_spread_enabled();
   static unsigned long long* prof_buf = nullptr;
   const int ctas = split ? tiles * C : tiles;
   if (prof) {

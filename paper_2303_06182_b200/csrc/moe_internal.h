@@ -49,18 +49,6 @@ inline cudaError_t launch_chain(void (*kernel)(KArgs...), dim3 grid, dim3 block,
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
-// TMA producers issue a stage's requests from different lanes of the producer
-// warp: one thread's bulk-tensor requests are serviced one after another
-// (tools/probes/tma_l2_probe.cu), so a single issuing thread caps an SM at
-// ~50 GB/s.  MOE_TMA_SPREAD=0 restores one issuing lane (A/B).
-inline bool tma_spread_enabled() {
-  static const bool on = [] {
-    const char* v = getenv("MOE_TMA_SPREAD");
-    return !v || atoi(v) != 0;
-  }();
-  return on;
-}
-
 #ifdef __CUDACC__
 // wait for the previous kernel of the stream (no-op without PDL)
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -191,7 +179,6 @@ struct GateArgs {
   const void* Wg = nullptr;  // [E, TD] bf16
   unsigned long long* prof = nullptr;  // experiments (MOE_GATE_PROF): per-CTA phase times
   int dbg = 0;  // ablations (MOE_GATE_DBG, wrong results): 1 no MMAs, 2 no loads, 4 no Wg, 8 no X
-  int tma_spread = 1;  // producer requests rotate over the warp's lanes (tma_spread_enabled)
 };
 cudaError_t gate_prepare(int E);
 cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateArgs& a,
