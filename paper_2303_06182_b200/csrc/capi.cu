@@ -559,7 +559,7 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
   if (d.weights_packed) {
     // the caller's buffers are the packed tiles: stream them, keep no copy
     const size_t n1 = (size_t)E * HD * TD;
-    if ((st = encode_bf16(&L->tmW1p, W1, n1 / 64, 64, 128)) || (st = encode_bf16(&L->tmW2p, W2, n1 / 64, 64, 128))) {
+    if ((st = encode_packed(&L->tmW1p, W1, n1)) || (st = encode_packed(&L->tmW2p, W2, n1))) {
       moe_layer_destroy(L);
       return st;
     }
@@ -569,8 +569,8 @@ int moe_layer_create(moe_ctx* ctx, const moe_layer_desc* desc, const void* Wg, c
              d.mode == MOE_GATING_DYNAMIC && (L->tile_n == 128 || fused256_enabled())) {
     const size_t n1 = (size_t)E * HD * TD;
     if (L->w1p.reserve(n1) == MOE_OK && L->w2p.reserve(n1) == MOE_OK &&
-        encode_bf16(&L->tmW1p, L->w1p.p, n1 / 64, 64, 128) == MOE_OK &&
-        encode_bf16(&L->tmW2p, L->w2p.p, n1 / 64, 64, 128) == MOE_OK) {
+        encode_packed(&L->tmW1p, L->w1p.p, n1) == MOE_OK &&
+        encode_packed(&L->tmW2p, L->w2p.p, n1) == MOE_OK) {
       L->packed = true;
       if ((st = moe_layer_repack(L, nullptr))) {
         moe_layer_destroy(L);
@@ -1114,8 +1114,8 @@ int moe_ffn_create(moe_ctx* ctx, const moe_ffn_desc* desc, const void* W1, const
   if (pack_env && (F->tile_n == 128 || fused256_enabled())) {
     const size_t n1 = (size_t)d.num_experts * HD * TD;
     if (F->w1p.reserve(n1) == MOE_OK && F->w2p.reserve(n1) == MOE_OK &&
-        encode_bf16(&F->tmW1p, F->w1p.p, n1 / 64, 64, 128) == MOE_OK &&
-        encode_bf16(&F->tmW2p, F->w2p.p, n1 / 64, 64, 128) == MOE_OK &&
+        encode_packed(&F->tmW1p, F->w1p.p, n1) == MOE_OK &&
+        encode_packed(&F->tmW2p, F->w2p.p, n1) == MOE_OK &&
         launch_pack_tiles(static_cast<const __nv_bfloat16*>(W1), F->w1p.p,
                           (long)d.num_experts * HD, TD, nullptr) == cudaSuccess &&
         launch_pack_tiles(static_cast<const __nv_bfloat16*>(W2), F->w2p.p,

@@ -576,8 +576,8 @@ int moe_ep_create(moe_ctx* ctx, const moe_ep_desc* desc, const void* Wg, const v
   MOE_CUDA(cudaMemset(P->h.p, 0, (R + 256) * HD * 2));
   char* rx = P->window + P->lay.recv_x;
   if ((st = encode_bf16(&P->tmWg, Wg, E, TD, moe::gate_box_rows(E), moe::gate_box_cols(E))) ||
-      (st = encode_bf16(&P->tmW1p, P->w1p.p, n1 / 64, 64, 128)) ||
-      (st = encode_bf16(&P->tmW2p, P->w2p.p, n1 / 64, 64, 128)) ||
+      (st = encode_packed(&P->tmW1p, P->w1p.p, n1)) ||
+      (st = encode_packed(&P->tmW2p, P->w2p.p, n1)) ||
       (st = encode_rows(&P->xpm, rx, R + 256, TD)) || (st = encode_rows(&P->hm, P->h.p, R + 256, HD)))
     return bail(st);
   // the fused FFN streams tile-packed weights (contiguous 16 KB 128 x 64 tiles)

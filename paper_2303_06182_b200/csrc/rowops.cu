@@ -49,83 +49,6 @@ __global__ void __launch_bounds__(256)
   if (late) pdl_trigger();
 }
 
-// TMA form of the gather: rows move global -> shared -> global as 1-D bulk
-// copies (cp.async.bulk), no register traffic.  Each of the CTA's 4 warps runs
-// one independent stream (lane 0 issues): a ring of RING row buffers, loads
-// RING/2 rows ahead of the stores, a slot reloaded only after the bulk store
-// that last read it has finished reading (bulk async-group accounting).
-// Placeholder rows (order < 0) are stored from a zeroed buffer.
-constexpr int kGatherWarps = 8;
-
-template <int RING>
-__global__ void __launch_bounds__(kGatherWarps * 32)
-    gather_rows_tma_kernel(const uint8_t* __restrict__ X, const int32_t* __restrict__ order,
-                           int rows, int k, int row_bytes, uint8_t* __restrict__ Xp) {
-  constexpr int kAhead = RING / 2;
-  extern __shared__ __align__(128) uint8_t gsm[];
-  __shared__ __align__(8) uint64_t bars[kGatherWarps][RING];
-  pdl_trigger();
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  uint8_t* buf = gsm + static_cast<size_t>(warp) * RING * row_bytes;
-  uint8_t* zero = gsm + static_cast<size_t>(kGatherWarps) * RING * row_bytes;
-  for (int i = threadIdx.x; i < row_bytes / 16; i += blockDim.x)
-    reinterpret_cast<uint4*>(zero)[i] = make_uint4(0, 0, 0, 0);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zero row visible to TMA
-  __syncthreads();
-  if (lane != 0) return;
-  uint64_t* bar = bars[warp];
-  for (int s = 0; s < RING; ++s) ptx::mbar_init(&bar[s], 1);
-  ptx::fence_barrier_init();
-  pdl_wait();
-  const int stream = blockIdx.x * kGatherWarps + warp;
-  const int nstreams = gridDim.x * kGatherWarps;
-  const int n = rows > stream ? (rows - stream + nstreams - 1) / nstreams : 0;
-  auto load = [&](int i) {
-    const int s = i % RING;
-    const int slot = order[stream + i * nstreams];
-    if (slot >= 0) {
-      ptx::mbar_arrive_expect_tx(&bar[s], row_bytes);
-      ptx::bulk_load(buf + s * row_bytes, X + static_cast<size_t>(slot / k) * row_bytes, row_bytes,
-                     &bar[s]);
-    } else {
-      ptx::mbar_arrive(&bar[s]);
-    }
-  };
-  for (int i = 0; i < kAhead && i < n; ++i) load(i);
-  for (int i = 0; i < n; ++i) {
-    if (i + kAhead < n) {
-      // slot (i + kAhead) % RING was last read by the store of row
-      // i + kAhead - RING; the RING - kAhead - 1 stores committed after it may
-      // still be reading
-      if (i + kAhead >= RING) ptx::bulk_wait_read<RING - kAhead - 1>();
-      load(i + kAhead);
-    }
-    const int s = i % RING;
-    ptx::mbar_wait(&bar[s], (i / RING) & 1);
-    const int p = stream + i * nstreams;
-    ptx::bulk_store(Xp + static_cast<size_t>(p) * row_bytes, order[p] < 0 ? zero : buf + s * row_bytes,
-                    row_bytes);
-    ptx::bulk_commit();
-  }
-  ptx::bulk_wait_all();
-}
-
-template <int RING>
-cudaError_t launch_gather_tma(const uint8_t* X, const int32_t* order, int rows, int k, int row_bytes,
-                              uint8_t* Xp, int grid, cudaStream_t stream) {
-  const int smem = (kGatherWarps * RING + 1) * row_bytes;
-  static int granted = 0;
-  if (smem > granted) {
-    cudaError_t e = cudaFuncSetAttribute(gather_rows_tma_kernel<RING>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    granted = smem;
-  }
-  return launch_chain(gather_rows_tma_kernel<RING>, dim3(grid), dim3(kGatherWarps * 32), smem,
-                      stream, false, X, order, rows, k, row_bytes, Xp);
-}
-
 __device__ __forceinline__ void add_bf16x8(float (&acc)[8], const uint4& v) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
@@ -337,19 +260,6 @@ int sm_count() {
 cudaError_t launch_gather_rows(const __nv_bfloat16* X, const int32_t* order, int rows, int k,
                                int TD, __nv_bfloat16* Xp, cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
-  static const int tma = [] {
-    const char* v = getenv("MOE_GATHER_TMA");
-    return v ? atoi(v) : 0;
-  }();
-  const int row_bytes = TD * 2;
-  if (tma && row_bytes % 16 == 0) {
-    const auto* x8 = reinterpret_cast<const uint8_t*>(X);
-    auto* xp8 = reinterpret_cast<uint8_t*>(Xp);
-    // ~24 KB of rows per warp stream, 8 streams per SM
-    if (row_bytes <= 2048) return launch_gather_tma<12>(x8, order, rows, k, row_bytes, xp8, sm_count(), stream);
-    if (row_bytes <= 4096) return launch_gather_tma<6>(x8, order, rows, k, row_bytes, xp8, sm_count(), stream);
-    if (row_bytes <= 8192) return launch_gather_tma<3>(x8, order, rows, k, row_bytes, xp8, sm_count(), stream);
-  }
   return launch_chain(gather_rows_kernel, dim3(grid_for(rows, sm_count())), dim3(256), 0, stream,
                       false, reinterpret_cast<const uint4*>(X), order, rows, k, TD / 8,
                       reinterpret_cast<uint4*>(Xp), late_trigger("MOE_GATHER_LATE_TRIGGER", 0));
@@ -422,7 +332,8 @@ cudaError_t launch_fill_uniform_bf16(__nv_bfloat16* dst, int64_t n, uint64_t see
 }
 
 // Weight prepack: row-major [mblocks * 128, K] -> tiles of 128 rows x 64
-// columns, each 16 KB contiguous, tile (mb, kc) at tile index mb * (K/64) + kc.
+// columns, each 16 KB contiguous, tile (mb, kc) at tile index mb * (K/64) + kc,
+// rows 128 B apart with the 128-byte swizzle already applied.
 // One CTA per tile: 128 rows x 8 x 16 B.
 __global__ void pack_tiles_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, int K) {
   const long tile = blockIdx.x;
@@ -432,7 +343,9 @@ __global__ void pack_tiles_kernel(const uint4* __restrict__ src, uint4* __restri
   const int vrow = K / 8;  // uint4 per source row
   for (int i = threadIdx.x; i < 128 * 8; i += blockDim.x) {
     const int r = i >> 3, c = i & 7;
-    dst[tile * 1024 + i] = src[(mb * 128 + r) * vrow + kc * 8 + c];
+    // 16-byte chunk c of row r at chunk c ^ (r % 8): the 128-byte swizzle the
+    // UMMA descriptors expect, applied here once instead of by every TMA load
+    dst[tile * 1024 + r * 8 + (c ^ (r & 7))] = src[(mb * 128 + r) * vrow + kc * 8 + c];
   }
 }
 

@@ -334,7 +334,38 @@ layer = MoeLayer(shape, S, weights=make_weights(shape, seed=2303061820), keep_lo
 layer(make_tokens(S, TD, seed=2303061820))
 torch.cuda.synchronize()
 np.save(sys.argv[7], layer.view()["logits"][:S * E].cpu().numpy())
+np.save(sys.argv[7] + ".idx.npy", layer.view()["idx"][:S * k].cpu().numpy())
 """
+
+
+@pytest.mark.parametrize("S,TD,HD,E,k", [(2048, 1024, 4096, 8, 1), (300, 256, 512, 9, 2),
+                                         (1000, 512, 512, 32, 4), (129, 1152, 256, 16, 2)])
+def test_small_e_gate_matches_tcgen05_gate(S, TD, HD, E, k, tmp_path):
+    """E <= 32: the CUDA-core gate (gate_small_kernel) against the tcgen05
+    gate (MOE_GATE_SMALL=0, a separate process since the choice is read once):
+    both within the fp32 oracle's tolerance, and each one's routing equal to
+    the top-k of its own logits."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for small in ("1", "0"):
+        f = str(tmp_path / f"logits_{small}.npy")
+        env = dict(os.environ, MOE_GATE_SMALL=small)
+        r = subprocess.run([sys.executable, "-c", _GATE_SCRIPT, root, str(S), str(TD), str(HD), str(E), str(k), f],
+                           env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[small] = np.load(f).reshape(S, E)
+        idx = np.load(f + ".idx.npy").reshape(S, k)
+        assert (idx == OL.topk_from_logits(outs[small], k)[0]).all(), small
+    x = _f32(make_tokens(S, TD, seed=SEED))
+    Wg = _f32(make_weights(LayerShape(TD, HD, E, k), seed=SEED)[0])
+    ref = OL.gate_logits(x, Wg)
+    tol = 2e-5 * max(float(np.abs(ref).max()), 1.0) * math.sqrt(TD / 256)
+    for small, lg in outs.items():
+        assert np.abs(lg - ref).max() <= tol, small
+    assert np.abs(outs["1"] - outs["0"]).max() <= tol
 
 
 @pytest.mark.parametrize("S,TD,HD,E,k", [(2048, 1024, 4096, 8, 1), (6144, 2048, 8192, 128, 2),
