@@ -804,6 +804,8 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
     fa.dbg = getenv("MOE_FFN_DBG") ? atoi(getenv("MOE_FFN_DBG")) : 0;
     // the expert-cache slot pool is row-major: packed tiles only for the layer's own weights
     fa.packed = L->packed && !L->slot_of;
+    fa.W1p = L->caller_packed ? L->W1 : L->w1p.p;
+    fa.W2p = L->caller_packed ? L->W2 : L->w2p.p;
     fa.pair_hint = auto_pair((double)L->rows_max / L->d.num_experts, L->d.num_experts, TD, HD,
                              L->tile_n, L->ctx->sms);
     if (fcomb) {
@@ -1186,6 +1188,8 @@ int moe_ffn_forward(moe_ffn* F, const void* X_rows, const int32_t* keys, const f
     fa.lag = std::max(2, (8 * F->ctx->sms + per_item - 1) / per_item);
     fa.discard_h = 1;
     fa.packed = F->packed;
+    fa.W1p = F->w1p.p;
+    fa.W2p = F->w2p.p;
     fa.pair_hint = auto_pair((double)F->d.max_rows / F->d.num_experts, F->d.num_experts, TD, HD,
                              F->tile_n, F->ctx->sms);
     e = launch_fused_ffn(F->packed ? F->tmW1p : F->tmW1, F->xpm, F->packed ? F->tmW2p : F->tmW2,

@@ -81,13 +81,14 @@ inline int encode_bf16(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t 
 // Packed weight tiles (launch_pack_tiles): 128 x 64 bf16 tiles stored already
 // in the 128-byte-swizzled shared-memory order, so the tensor map copies them
 // verbatim (no swizzle) and a 1-D bulk copy of consecutive tiles lands the same
-// bytes.  n = elements of the packed buffer.
+// bytes.  The box is two tiles (256 rows): the CTA-pair FFN loads a stage's
+// weights (KCH = 2 consecutive tiles) as one request.  n = elements.
 inline int encode_packed(CUtensorMap* m, const void* ptr, uint64_t n) {
   int st = get_encoder();
   if (st) return st;
   cuuint64_t dims[2] = {64, n / 64};
   cuuint64_t strides[1] = {128};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, 256};  // two consecutive tiles: one CTA-pair stage (KCH = 2)
   cuuint32_t estr[2] = {1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

@@ -485,6 +485,8 @@ int ep_launch_ffn(moe_ep* P, cudaStream_t s) {
   fa.lag = std::max(2, (8 * P->ctx->sms + per_item - 1) / per_item);
   fa.discard_h = 1;
   fa.packed = 1;
+  fa.W1p = P->w1p.p;
+  fa.W2p = P->w2p.p;
   fa.pair_hint = auto_pair((double)D * d.max_tokens * d.top_k / E, P->El, TD, HD, P->tile_n,
                            P->ctx->sms);
   cudaError_t ce = launch_fused_ffn(P->tmW1p, P->xpm, P->tmW2p, P->hm, fa, P->tile_n, P->ctx->sms, s);

@@ -261,17 +261,21 @@ __global__ void __launch_bounds__(256, 1)
         fence_proxy_async_global();
       }
       const uint32_t bytes = ((g.dbg & 16) ? 0 : kABytes) + ((g.dbg & 1) ? 0 : KCH * nrows * kChunkK * 2);
+      // packed weights: the stage's KCH tiles are consecutive 16 KB tiles,
+      // already in the swizzled smem order -> one 1-D bulk copy
+      const uint8_t* wbulk = static_cast<const uint8_t*>(tr.gemm ? g.W2p : g.W1p);
       for (int kb = 0; kb < KB; ++kb) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         ptx::mbar_arrive_expect_tx(&full[stage], bytes);
+        if (g.packed && !(g.dbg & 16))
+          ptx::bulk_load_hint(sA + stage * kABytes,
+                              wbulk + static_cast<size_t>(a_tile + kb * KCH) * Cfg::kAChunk, kABytes,
+                              &full[stage], pol_w);
 #pragma unroll
         for (int c = 0; c < KCH; ++c) {
           const int k0 = kb * Cfg::kStageK + c * kChunkK;
-          if (g.dbg & 16) {
-          } else if (g.packed)
-            ptx::tma_load_2d(sA + stage * kABytes + c * Cfg::kAChunk, tA, &full[stage], 0,
-                             (a_tile + kb * KCH + c) * kBlockM, pol_w);
-          else
+          if ((g.dbg & 16) || g.packed) {
+          } else
             ptx::tma_load_2d(sA + stage * kABytes + c * Cfg::kAChunk, tA, &full[stage], k0, a_row,
                              pol_w);
           uint8_t* b_dst = sB + stage * Cfg::kBBytes + c * Cfg::kBChunk;
@@ -513,6 +517,9 @@ cudaError_t launch_fused_ffn(const CUtensorMap& tmW1, const RowMaps& xp, const C
   FusedFfnArgs args = args_in;
   args.full_fence = full_fence;
   args.dyn_tail = dyn_tail;
+  // packed weights are always loaded as 1-D bulk copies by the 1-SM kernel
+  // (the packed tensor maps' 256-row boxes are shaped for the CTA pair)
+  if (args.packed && (!args.W1p || !args.W2p)) return cudaErrorInvalidValue;
   if (dyn_tail < 0) args.tile_ctr = nullptr;
   args.late_trigger = late;
   if (!prof) return launch_fused_ffn_impl(tmW1, xp, tmW2, h, args, tile_n, grid, stream);

@@ -39,6 +39,7 @@ constexpr int kAChunk = kBlockM * kChunkK * 2;      // 16 KB
 // stages half of the item's token rows.
 template <int BN, int STAGES, int KCH>
 struct PairCfg {
+  static_assert(KCH == 2, "packed weights: one 256-row (two-tile) box per stage");
   static constexpr int kBN = BN;
   static constexpr int kBChunk = (BN / 2) * kChunkK * 2;  // half of the token rows
   static constexpr int kTmemCols = 2 * BN;
@@ -313,14 +314,13 @@ __global__ void __launch_bounds__(256, 1)
         const uint32_t fb = leader_addr(&full[stage]);
         // the leader arms its own barrier (CTA-scope arrive: no cluster fence)
         if (leader) ptx::mbar_arrive_expect_tx(&full[stage], bytes);
+        // packed weights: the stage's two consecutive (pre-swizzled) tiles as
+        // one 256-row box
+        if (g.packed) tma_load_2d_pair(sA + stage * kABytes, tA, fb, 0, (a_tile + kb * kKch) * kBlockM, pol_w);
 #pragma unroll
         for (int c = 0; c < kKch; ++c) {
           const int k0 = kb * kStageK + c * kChunkK;
-          if (g.packed)
-            tma_load_2d_pair(sA + stage * kABytes + c * kAChunk, tA, fb, 0,
-                             (a_tile + kb * kKch + c) * kBlockM, pol_w);
-          else
-            tma_load_2d_pair(sA + stage * kABytes + c * kAChunk, tA, fb, k0, a_row, pol_w);
+          if (!g.packed) tma_load_2d_pair(sA + stage * kABytes + c * kAChunk, tA, fb, k0, a_row, pol_w);
           load_rows(sB + stage * kBBytes + c * kBChunk, tB, fb, k0, b_row, half, pol_x);
         }
         if (++stage == kStages) {

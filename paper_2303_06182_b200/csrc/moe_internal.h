@@ -142,6 +142,10 @@ struct FusedFfnArgs {
   int late_trigger;         // let the next kernel launch only as CTAs finish
   int pair_hint;            // the caller expects >= ~8 waves of CTA-pair tiles (see auto_pair)
   int dyn_tail;             // tail tiles claimed dynamically (0 = the last lag * MT2)
+  // packed tiles' base addresses: the 1-SM kernel loads a stage's consecutive
+  // weight tiles as ONE 1-D bulk copy (null: tensor-map loads)
+  const void* W1p = nullptr;
+  const void* W2p = nullptr;
   // expert parallelism (ep_p2p.cu): a GEMM1 tile's token rows are loaded only
   // once arrived[expert] >= arrived_expect[expert] (peer stores, acquire.sys);
   // after arrive_timeout_ns the wait gives up and sets arrive_err[0]
