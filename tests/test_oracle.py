@@ -229,3 +229,34 @@ def test_layer_oracle_k1_identity_expert():
     w = np.ones((3, 1))
     out = OL.layer_forward(X, W1, W2, idx, w, E)
     assert np.allclose(out, np.maximum(X, 0))
+
+
+@needs_ref
+@pytest.mark.parametrize("S,TD,HD,E,k", [(64, 32, 48, 8, 2), (50, 16, 16, 6, 3), (40, 24, 32, 5, 1)])
+def test_layer_oracle_combine_equals_reference_dispatch_and_combine(S, TD, HD, E, k):
+    """Pins the oracle's dispatch -> FFN -> weighted-combine plumbing to the
+    reference where the reference has semantics: expert rows are computed in
+    the reference's dynamic_dispatch order (gating.cpp:58-86) and each
+    token's output is summed over the entries the reference's combine<T>
+    returns (gating.hpp:107-141: slot order, the routing weights), payload =
+    the row index of that slot's expert output.  Same fp32 operations ->
+    bitwise equal to oracle.layer.layer_forward."""
+    rng = np.random.default_rng(S * 1000 + E)
+    X = rng.standard_normal((S, TD)).astype(np.float32)
+    W1 = (rng.standard_normal((E, HD, TD)) / np.sqrt(TD)).astype(np.float32)
+    W2 = (rng.standard_normal((E, TD, HD)) / np.sqrt(HD)).astype(np.float32)
+    idx, w = OL.topk_from_logits(rng.standard_normal((S, E)).astype(np.float32), k)
+    order, counts, splits = N.ref_dynamic_dispatch(idx, E, w)
+    # expert FFN over the reference's expert-grouped rows
+    Y = np.zeros((S * k, TD), np.float32)
+    for e in range(E):
+        rows = order[splits[e]:splits[e + 1]]
+        if len(rows):
+            Y[splits[e]:splits[e + 1]] = OL.expert_ffn(X[rows // k], W1[e], W2[e])
+    n, oe, ow, op = N.ref_combine_dynamic(idx, w, E, np.arange(S * k, dtype=np.int32))
+    assert (n == k).all() and (oe == idx).all()
+    out = np.zeros((S, TD), np.float32)
+    for j in range(k):  # the reference's presentation order == slot order
+        out += ow[:, j].astype(np.float32)[:, None] * Y[op[:, j]]
+    ref = OL.layer_forward(X, W1, W2, idx, w, E)
+    assert np.array_equal(out, ref)
