@@ -134,7 +134,16 @@ struct EpDispatchArgs {
   unsigned long long timeout_ns;
   int full_fence;          // A/B: per-thread fence.sc.sys before the arrival
   int overlap;             // expert-ordered rows + per-expert arrival counters
+  // by-token form (default without overlap): one warp per token reads its X
+  // row once and stores it to the k destination rows
+  const int32_t* idx;      // [S*k] expert ids (null: by-row form)
+  const int32_t* pos;      // [S*k] slot -> sorted row
+  const int32_t* key_map;  // [E] expert -> key (device * El + local expert)
+  const float* w;          // [S*k] gate weight per slot
 };
+
+// by-token rows per lane kept in registers (TD <= 4096)
+constexpr int kTokVecs = 16;
 
 __device__ __forceinline__ void red_add_release_sys_u32(unsigned* p, unsigned v) {
   asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -200,7 +209,46 @@ __global__ void __launch_bounds__(512) ep_dispatch_kernel(EpDispatchArgs a) {
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     const int nwarps = gridDim.x * wpb;
-    for (int v_ = blockIdx.x * wpb + (threadIdx.x >> 5); v_ < a.rows; v_ += nwarps) {
+    if (!a.overlap && a.idx) {
+      // ---- by token: X row read once, stored to its k destination rows.
+      // Destination of slot t*k+j: key = key_map[idx], sorted row i = pos[slot],
+      // row = s_off[key] + i at device key / El (the by-row formula, with the
+      // key known directly instead of searched in splits)
+      const int S = a.rows / a.k;
+      const int nv = a.vpr / 32;  // 16-byte vectors per lane
+      for (int t = blockIdx.x * wpb + (threadIdx.x >> 5); t < S; t += nwarps) {
+        const uint4* src = a.X + static_cast<size_t>(t) * a.vpr;
+        uint4 xv[kTokVecs];
+#pragma unroll
+        for (int u = 0; u < kTokVecs; ++u)
+          if (u < nv) xv[u] = __ldg(src + u * 32 + lane);
+        for (int j = 0; j < a.k; ++j) {
+          const int slot = t * a.k + j;
+          const int i = a.pos[slot];
+          if (i < 0) continue;  // rejected id (the route flagged it)
+          const int key = a.key_map[a.idx[slot]];
+          const int p = key / a.El;
+          const int row = s_off[key] + i;
+          if (row >= a.max_recv) {
+            if (lane == 0) {
+              atomicExch(a.err + 1, 1);
+              a.dest[i] = -1;
+            }
+            continue;
+          }
+          char* peer = a.peers.base[p];
+          uint4* dst = reinterpret_cast<uint4*>(peer + a.lay.recv_x) + static_cast<size_t>(row) * a.vpr;
+#pragma unroll
+          for (int u = 0; u < kTokVecs; ++u)
+            if (u < nv) dst[u * 32 + lane] = xv[u];
+          if (lane == 0) {
+            reinterpret_cast<float*>(peer + a.lay.recv_w)[row] = a.w[slot];
+            a.dest[i] = (p << kRowBits) | row;
+          }
+        }
+      }
+    }
+    for (int v_ = blockIdx.x * wpb + (threadIdx.x >> 5); v_ < a.rows && (a.overlap || !a.idx); v_ += nwarps) {
       int lo, i;
       if (a.overlap) {
         int jl = 0, jh = a.E - 1;  // last (e, p) segment starting at or before v_
@@ -264,6 +312,15 @@ __global__ void __launch_bounds__(512) ep_dispatch_kernel(EpDispatchArgs a) {
     fence_acq_rel_sys();
     red_add_release_sys(&hdr(a.peers.base[threadIdx.x])->sig_data, 1ull);
   }
+}
+
+// MOE_EP_DISPATCH_TOKENS=0 restores the by-row dispatch (A/B)
+bool ep_dispatch_by_token() {
+  static const bool on = [] {
+    const char* v = getenv("MOE_EP_DISPATCH_TOKENS");
+    return !v || atoi(v) != 0;
+  }();
+  return on;
 }
 
 // ---------------------------------------------------------------- receive side
@@ -721,6 +778,13 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
   da.timeout_ns = P->timeout_ns;
   da.full_fence = P->full_fence;
   da.overlap = P->overlap;
+  // the by-token form needs the whole row in registers (TD <= 4096, TD % 256 == 0)
+  if (!P->overlap && (TD / 8) % 32 == 0 && TD / 8 <= 32 * kTokVecs && ep_dispatch_by_token()) {
+    da.idx = P->idx.p;
+    da.pos = P->pos.p;
+    da.key_map = P->key_map.p;
+    da.w = P->w.p;
+  }
   mark(2);
   ce = launch_chain(ep_dispatch_kernel, dim3(P->dispatch_ctas), dim3(512), 0, s, false, da);
   if (ce != cudaSuccess) return cuda_fail(ce, "EP dispatch launch");
