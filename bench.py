@@ -472,7 +472,7 @@ def run_ep(args, world, rank, local):
                 "exchange_bytes_offrank_per_step": xbytes,
                 "exchange_gbs_over_whole_step": xbytes / (ms * 1e-3) / 1e9,
                 "nvlink_peak_gbs_per_direction": 900.0,
-                "nvlink_measured_peer_copy_gbs": 770.0,
+                "nvlink_peer_copy_gbs_profiling_guide": 770.0,  # B200_PROFILING.md measured figure, not this run
                 **({"dispatch_ms": ep_stage["dispatch"], "combine_ms": ep_stage["combine"],
                     "dispatch_gbs_offrank": sent_off * TD * 2 / (ep_stage["dispatch"] * 1e-3) / 1e9,
                     "combine_gbs_offrank": sent_off * TD * 2 / (ep_stage["combine"] * 1e-3) / 1e9,
