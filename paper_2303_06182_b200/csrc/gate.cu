@@ -803,9 +803,11 @@ bool gate_small(int E, int TD) {
 cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateArgs& a,
                         cudaStream_t stream) {
   if (a.X && a.Wg && a.k >= 1 && a.k <= kMaxK && a.E >= a.k && gate_small(a.E, a.TD)) {
-    int dev = 0, sms = 0;
+    static int sms_of[64] = {0};  // SM count per device (queried once)
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int& sms = sms_of[dev & 63];
+    if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int wpb = kSmallThreads / 32;
     const int grid = std::max(1, std::min((a.S + wpb - 1) / wpb, 2 * sms));
     const int smem = a.E * a.TD * 2;
