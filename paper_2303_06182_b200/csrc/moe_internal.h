@@ -94,6 +94,7 @@ struct RouteArgs {
   int32_t* zero;              // optional [zero_n] buffer zeroed by the kernel (FFN counters)
   int zero_n;
   int late_trigger;           // release the next kernel (gather) only at completion
+  unsigned long long* prof = nullptr;  // experiments (MOE_ROUTE_PROF): phase stamps of block 0
 };
 
 size_t route_smem_bytes(int E);

@@ -25,6 +25,7 @@
 //            grid-wide barriers.
 #include <cooperative_groups.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -131,11 +132,21 @@ __device__ __forceinline__ void load_keys(const RouteArgs& a, int base0, int hi,
   }
 }
 
+__device__ __forceinline__ unsigned long long route_clock() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// MOE_ROUTE_PROF: block 0's thread 0 stamps the phase boundaries
+#define ROUTE_STAMP(j) \
+  if (a.prof && blockIdx.x == 0 && threadIdx.x == 0) a.prof[j] = route_clock()
+
 template <bool kSingle>
 __global__ void __launch_bounds__(kSingle ? kSingleThreads : kMultiThreads)
     route_kernel(RouteArgs a) {
   if (!a.late_trigger) pdl_trigger();
   pdl_wait();
+  ROUTE_STAMP(0);
   // zero the FFN's per-item / tile counters for this forward (saves a
   // memset node between the gather and the FFN, which would break the PDL chain)
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.zero_n; i += gridDim.x * blockDim.x)
@@ -179,6 +190,7 @@ __global__ void __launch_bounds__(kSingle ? kSingleThreads : kMultiThreads)
   }
   __syncthreads();
 
+  ROUTE_STAMP(1);
   // ---- phase 2: global scan + per-warp bases
   if constexpr (kSingle) {
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
@@ -230,6 +242,7 @@ __global__ void __launch_bounds__(kSingle ? kSingleThreads : kMultiThreads)
   }
   __syncthreads();
 
+  ROUTE_STAMP(2);
   // ---- phase 3: stable rank + scatter
   const int cap = a.capacity;  // 0 => dynamic
   int my_drops = 0;
@@ -273,6 +286,7 @@ __global__ void __launch_bounds__(kSingle ? kSingleThreads : kMultiThreads)
     }
   }
 
+  ROUTE_STAMP(3);
   // ---- FFN work items (block 0): expert e contributes ceil(rows_e / tile_n)
   //      items; rows_e = count (dynamic) or capacity (static, placeholders
   //      included -- the waste static gating pays for).
@@ -303,6 +317,7 @@ __global__ void __launch_bounds__(kSingle ? kSingleThreads : kMultiThreads)
     }
     if (threadIdx.x == 0) *a.n_items = n_items;
   }
+  ROUTE_STAMP(4);
 
   if (cap == 0) return;
 
@@ -383,6 +398,22 @@ cudaError_t launch_route(RouteArgs a, int max_blocks, cudaStream_t stream) {
     return v ? atoi(v) : 0;
   }();
   a.late_trigger = late;
+  static const bool prof = getenv("MOE_ROUTE_PROF") != nullptr;
+  static unsigned long long* prof_buf = nullptr;
+  if (prof && !prof_buf) cudaMalloc(&prof_buf, 8 * sizeof(unsigned long long));
+  a.prof = prof ? prof_buf : nullptr;
+  struct ProfPrint {  // experiments only: phase times of this launch on exit
+    unsigned long long* buf;
+    cudaStream_t s;
+    ~ProfPrint() {
+      if (!buf) return;
+      unsigned long long h[5];
+      cudaStreamSynchronize(s);
+      cudaMemcpy(h, buf, sizeof h, cudaMemcpyDeviceToHost);
+      fprintf(stderr, "[route prof] us: histogram %.2f | scan %.2f | scatter %.2f | items %.2f\n",
+              (h[1] - h[0]) * 1e-3, (h[2] - h[1]) * 1e-3, (h[3] - h[2]) * 1e-3, (h[4] - h[3]) * 1e-3);
+    }
+  } pp{a.prof, stream};
   const size_t single_smem = smem_bytes(a.num_experts, kSingleThreads / 32);
   static const int single_max = [] {
     const char* v = getenv("MOE_ROUTE_SINGLE_MAX");  // A/B: largest slot count for the 1-CTA form
