@@ -202,8 +202,9 @@ int moe_layer_destroy(moe_layer* layer);
 
 /* Expert weights, row-major [rows, K] bf16 (rows = E * HD for W1 with K = TD,
  * rows = E * TD for W2 with K = HD), -> the tile-packed layout the fused FFN
- * streams (128 x 64 tiles, 16 KB contiguous; every expert's tiles stay inside
- * its own row range).  dst == src packs IN PLACE (expert-block-wise through a
+ * streams (128 x 64 tiles, 16 KB contiguous, each stored in the 128-byte
+ * swizzled shared-memory order so consecutive tiles are copied verbatim by
+ * one bulk transfer; every expert's tiles stay inside its own row range).  dst == src packs IN PLACE (expert-block-wise through a
  * 64 MB scratch); otherwise the buffers must not overlap.  rows % 128 == 0,
  * K % 64 == 0.  Synchronous on `stream`. */
 int moe_pack_expert_weights(moe_ctx* ctx, const void* src, void* dst, int64_t rows, int K,
