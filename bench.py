@@ -257,7 +257,7 @@ def run_reference(args):
         "data": "synthetic (counter-hash uniform tokens; random-init experts)",
         "config": {"workload": desc, "S": S, "TD": TD, "HD": HD, "E": E, "top_k": k, "gating": mode},
         "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": r["cores"], "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": r["cpu_model"], "host_cpus": r["host_cpus"]},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "breakdown_s": r["breakdown_s"],
     }
@@ -397,6 +397,7 @@ def run_ep(args, world, rank, local):
     elapsed = max_over_ranks(ev0.elapsed_time(ev1), world)
     steps = [step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(K)]
     p50 = max_over_ranks(float(np.median(steps)), world)
+    p90 = max_over_ranks(float(np.percentile(steps, 90)), world)
     if sampler:
         sampler.stop()
     check(stream)
@@ -455,7 +456,7 @@ def run_ep(args, world, rank, local):
                  "NCCL (C ABI): count all-gather + host sync + grouped send/recv of the rows and back")
     line = {
         "metric": "MoE-layer tokens/s (dynamic gating)", "value": S_total / (ms * 1e-3), "unit": "tokens/s",
-        "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms, "p50_ms": p50,
+        "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms, "p50_ms": p50, "p90_ms": p90,
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (counter-hash uniform tokens; random-init experts, std 1/sqrt(fan-in))",
         "config": {"workload": desc + " -- expert parallel" + (", one batch split over the GPUs" if strong else ""),
@@ -720,6 +721,7 @@ def run_b200(args):
     elapsed_max = max_over_ranks(elapsed_ms, world)
     p50 = float(np.median(step_ms))
     p50_max = max_over_ranks(p50, world)
+    p90_max = max_over_ranks(float(np.percentile(step_ms, 90)), world)
     if remeasured and clocks is not None:
         clocks = dict(clocks, remeasured=remeasured)
 
@@ -797,7 +799,8 @@ def run_b200(args):
 
         r = cpu_layer_bench(S, TD, HD, E, k, min_seconds=cpu_seconds())
         cpu = {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": r["cores"], "kind": "port",
-               "sample": r["sample"], "breakdown_s": r["breakdown_s"]}
+               "sample": r["sample"], "breakdown_s": r["breakdown_s"], "cpu_model": r["cpu_model"],
+               "host_cpus": r["host_cpus"]}
         if os.environ.get("MOE_BENCH_CPU_DETAIL", "1") != "0":
             # the 1-thread layer and the reference's routing
             # alone (Batch prebuilt, no marshalling) beside the GPU route stage
@@ -807,7 +810,8 @@ def run_b200(args):
     line = {
         "metric": "MoE-layer tokens/s (dynamic gating)" if mode == "dynamic" else "MoE-layer tokens/s (static gating)",
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms_per_step, "p50_ms": p50_max, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": ms_per_step, "p50_ms": p50_max, "p90_ms": p90_max, "higher_is_better": True,
+        "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (counter-hash uniform tokens; random-init experts, std 1/sqrt(fan-in))",
         "config": {"workload": desc, "S_per_gpu": S, "TD": TD, "HD": HD, "E": E, "top_k": k, "gating": mode,

@@ -86,6 +86,17 @@ class CpuLayer:
         return "reference gating.cpp (verbatim build)" if self.use_ref else "C restatement"
 
 
+def cpu_model() -> str:
+    """The host CPU (report the GPU box's CPU beside the baseline)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def blas_threads() -> int:
     """Threads the BLAS backing numpy will use (threadpoolctl)."""
     try:
@@ -130,6 +141,8 @@ def _cpu_layer_bench(S, TD, HD, E, k, min_seconds, max_passes, weight_pool, laye
         "dispatch_impl": L.dispatch_impl,
         "weight_pool": L.n_pool,
         "cores": blas_threads(),
+        "cpu_model": cpu_model(),
+        "host_cpus": os.cpu_count(),
         "sample": (f"{len(passes)} full layer passes (all {S} tokens, {S * k} slots, {E} experts; "
                    f"expert weights cycled over {L.n_pool} materialised experts), median pass; "
                    f"dispatch/combine = {L.dispatch_impl} (single-threaded, as the reference); "
