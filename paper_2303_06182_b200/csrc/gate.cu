@@ -539,6 +539,7 @@ const void* split_fn(int C, int k) {
 constexpr int kSmallMaxE = 32;
 constexpr int kSmallThreads = 512;
 constexpr int kSmallMaxSmem = 64 * 1024;
+constexpr int kSmallMaxVec = 16;  // 16-byte vectors of an X row per lane: TD <= 4096
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
   const uint32_t u[4] = {v.x, v.y, v.z, v.w};
@@ -554,21 +555,41 @@ __global__ void __launch_bounds__(kSmallThreads) gate_small_kernel(GateArgs a) {
   extern __shared__ uint4 swg[];  // Wg [E][TD] bf16
   const int vpr = a.TD / 8;       // 16-byte vectors per row
   const uint4* wg = reinterpret_cast<const uint4*>(a.Wg);
-  for (int i = threadIdx.x; i < a.E * vpr; i += blockDim.x) swg[i] = __ldg(wg + i);
-  __syncthreads();
+  // Wg -> smem with cp.async: the copies are in flight while this warp waits
+  // for the previous kernel and then loads its first X row
+  for (int i = threadIdx.x; i < a.E * vpr; i += blockDim.x)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ptx::smem_u32(swg + i)), "l"(wg + i)
+                 : "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
   pdl_trigger();
   pdl_wait();  // X belongs to the previous kernel until here
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
-  for (int t = blockIdx.x * wpb + (threadIdx.x >> 5); t < a.S; t += gridDim.x * wpb) {
-    const uint4* xr = reinterpret_cast<const uint4*>(a.X) + static_cast<size_t>(t) * vpr;
+  const int stride = gridDim.x * wpb;
+  int t = blockIdx.x * wpb + (threadIdx.x >> 5);
+  // this lane's 16-byte vectors of the current X row: the smem bound
+  // (E * TD * 2 <= 64 KB) caps TD at 4096 / 2048 / 1024 for EM = 8 / 16 / 32
+  constexpr int NV = kSmallMaxVec * 8 / EM;
+  uint4 xv[NV];
+  auto load_x = [&](int tt) {
+    const uint4* xr = reinterpret_cast<const uint4*>(a.X) + static_cast<size_t>(tt) * vpr;
+#pragma unroll
+    for (int u = 0; u < NV; ++u)
+      if (lane + 32 * u < vpr) xv[u] = __ldcs(xr + lane + 32 * u);
+  };
+  if (t < a.S) load_x(t);
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  for (; t < a.S; t += stride) {
     float acc[EM];
 #pragma unroll
     for (int e = 0; e < EM; ++e) acc[e] = 0.f;
-#pragma unroll 4
-    for (int v = lane; v < vpr; v += 32) {
+#pragma unroll
+    for (int u = 0; u < NV; ++u) {
+      const int v = lane + 32 * u;
+      if (v >= vpr) break;
       float xf[8];
-      bf16x8_to_f32(__ldcs(xr + v), xf);
+      bf16x8_to_f32(xv[u], xf);
 #pragma unroll
       for (int e = 0; e < EM; ++e) {
         if (e < a.E) {
@@ -579,6 +600,7 @@ __global__ void __launch_bounds__(kSmallThreads) gate_small_kernel(GateArgs a) {
         }
       }
     }
+    if (t + stride < a.S) load_x(t + stride);  // the next row is in flight during the reduction
 #pragma unroll
     for (int e = 0; e < EM; ++e)
 #pragma unroll
@@ -797,7 +819,9 @@ bool gate_small(int E, int TD) {
     const char* v = getenv("MOE_GATE_SMALL");
     return v ? atoi(v) : 1;
   }();
-  return env != 0 && E <= kSmallMaxE && TD % 8 == 0 && E * TD * 2 <= kSmallMaxSmem;
+  const int em = E <= 8 ? 8 : E <= 16 ? 16 : 32;  // the kernel's E bucket
+  return env != 0 && E <= kSmallMaxE && TD % 8 == 0 && TD / 8 <= 32 * (kSmallMaxVec * 8 / em) &&
+         E * TD * 2 <= kSmallMaxSmem;
 }
 
 cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateArgs& a,
