@@ -54,8 +54,11 @@ struct moe_ep {
   DevBuf<__nv_bfloat16> h, w1p, w2p;
   unsigned long long timeout_ns = 20ull * 1000 * 1000 * 1000;
   // CTAs of the dispatch kernel: every rank must use the same count (the
-  // receivers wait for D * dispatch_ctas arrivals); MOE_EP_DISPATCH_CTAS
-  int dispatch_ctas = 256;
+  // receivers wait for D * dispatch_ctas arrivals), hence a constant, one per
+  // B200 SM (world 1, ncu: 32 CTAs 106 us, 96 45 us, 148 34 us, 256 48 us,
+  // 512 69 us -- every CTA pays the count wait, the scans and a system-scope
+  // release); MOE_EP_DISPATCH_CTAS overrides
+  int dispatch_ctas = 148;
   int full_fence = 0;
   // MOE_EP_OVERLAP=1: expert-ordered dispatch with per-expert arrival counts,
   // GEMM1 tiles wait only for their expert's rows (the FFN starts while later
