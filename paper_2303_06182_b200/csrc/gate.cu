@@ -315,7 +315,11 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
   constexpr int kABytes = kBlockM * BK * 2;
   if (a.prof && threadIdx.x == 0) a.prof[kProf * blockIdx.x] = gate_clock();
   const GateLayout L = gate_layout(a.E, BK);
-  const int stage_bytes = kABytes + L.b_rows * BK * 2;
+  const int stage_bytes = kABytes + L.b_rows * BK * 2;  // one k-block (X box + Wg boxes)
+  // k-blocks per pipeline stage (one barrier phase): more bytes per phase
+  // keep more of one SM's TMA stream in flight (tools/probes/tma_l2_probe.cu)
+  const int kps = (a.kps > 1 && L.stages >= 2 * a.kps) ? a.kps : 1;
+  const int nstages = L.stages / kps;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.stages * stage_bytes);
   uint64_t* empty = full + L.stages;
   uint64_t* tfull = empty + L.stages;
@@ -373,26 +377,29 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
       const int b_lo = MC > 1 ? crank * per : 0;
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = kb_lo; kb < kb_hi; ++kb) {
+      for (int kb = kb_lo; kb < kb_hi; kb += kps) {
+        const int nk = min(kps, kb_hi - kb);  // k-blocks in this stage
         // free once every CTA of the cluster has consumed the stage
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         if (a.dbg & 2) {  // ablation: no loads at all
           ptx::mbar_arrive(&full[stage]);
         } else {
-          ptx::mbar_arrive_expect_tx(&full[stage], stage_bytes - ((a.dbg & 4) ? L.b_rows * BK * 2 : 0) -
-                                                       ((a.dbg & 8) ? kABytes : 0));
-          uint8_t* st = smem + stage * stage_bytes;
-          if (!(a.dbg & 8)) ptx::tma_load_2d(st, &tmX, &full[stage], kb * BK, tok0, pol_x);
-          for (int b = b_lo; b < b_lo + per && !(a.dbg & 4); ++b) {
-            const int r = b * L.box_rows;
-            if (MC > 1)
-              ptx::tma_load_2d_mc(st + kABytes + r * BK * 2, &tmWg, &full[stage], kb * BK, r,
-                                  static_cast<uint16_t>((1u << MC) - 1), pol_w);
-            else
-              ptx::tma_load_2d(st + kABytes + r * BK * 2, &tmWg, &full[stage], kb * BK, r, pol_w);
+          ptx::mbar_arrive_expect_tx(&full[stage], nk * (stage_bytes - ((a.dbg & 4) ? L.b_rows * BK * 2 : 0) -
+                                                         ((a.dbg & 8) ? kABytes : 0)));
+          for (int j = 0; j < nk; ++j) {
+            uint8_t* st = smem + (stage * kps + j) * stage_bytes;
+            if (!(a.dbg & 8)) ptx::tma_load_2d(st, &tmX, &full[stage], (kb + j) * BK, tok0, pol_x);
+            for (int b = b_lo; b < b_lo + per && !(a.dbg & 4); ++b) {
+              const int r = b * L.box_rows;
+              if (MC > 1)
+                ptx::tma_load_2d_mc(st + kABytes + r * BK * 2, &tmWg, &full[stage], (kb + j) * BK, r,
+                                    static_cast<uint16_t>((1u << MC) - 1), pol_w);
+              else
+                ptx::tma_load_2d(st + kABytes + r * BK * 2, &tmWg, &full[stage], (kb + j) * BK, r, pol_w);
+            }
           }
         }
-        if (++stage == L.stages) {
+        if (++stage == nstages) {
           stage = 0;
           phase ^= 1;
         }
@@ -408,11 +415,12 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
       const uint32_t id1 = ptx::idesc_bf16(kBlockM, n1 > 0 ? n1 : 16);
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = kb_lo; kb < kb_hi; ++kb) {
+      for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += kps) {
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
-        if (a.prof && kb == kb_lo) a.prof[kProf * blockIdx.x + 2] = gate_clock();
-        const uint32_t a0 = ptx::smem_u32(smem + stage * stage_bytes);
+        if (a.prof && kb0 == kb_lo) a.prof[kProf * blockIdx.x + 2] = gate_clock();
+        for (int kb = kb0; kb < min(kb0 + kps, kb_hi); ++kb) {
+        const uint32_t a0 = ptx::smem_u32(smem + (stage * kps + (kb - kb0)) * stage_bytes);
         const uint32_t b0 = a0 + kABytes;
 #pragma unroll
         for (int kk = 0; kk < BK / 16 && !(a.dbg & 1); ++kk) {
@@ -422,11 +430,12 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
             ptx::mma_bf16(tmem_base + 256, desc(a0 + kk * 32), desc(b0 + 256 * BK * 2 + kk * 32), id1,
                           acc);
         }
+        }
         if (!SPLIT && C > 1)
           ptx::mma_commit_mc(&empty[stage], static_cast<uint16_t>((1u << C) - 1));
         else
           ptx::mma_commit(&empty[stage]);
-        if (++stage == L.stages) {
+        if (++stage == nstages) {
           stage = 0;
           phase ^= 1;
         }
@@ -868,6 +877,13 @@ cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const G
   static const int dbg = getenv("MOE_GATE_DBG") ? atoi(getenv("MOE_GATE_DBG")) : 0;
   GateArgs b = a;
   b.dbg = dbg;
+  static const int kps_env = [] {
+    const char* v = getenv("MOE_GATE_KPS");
+    return v ? atoi(v) : 0;
+  }();
+  // measured (ncu, same box): 64-deep path (MT) 2 per stage 16.4 vs 17.5 us
+  // (1) / 17.7 (3); 32-deep E = 512 path (LM) 1 per stage 24.8 vs 28.5 (2)
+  b.kps = kps_env > 0 ? kps_env : (wide ? 2 : 1);
   static unsigned long long* prof_buf = nullptr;
   const int ctas = split ? tiles * C : tiles;
   if (prof) {
