@@ -260,3 +260,20 @@ def test_layer_oracle_combine_equals_reference_dispatch_and_combine(S, TD, HD, E
         out += ow[:, j].astype(np.float32)[:, None] * Y[op[:, j]]
     ref = OL.layer_forward(X, W1, W2, idx, w, E)
     assert np.array_equal(out, ref)
+
+
+@needs_ref
+def test_reference_routing_timer_runs_the_reference_functions():
+    """oracle/ref_capi.cpp ref_time_routing (bench.py cpu_baseline's routing
+    numbers): every timed function ran (positive times), static ones only when
+    a capacity factor is given, and the plans it timed are the reference's
+    (same order as ref_dynamic_dispatch)."""
+    rng = np.random.default_rng(5)
+    S, k, E = 4096, 2, 64
+    ex = np.stack([rng.permutation(E)[:k] for _ in range(S)]).astype(np.int32)
+    w = np.full((S, k), 0.5)
+    t = N.ref_time_routing(ex, w, E, 0.0, reps=2)
+    assert set(t) == {"dynamic_dispatch", "combine_dynamic"} and all(v > 0 for v in t.values())
+    t = N.ref_time_routing(ex, w, E, 0.25, reps=2)
+    assert set(t) == {"dynamic_dispatch", "combine_dynamic", "static_dispatch", "combine_static"}
+    assert all(v > 0 for v in t.values())
