@@ -265,9 +265,8 @@ def test_layer_oracle_combine_equals_reference_dispatch_and_combine(S, TD, HD, E
 @needs_ref
 def test_reference_routing_timer_runs_the_reference_functions():
     """oracle/ref_capi.cpp ref_time_routing (bench.py cpu_baseline's routing
-    numbers): every timed function ran (positive times), static ones only when
-    a capacity factor is given, and the plans it timed are the reference's
-    (same order as ref_dynamic_dispatch)."""
+    numbers): every timed function ran (positive times), the static ones only
+    when a capacity factor is given."""
     rng = np.random.default_rng(5)
     S, k, E = 4096, 2, 64
     ex = np.stack([rng.permutation(E)[:k] for _ in range(S)]).astype(np.int32)
