@@ -115,15 +115,20 @@ def test_layer_small_all_stages(S, TD, HD, E, k, tile_n):
     assert err < TOL_OUT
 
 
-def test_gate_ties_go_to_lower_expert():
-    S, TD, HD, E, k = 130, 128, 128, 8, 2
+@pytest.mark.parametrize("S,TD,E,k", [(130, 128, 8, 2),     # small-E CUDA-core gate
+                                      (300, 256, 512, 2),   # tcgen05 gate, 2 x N=256 MMAs, 32-deep
+                                      (300, 256, 512, 4),
+                                      (260, 256, 200, 3),   # tcgen05 gate, one N=208 MMA
+                                      (200, 256, 96, 2)])   # 64-deep tcgen05 gate
+def test_gate_ties_go_to_lower_expert(S, TD, E, k):
+    HD = 128
     shape = LayerShape(TD, HD, E, k)
     Wg, W1, W2 = make_weights(shape, seed=SEED)
     Wg[:] = Wg[0:1]  # every expert row identical -> all logits equal
     layer, x, out, w, v = _run(S, TD, HD, E, k, weights=(Wg, W1, W2))
     idx = v["idx"][:S * k].reshape(S, k).cpu().numpy()
-    assert (idx == np.array([0, 1])).all()
-    assert np.allclose(v["w"][:S * k].cpu().numpy(), 0.5)
+    assert (idx == np.arange(k)).all()
+    assert np.allclose(v["w"][:S * k].cpu().numpy(), 1.0 / k)
 
 
 def test_layer_cfg1_shape():
