@@ -49,6 +49,9 @@ CASES = [
     ("lm", 16384, 1024, 4096, 512, 2, "dynamic", 1.0, 2, 128),
     ("mt-seq128", 6144, 2048, 8192, 128, 2, "dynamic", 1.0, 2, 128),
     ("mt-seq256", 12288, 2048, 8192, 128, 2, "dynamic", 1.0, 2, 256),
+    # one GPU's share of the LM layer under expert parallelism at D = 8
+    # (64 local experts, n_e ~ 512: 256-token items on CTA pairs at LM dims)
+    ("lm-ep8-local", 16384, 1024, 4096, 64, 2, "dynamic", 1.0, 2, 256),
     ("lm-static", 16384, 1024, 4096, 512, 2, "static", 0.05, None, None),
     ("mt-static", 6144, 2048, 8192, 128, 2, "static", 1.0, None, None),
     # BASELINE's capacity factors drop nothing at these shapes (cap 820 vs
