@@ -408,6 +408,10 @@ def test_split_k_gate_matches_one_cta_gate(S, TD, HD, E, k, tmp_path):
     (129, 256, 512, 5, 1, "dynamic", 1.0),     # E not a power of two, S not a tile multiple
     (4097, 256, 256, 64, 2, "dynamic", 1.0),   # just past the single-CTA route (multi-block sort)
     (300, 256, 512, 8, 2, "static", 0.1),      # static with drops, one-launch fused FFN
+    (1, 256, 256, 512, 2, "dynamic", 1.0),     # a single token through the E = 512 tcgen05 gate
+    (3, 256, 256, 1, 1, "dynamic", 1.0),       # one expert
+    (33, 256, 256, 33, 2, "dynamic", 1.0),     # first E past the CUDA-core gate (64-deep, E_pad 48)
+    (200, 256, 256, 128, 8, "dynamic", 1.0),   # k = 8 on the tcgen05 gate
 ])
 def test_layer_edge_shapes_fused_default(S, TD, HD, E, k, mode, C):
     """The default (fused, packed) path on edge shapes: routing bit-exact,
