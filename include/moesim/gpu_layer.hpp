@@ -133,8 +133,12 @@ struct StageTimes {
 // device weights Wg [E,TD], W1 [E,HD,TD], W2 [E,TD,HD].
 class MoeLayer {
  public:
+  // weights_packed: W1/W2 are already tile-packed (pack_expert_weights, e.g.
+  // in place) and are streamed as given -- expert weights held once.
+  // W1 = W2 = nullptr: a pool-only layer for expert buffering (ExpertCache).
   MoeLayer(Context& ctx, const LayerShape& shape, int max_tokens, const GatingConfig& gating,
-           const void* Wg, const void* W1, const void* W2, bool keep_logits = false)
+           const void* Wg, const void* W1, const void* W2, bool keep_logits = false,
+           bool weights_packed = false)
       : ctx_(&ctx), shape_(shape) {
     if (gating.num_experts != shape.num_experts || gating.top_k != shape.top_k)
       throw std::invalid_argument("gating config does not match the layer shape");
@@ -147,6 +151,7 @@ class MoeLayer {
     d.mode = gating.mode == GatingMode::kStatic ? MOE_GATING_STATIC : MOE_GATING_DYNAMIC;
     d.capacity_factor = gating.capacity_factor;
     d.keep_logits = keep_logits ? 1 : 0;
+    d.weights_packed = weights_packed ? 1 : 0;
     check(moe_layer_create(ctx.get(), &d, Wg, W1, W2, &h_));
   }
   ~MoeLayer() { moe_layer_destroy(h_); }
@@ -198,6 +203,13 @@ class MoeLayer {
   LayerShape shape_;
   moe_layer* h_ = nullptr;
 };
+
+// Expert weights [rows, K] bf16 -> the tile-packed layout the fused FFN
+// streams; dst == src packs in place (moe_pack_expert_weights).
+inline void pack_expert_weights(Context& ctx, const void* src, void* dst, std::int64_t rows, int K,
+                                void* stream = nullptr) {
+  check(moe_pack_expert_weights(ctx.get(), src, dst, rows, K, stream));
+}
 
 // GPU-resident LIFO/FIFO expert cache over pinned host weights
 // (buffer.hpp access_batch decisions).  While it exists the layer reads its
@@ -252,23 +264,35 @@ class ExpertParallelLayer {
  public:
   using AllGather = std::function<std::vector<std::string>(const std::string& mine)>;
 
+  // NCCL transport (moe_ep_connect_nccl): rank 0's unique id reaches every
+  // rank through `broadcast` (called on every rank with rank 0's bytes on
+  // rank 0, returns rank 0's bytes everywhere).
+  using Broadcast = std::function<std::string(const std::string& root_bytes)>;
+  struct Nccl {
+    Broadcast broadcast;
+  };
+
+  ExpertParallelLayer(Context& ctx, const LayerShape& shape, int rank, int world_size,
+                      int max_tokens, const std::vector<std::int32_t>& device_of, const void* Wg,
+                      const void* W1_local, const void* W2_local, const Nccl& nccl,
+                      int max_recv_rows = 0)
+      : ctx_(&ctx), shape_(shape), world_(world_size) {
+    create(ctx, shape, rank, world_size, max_tokens, device_of, Wg, W1_local, W2_local, max_recv_rows,
+           MOE_EP_TRANSPORT_NCCL);
+    std::string id(MOE_NCCL_ID_BYTES, '\0');
+    if (rank == 0) check(moe_nccl_get_unique_id(id.data()));
+    if (world_size > 1) id = nccl.broadcast(id);
+    if (id.size() != MOE_NCCL_ID_BYTES) throw std::invalid_argument("bad NCCL id size");
+    check(moe_ep_connect_nccl(h_, id.data()));
+  }
+
   ExpertParallelLayer(Context& ctx, const LayerShape& shape, int rank, int world_size,
                       int max_tokens, const std::vector<std::int32_t>& device_of, const void* Wg,
                       const void* W1_local, const void* W2_local, const AllGather& all_gather,
                       int max_recv_rows = 0)
       : ctx_(&ctx), shape_(shape), world_(world_size) {
-    if (static_cast<int>(device_of.size()) != shape.num_experts)
-      throw std::invalid_argument("device_of must have one entry per expert");
-    moe_ep_desc d{};
-    d.rank = rank;
-    d.world_size = world_size;
-    d.max_tokens = max_tokens;
-    d.token_dim = shape.token_dim;
-    d.hidden_dim = shape.hidden_dim;
-    d.num_experts = shape.num_experts;
-    d.top_k = shape.top_k;
-    d.max_recv_rows = max_recv_rows;
-    check(moe_ep_create(ctx.get(), &d, Wg, W1_local, W2_local, device_of.data(), &h_));
+    create(ctx, shape, rank, world_size, max_tokens, device_of, Wg, W1_local, W2_local, max_recv_rows,
+           MOE_EP_TRANSPORT_P2P);
     std::string mine(MOE_EP_HANDLE_BYTES, '\0');
     check(moe_ep_get_handle(h_, mine.data()));
     std::vector<std::string> all = world_size > 1 ? all_gather(mine) : std::vector<std::string>{mine};
@@ -301,6 +325,25 @@ class ExpertParallelLayer {
   }
 
  private:
+  // the moe_ep object of either transport
+  void create(Context& ctx, const LayerShape& shape, int rank, int world_size, int max_tokens,
+              const std::vector<std::int32_t>& device_of, const void* Wg, const void* W1_local,
+              const void* W2_local, int max_recv_rows, int transport) {
+    if (static_cast<int>(device_of.size()) != shape.num_experts)
+      throw std::invalid_argument("device_of must have one entry per expert");
+    moe_ep_desc d{};
+    d.rank = rank;
+    d.world_size = world_size;
+    d.max_tokens = max_tokens;
+    d.token_dim = shape.token_dim;
+    d.hidden_dim = shape.hidden_dim;
+    d.num_experts = shape.num_experts;
+    d.top_k = shape.top_k;
+    d.max_recv_rows = max_recv_rows;
+    d.transport = transport;
+    check(moe_ep_create(ctx.get(), &d, Wg, W1_local, W2_local, device_of.data(), &h_));
+  }
+
   Context* ctx_;
   LayerShape shape_;
   int world_;

@@ -308,16 +308,18 @@ def test_peer_ep_missing_peer_times_out_instead_of_hanging():
     assert res[0] == MOE_ERR_PEER_TIMEOUT
 
 
-@pytest.mark.parametrize("world", [1, 2, 4])
-def test_cxx_host_expert_parallel_demo(world, tmp_path):
+@pytest.mark.parametrize("world,transport", [(1, "p2p"), (2, "p2p"), (4, "p2p"), (1, "nccl")])
+def test_cxx_host_expert_parallel_demo(world, transport, tmp_path):
     """Pure C++ host (include/moesim/gpu_layer.hpp ExpertParallelLayer), ranks
-    forked by tools/ep_p2p_demo.cpp, handles exchanged through files; every
-    rank's rows bitwise equal to the single-GPU layer."""
+    forked by tools/ep_p2p_demo.cpp, handles (p2p) or the NCCL unique id
+    exchanged through files; every rank's rows bitwise equal to the
+    single-GPU layer.  NCCL refuses two ranks on one GPU: world 1 here."""
     import subprocess
 
     exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "build", "bin",
                        "ep_p2p_demo")
     r = subprocess.run([exe, "--world", str(world), "--tokens", "1024", "--experts", "32",
-                        "--dir", str(tmp_path / "ep")], capture_output=True, text=True, timeout=300)
+                        "--transport", transport, "--dir", str(tmp_path / "ep")],
+                       capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 rows differ" in r.stdout

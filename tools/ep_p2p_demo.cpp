@@ -10,7 +10,7 @@
 //
 //   ep_p2p_demo [--world 2] [--devices 1] [--tokens 2048] [--token-dim 1024]
 //               [--hidden-dim 4096] [--experts 64] [--topk 2] [--steps 4]
-//               [--dir /tmp/ep_demo]
+//               [--dir /tmp/ep_demo] [--transport p2p|nccl]
 // Exit 0 = bitwise equal on every rank and step.
 #include <sys/wait.h>
 #include <unistd.h>
@@ -22,6 +22,7 @@
 #include <filesystem>
 #include <fstream>
 #include <iostream>
+#include <memory>
 #include <sstream>
 #include <string>
 #include <thread>
@@ -38,6 +39,7 @@ struct Options {
   int world = 2, devices = 1, tokens = 2048, token_dim = 1024, hidden_dim = 4096, experts = 64,
       topk = 2, steps = 4;
   std::string dir = "/tmp/ep_p2p_demo";
+  std::string transport = "p2p";  // or "nccl" (NCCL refuses two ranks on one GPU: world 1 there)
 };
 
 constexpr std::uint64_t kSeed = 2303061820ull;
@@ -62,6 +64,7 @@ Options parse(int argc, char** argv) {
     else if (a == "--topk") o.topk = std::stoi(next());
     else if (a == "--steps") o.steps = std::stoi(next());
     else if (a == "--dir") o.dir = next();
+    else if (a == "--transport") o.transport = next();
     else {
       std::cerr << "unknown option " << a << "\n";
       std::exit(2);
@@ -142,12 +145,24 @@ int run_rank(const Options& o, int rank) {
   const char* w2 = static_cast<const char*>(m.w2.get()) + (std::size_t)rank * El * TD * HD * 2;
   std::string bits;
   {
-    gpu::ExpertParallelLayer ep(ctx, {TD, HD, E, o.topk}, rank, D, S, device_of, m.wg.get(), w1, w2,
-                                [&](const std::string& mine) {
-                                  return file_all_gather(o.dir, "handle", rank, D, mine);
-                                });
+    std::unique_ptr<gpu::ExpertParallelLayer> ep_ptr;
+    if (o.transport == "nccl") {
+      gpu::ExpertParallelLayer::Nccl nccl{[&](const std::string& root_bytes) {
+        return file_all_gather(o.dir, "ncclid", rank, D, root_bytes)[0];
+      }};
+      ep_ptr = std::make_unique<gpu::ExpertParallelLayer>(ctx, gpu::LayerShape{TD, HD, E, o.topk}, rank, D, S,
+                                                          device_of, m.wg.get(), w1, w2, nccl);
+    } else {
+      ep_ptr = std::make_unique<gpu::ExpertParallelLayer>(
+          ctx, gpu::LayerShape{TD, HD, E, o.topk}, rank, D, S, device_of, m.wg.get(), w1, w2,
+          gpu::ExpertParallelLayer::AllGather([&](const std::string& mine) {
+            return file_all_gather(o.dir, "handle", rank, D, mine);
+          }));
+    }
+    gpu::ExpertParallelLayer& ep = *ep_ptr;
+    const bool graph_ok = o.transport != "nccl";  // the NCCL transport syncs the host: eager
     for (int step = 0; step < o.steps; ++step) {
-      if (step < o.steps / 2)
+      if (step < o.steps / 2 || !graph_ok)
         ep.forward(xl.get(), S, out.get(), stream.get());
       else
         ep.forward_graph(xl.get(), S, out.get(), stream.get());
