@@ -66,3 +66,28 @@ def test_gpus_flag_must_match_world_size():
     r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--dry-run"], cwd=ROOT, capture_output=True,
                        text=True, timeout=120, env=env)
     assert r.returncode != 0 and "WORLD_SIZE=1" in (r.stderr + r.stdout)
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(400)
+def test_b200_arm_json_line_on_gpu():
+    """The driver's own arm on the B200 (short run): one JSON line with every
+    key of the contract, the roofline / cpu_baseline / e2e / clocks objects,
+    e2e copies counted, and a positive kernel-launch claim."""
+    env = dict(os.environ, MOE_CPU_BASELINE_SECONDS="1", MOE_BENCH_CPU_DETAIL="0")
+    r = subprocess.run([sys.executable, "bench.py", "--workload", "cfg1", "--steps", "5", "--warmup", "3",
+                        "--e2e-steps", "4"], cwd=ROOT, capture_output=True, text=True, timeout=380, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    need = (KEYS - {"impl"}) | {"roofline", "clocks", "gpu_launches", "p50_ms"}
+    assert need <= set(d), need - set(d)
+    assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3 and d["value"] > 0
+    ro = d["roofline"]
+    assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(ro) and ro["frac"] > 0
+    cb = d["cpu_baseline"]
+    assert {"value", "unit", "cores", "kind", "sample"} <= set(cb)
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] >= 5 * 5
