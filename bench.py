@@ -175,9 +175,19 @@ def load_traffic(workload):
         return None
 
 
+def _write_line(text):
+    """One line to stdout in as few write(2) calls as the pipe allows: under
+    torchrun every rank shares the parent's stdout, and print() may split a
+    line around another rank's output."""
+    sys.stdout.flush()
+    buf = (text + "\n").encode()
+    while buf:
+        buf = buf[os.write(1, buf):]
+
+
 def emit(line, args):
     """The one JSON line on stdout (+ --json-out copy)."""
-    print(json.dumps(line), flush=True)
+    _write_line(json.dumps(line))
     if getattr(args, "json_out", None):
         with open(args.json_out, "w") as f:
             json.dump(line, f, indent=1)
@@ -900,8 +910,9 @@ def main():
     if args.impl != "reference" and world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.dry_run:
-        print(json.dumps({"dry_run": True, "impl": args.impl, "n_gpus": args.gpus, "world": world,
-                          "rank": int(os.environ.get("RANK", "0")), "scaling": args.scaling}), flush=True)
+        # every rank prints here
+        _write_line(json.dumps({"dry_run": True, "impl": args.impl, "n_gpus": args.gpus, "world": world,
+                                "rank": int(os.environ.get("RANK", "0")), "scaling": args.scaling}))
         return
     if args.impl == "reference":
         run_reference(args)
