@@ -97,12 +97,36 @@ inline int encode_packed(CUtensorMap* m, const void* ptr, uint64_t n) {
   return MOE_OK;
 }
 
+// [rows, cols] bf16 as a 3-D tensor (64 cols, rows, cols / 64 chunks): a box of
+// {64, box_rows, 2} lands as two chunk slabs of box_rows x 128 B, 128-byte swizzled.
+inline int encode_rows_k2(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  int st = get_encoder();
+  if (st) return st;
+  cuuint64_t dims[3] = {64, rows, cols / 64};
+  cuuint64_t strides[2] = {cols * 2, 128};
+  cuuint32_t box[3] = {64, box_rows, 2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed (3-D row boxes)");
+  return MOE_OK;
+}
+
 inline int encode_rows(moe::RowMaps* m, const void* ptr, uint64_t rows, uint64_t cols) {
   int st;
   if ((st = encode_bf16(&m->m8, ptr, rows, cols, 8)) ||
       (st = encode_bf16(&m->m16, ptr, rows, cols, 16)) ||
       (st = encode_bf16(&m->m32, ptr, rows, cols, 32)) ||
       (st = encode_bf16(&m->m64, ptr, rows, cols, 64)))
+    return st;
+  static const bool k2 = [] {
+    const char* v = getenv("MOE_FFN_ROWS_K2");
+    return !v || atoi(v) != 0;
+  }();
+  m->has_k2 = k2 && cols % 128 == 0;
+  if (m->has_k2 && ((st = encode_rows_k2(&m->k2r64, ptr, rows, cols, 64)) ||
+                    (st = encode_rows_k2(&m->k2r128, ptr, rows, cols, 128))))
     return st;
   return MOE_OK;
 }

@@ -264,6 +264,8 @@ __global__ void __launch_bounds__(256, 1)
       // packed weights: the stage's KCH tiles are consecutive 16 KB tiles,
       // already in the swizzled smem order -> one 1-D bulk copy
       const uint8_t* wbulk = static_cast<const uint8_t*>(tr.gemm ? g.W2p : g.W1p);
+      // a full 128-row item at KCH = 2: the stage's token rows as one 3-D box
+      const bool b_k2 = BN == 128 && KCH == 2 && nrows == 128 && tB->has_k2 && !(g.dbg & 1);
       for (int kb = 0; kb < KB; ++kb) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         ptx::mbar_arrive_expect_tx(&full[stage], bytes);
@@ -280,6 +282,10 @@ __global__ void __launch_bounds__(256, 1)
                              pol_w);
           uint8_t* b_dst = sB + stage * Cfg::kBBytes + c * Cfg::kBChunk;
           if (g.dbg & 1) continue;
+          if (b_k2) {
+            if (c == 0) ptx::tma_load_3d(b_dst, &tB->k2r128, &full[stage], 0, it.row0, kb * KCH, pol_x);
+            continue;
+          }
           int r = 0;
           for (; r + 64 <= nrows; r += 64)
             ptx::tma_load_2d(b_dst + r * kChunkK * 2, &tB->m64, &full[stage], k0, it.row0 + r,

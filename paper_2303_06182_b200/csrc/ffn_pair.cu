@@ -136,6 +136,16 @@ __device__ __forceinline__ void arrive_remote(uint32_t cluster_bar) {
                : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d_pair(void* smem_dst, const CUtensorMap* m,
+                                                 uint32_t leader_bar, int32_t c0, int32_t c1, int32_t c2,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(ptx::smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+      : "memory");
+}
+
 // rows [r0, r0 + h) of B (h % 8 == 0) into dst with 64/32/16/8-row boxes
 __device__ __forceinline__ void load_rows(uint8_t* dst, const RowMaps* m, uint32_t bar, int k0,
                                           int r0, int h, uint64_t pol) {
@@ -309,6 +319,7 @@ __global__ void __launch_bounds__(256, 1)
       }
       // both CTAs' A halves + all token rows, counted on the leader's barrier
       const uint32_t bytes = 2 * kABytes + kKch * nrows * kChunkK * 2;
+      const bool b_k2 = kKch == 2 && (half == 128 || half == 64) && half * 2 == kBN && tB->has_k2;
       for (int kb = 0; kb < KB; ++kb) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         const uint32_t fb = leader_addr(&full[stage]);
@@ -317,11 +328,14 @@ __global__ void __launch_bounds__(256, 1)
         // packed weights: the stage's two consecutive (pre-swizzled) tiles as
         // one 256-row box
         if (g.packed) tma_load_2d_pair(sA + stage * kABytes, tA, fb, 0, (a_tile + kb * kKch) * kBlockM, pol_w);
+        if (b_k2)  // this CTA's full half of the token rows, both k chunks, one 3-D box
+          tma_load_3d_pair(sB + stage * kBBytes, half == 128 ? &tB->k2r128 : &tB->k2r64, fb, 0, b_row,
+                           kb * kKch, pol_x);
 #pragma unroll
         for (int c = 0; c < kKch; ++c) {
           const int k0 = kb * kStageK + c * kChunkK;
           if (!g.packed) tma_load_2d_pair(sA + stage * kABytes + c * kAChunk, tA, fb, k0, a_row, pol_w);
-          load_rows(sB + stage * kBBytes + c * kBChunk, tB, fb, k0, b_row, half, pol_x);
+          if (!b_k2) load_rows(sB + stage * kBBytes + c * kBChunk, tB, fb, k0, b_row, half, pol_x);
         }
         if (++stage == kStages) {
           stage = 0;

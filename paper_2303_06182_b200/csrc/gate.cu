@@ -228,6 +228,20 @@ __device__ __forceinline__ void gate_epilogue(const GateArgs& a, uint32_t tmem_b
   };
   uint32_t ra[32], rb[32];
   int c0 = c_begin;
+  if (a.dbg & 48) {  // epilogue ablations: 16 no TMEM loads, 32 no scan (wrong results)
+#pragma unroll
+    for (int i = 0; i < 32; ++i) ra[i] = __float_as_uint(static_cast<float>(i ^ lane));
+    for (; c0 < c_end; c0 += 32) {
+      if (!(a.dbg & 16)) {
+        ptx::tmem_ld32(trow + c0, ra);
+        ptx::tmem_ld_wait();
+      }
+      reg_fence32(ra);
+      if (!(a.dbg & 32)) consume(ra, c0);
+    }
+    if (a.dbg & 32) bv[0] = __uint_as_float(ra[0] ^ ra[31]);
+    c0 = c_end;
+  }
   if (c0 < c_end) ptx::tmem_ld32(trow + c0, ra);
   while (c0 < c_end) {
     ptx::tmem_ld_wait();

@@ -160,6 +160,11 @@ struct FusedFfnArgs {
 // 16 and 8 -- a few TMA issues per k-block instead of n/16.
 struct RowMaps {
   CUtensorMap m8, m16, m32, m64;
+  // 3-D views [k chunk][row][64 cols] with boxes of two consecutive 64-wide k
+  // chunks x 64 / 128 rows: one request per KCH = 2 stage for a full block of
+  // token rows (lands chunk-major, the smem layout of the stage)
+  CUtensorMap k2r64, k2r128;
+  int has_k2;
 };
 cudaError_t fused_ffn_prepare();
 // whether launch_fused_ffn will run the CTA-pair kernel for these arguments
