@@ -27,6 +27,7 @@
 //     their fp32 partial logits into the leader's shared memory over DSMEM
 //     (mapa + st.shared::cluster) and the leader adds them in rank order
 //     (deterministic) before the top-k -- C times the SMs streaming X.
+#include <cudaTypedefs.h>
 #include <float.h>
 
 #include <algorithm>
@@ -321,9 +322,16 @@ __device__ __forceinline__ void gate_epilogue(const GateArgs& a, uint32_t tmem_b
 //   SPLIT = true:  a cluster of C CTAs = one tile, CTA r covering k-blocks
 //                  [r*KB/C, (r+1)*KB/C) (C = 2..8), partials reduced into the
 //                  leader over DSMEM.
+// 3-D views of X and Wg ({BK cols, rows, TD / BK k-blocks}, boxes of 128 /
+// b_rows rows x 2 k-blocks): a 2-k-block stage's X and Wg as one request each
+struct GateK2Maps {
+  CUtensorMap x, w;
+  int on;
+};
+
 template <int K, int C = 1, int BK = kBlockK, bool SPLIT = false>
 __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensorMap& tmWg,
-                                          const GateArgs& a, uint8_t* smem) {
+                                          const GateK2Maps& k2m, const GateArgs& a, uint8_t* smem) {
   static_assert(SPLIT ? (C >= 2 && C <= 8) : (C == 1 || C == 2 || C == 4), "cluster shape");
   static_assert(BK == 32 || BK == 64, "32-deep (64-byte swizzle) or 64-deep (128-byte) k-blocks");
   constexpr int kABytes = kBlockM * BK * 2;
@@ -334,6 +342,10 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
   // keep more of one SM's TMA stream in flight (tools/probes/tma_l2_probe.cu)
   const int kps = (a.kps > 1 && L.stages >= 2 * a.kps) ? a.kps : 1;
   const int nstages = L.stages / kps;
+  // stage s holds its kps X boxes, then their kps Wg slabs
+  const int w_bytes = L.b_rows * BK * 2;
+  auto x_at = [&](int st, int j) { return smem + st * kps * stage_bytes + j * kABytes; };
+  auto w_at = [&](int st, int j) { return smem + st * kps * stage_bytes + kps * kABytes + j * w_bytes; };
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.stages * stage_bytes);
   uint64_t* empty = full + L.stages;
   uint64_t* tfull = empty + L.stages;
@@ -400,16 +412,21 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
         } else {
           ptx::mbar_arrive_expect_tx(&full[stage], nk * (stage_bytes - ((a.dbg & 4) ? L.b_rows * BK * 2 : 0) -
                                                          ((a.dbg & 8) ? kABytes : 0)));
-          for (int j = 0; j < nk; ++j) {
-            uint8_t* st = smem + (stage * kps + j) * stage_bytes;
-            if (!(a.dbg & 8)) ptx::tma_load_2d(st, &tmX, &full[stage], (kb + j) * BK, tok0, pol_x);
-            for (int b = b_lo; b < b_lo + per && !(a.dbg & 4); ++b) {
-              const int r = b * L.box_rows;
-              if (MC > 1)
-                ptx::tma_load_2d_mc(st + kABytes + r * BK * 2, &tmWg, &full[stage], (kb + j) * BK, r,
-                                    static_cast<uint16_t>((1u << MC) - 1), pol_w);
-              else
-                ptx::tma_load_2d(st + kABytes + r * BK * 2, &tmWg, &full[stage], (kb + j) * BK, r, pol_w);
+          if (MC == 1 && k2m.on && nk == kps) {
+            // all k-blocks of the stage: one X request, one Wg request
+            if (!(a.dbg & 8)) ptx::tma_load_3d(x_at(stage, 0), &k2m.x, &full[stage], 0, tok0, kb, pol_x);
+            if (!(a.dbg & 4)) ptx::tma_load_3d(w_at(stage, 0), &k2m.w, &full[stage], 0, 0, kb, pol_w);
+          } else {
+            for (int j = 0; j < nk; ++j) {
+              if (!(a.dbg & 8)) ptx::tma_load_2d(x_at(stage, j), &tmX, &full[stage], (kb + j) * BK, tok0, pol_x);
+              for (int b = b_lo; b < b_lo + per && !(a.dbg & 4); ++b) {
+                const int r = b * L.box_rows;
+                if (MC > 1)
+                  ptx::tma_load_2d_mc(w_at(stage, j) + r * BK * 2, &tmWg, &full[stage], (kb + j) * BK, r,
+                                      static_cast<uint16_t>((1u << MC) - 1), pol_w);
+                else
+                  ptx::tma_load_2d(w_at(stage, j) + r * BK * 2, &tmWg, &full[stage], (kb + j) * BK, r, pol_w);
+              }
             }
           }
         }
@@ -434,8 +451,8 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
         ptx::tc_fence_after();
         if (a.prof && kb0 == kb_lo) a.prof[kProf * blockIdx.x + 2] = gate_clock();
         for (int kb = kb0; kb < min(kb0 + kps, kb_hi); ++kb) {
-        const uint32_t a0 = ptx::smem_u32(smem + (stage * kps + (kb - kb0)) * stage_bytes);
-        const uint32_t b0 = a0 + kABytes;
+        const uint32_t a0 = ptx::smem_u32(x_at(stage, kb - kb0));
+        const uint32_t b0 = ptx::smem_u32(w_at(stage, kb - kb0));
 #pragma unroll
         for (int kk = 0; kk < BK / 16 && !(a.dbg & 1); ++kk) {
           const uint32_t acc = (kb != kb_lo || kk != 0) ? 1u : 0u;
@@ -528,8 +545,9 @@ __device__ __forceinline__ uint8_t* aligned_smem() {
 template <int K, int C, int BK, bool SPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
     gate_topk_kernel(const __grid_constant__ CUtensorMap tmX,
-                     const __grid_constant__ CUtensorMap tmWg, GateArgs a) {
-  gate_tile<K, C, BK, SPLIT>(tmX, tmWg, a, aligned_smem());
+                     const __grid_constant__ CUtensorMap tmWg, const __grid_constant__ GateK2Maps k2m,
+                     GateArgs a) {
+  gate_tile<K, C, BK, SPLIT>(tmX, tmWg, k2m, a, aligned_smem());
 }
 
 template <int C, int BK, bool SPLIT = false>
@@ -789,7 +807,7 @@ int gate_split(int E, int TD, int tiles, int sms) {
 }
 
 template <int K, int BK>
-cudaError_t launch_gate_k(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateArgs& a,
+cudaError_t launch_gate_k(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateK2Maps& k2m, const GateArgs& a,
                           int C, bool split, int tiles, int smem, cudaStream_t stream) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(split ? tiles * C : (tiles + C - 1) / C * C);
@@ -813,26 +831,26 @@ cudaError_t launch_gate_k(const CUtensorMap& tmX, const CUtensorMap& tmWg, const
   if (split) {
     if constexpr (BK == 64) {
       switch (C) {
-        case 2: return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 2, 64, true>, tmX, tmWg, a);
-        case 3: return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 3, 64, true>, tmX, tmWg, a);
-        case 4: return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 4, 64, true>, tmX, tmWg, a);
-        default: return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 8, 64, true>, tmX, tmWg, a);
+        case 2: return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 2, 64, true>, tmX, tmWg, k2m, a);
+        case 3: return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 3, 64, true>, tmX, tmWg, k2m, a);
+        case 4: return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 4, 64, true>, tmX, tmWg, k2m, a);
+        default: return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 8, 64, true>, tmX, tmWg, k2m, a);
       }
     }
     return cudaErrorInvalidValue;
   }
-  if (C == 4) return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 4, BK, false>, tmX, tmWg, a);
-  if (C == 2) return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 2, BK, false>, tmX, tmWg, a);
-  return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 1, BK, false>, tmX, tmWg, a);
+  if (C == 4) return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 4, BK, false>, tmX, tmWg, k2m, a);
+  if (C == 2) return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 2, BK, false>, tmX, tmWg, k2m, a);
+  return cudaLaunchKernelEx(&cfg, gate_topk_kernel<K, 1, BK, false>, tmX, tmWg, k2m, a);
 }
 
 template <int BK>
-cudaError_t launch_gate_bk(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateArgs& a, int C,
+cudaError_t launch_gate_bk(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateK2Maps& k2m, const GateArgs& a, int C,
                            bool split, int tiles, int smem, cudaStream_t stream) {
-  if (a.k == 1) return launch_gate_k<1, BK>(tmX, tmWg, a, C, split, tiles, smem, stream);
-  if (a.k == 2) return launch_gate_k<2, BK>(tmX, tmWg, a, C, split, tiles, smem, stream);
-  if (a.k <= 4) return launch_gate_k<4, BK>(tmX, tmWg, a, C, split, tiles, smem, stream);
-  return launch_gate_k<8, BK>(tmX, tmWg, a, C, split, tiles, smem, stream);
+  if (a.k == 1) return launch_gate_k<1, BK>(tmX, tmWg, k2m, a, C, split, tiles, smem, stream);
+  if (a.k == 2) return launch_gate_k<2, BK>(tmX, tmWg, k2m, a, C, split, tiles, smem, stream);
+  if (a.k <= 4) return launch_gate_k<4, BK>(tmX, tmWg, k2m, a, C, split, tiles, smem, stream);
+  return launch_gate_k<8, BK>(tmX, tmWg, k2m, a, C, split, tiles, smem, stream);
 }
 
 }  // namespace
@@ -845,6 +863,50 @@ bool gate_small(int E, int TD) {
   const int em = E <= 8 ? 8 : E <= 16 ? 16 : 32;  // the kernel's E bucket
   return env != 0 && E <= kSmallMaxE && TD % 8 == 0 && TD / 8 <= 32 * (kSmallMaxVec * 8 / em) &&
          E * TD * 2 <= kSmallMaxSmem;
+}
+
+// The 3-D X / Wg views of a 64-deep, two-k-blocks-per-stage launch, cached per
+// (X, Wg, S, TD, E) (encoding is host work; graph replays reuse the captured
+// parameters).  MOE_GATE_K2=0 disables.  False when unavailable.
+bool gate_k2_maps(GateK2Maps* m, const void* X, const void* Wg, int S, int TD, int E, int b_rows, int depth) {
+  static const bool enabled = [] {
+    const char* v = getenv("MOE_GATE_K2");
+    return !v || atoi(v) != 0;
+  }();
+  if (!enabled || TD % 64) return false;
+  using Key = std::tuple<const void*, const void*, int, int, int, int>;
+  static std::mutex mu;
+  static std::map<Key, std::pair<CUtensorMap, CUtensorMap>> cache;
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!enc) return false;
+  std::lock_guard<std::mutex> lock(mu);
+  const Key key{X, Wg, S, TD, E, depth};
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    if (cache.size() > 256) cache.clear();
+    std::pair<CUtensorMap, CUtensorMap> v;
+    auto encode = [&](CUtensorMap* t, const void* p, int rows, int box_rows) {
+      cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(TD / 64)};
+      cuuint64_t strides[2] = {(cuuint64_t)TD * 2, 128};
+      cuuint32_t box[3] = {64, (cuuint32_t)box_rows, (cuuint32_t)depth};
+      cuuint32_t estr[3] = {1, 1, 1};
+      return enc(t, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(p), dims, strides, box, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    if (!encode(&v.first, X, S, kBlockM) || !encode(&v.second, Wg, E, b_rows)) return false;
+    it = cache.emplace(key, v).first;
+  }
+  m->x = it->second.first;
+  m->w = it->second.second;
+  return true;
 }
 
 cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateArgs& a,
@@ -905,8 +967,12 @@ cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const G
     if (prof_buf) cudaMemsetAsync(prof_buf, 0, kProf * 4096 * sizeof(unsigned long long), stream);
     b.prof = ctas <= 4096 ? prof_buf : nullptr;
   }
-  const cudaError_t e = wide ? launch_gate_bk<64>(tmX, tmWg, b, C, split, tiles, L.smem, stream)
-                             : launch_gate_bk<kBlockK>(tmX, tmWg, b, C, split, tiles, L.smem, stream);
+  GateK2Maps k2m;
+  k2m.on = 0;
+  if (wide && b.kps >= 2 && L.stages >= 2 * b.kps && (split || C == 1) && L.b_rows <= 256 && a.X && a.Wg)
+    k2m.on = gate_k2_maps(&k2m, a.X, a.Wg, a.S, a.TD, a.E, L.b_rows, b.kps) ? 1 : 0;
+  const cudaError_t e = wide ? launch_gate_bk<64>(tmX, tmWg, k2m, b, C, split, tiles, L.smem, stream)
+                             : launch_gate_bk<kBlockK>(tmX, tmWg, k2m, b, C, split, tiles, L.smem, stream);
   if (!b.prof || e != cudaSuccess) return e;
   // experiments only: mean per-CTA phase times of this launch (split
   // followers have no epilogue stamps and are left out)
