@@ -175,10 +175,24 @@ __global__ void __launch_bounds__(kSingle ? kSingleThreads : kMultiThreads)
 
   // ---- phase 1: warp-aggregated histogram
   for (int i = threadIdx.x; i < kWarps * E; i += blockDim.x) warp_cnt[i] = 0;
+  // a warp whose slots fit one prefetch batch keeps its keys (and the slots'
+  // gate weights) in registers for phase 3 instead of re-reading them
+  const bool keep = w_hi - w_lo <= 32 * kPrefetch;
+  int kept[kPrefetch];
+  float kept_w[kPrefetch];
+  if (keep && a.wpos)
+#pragma unroll
+    for (int u = 0; u < kPrefetch; ++u) {
+      const int slot = w_lo + u * 32 + lane;
+      kept_w[u] = slot < w_hi ? __ldg(a.gate_w + slot) : 0.f;
+    }
   __syncthreads();
   for (int base0 = w_lo; base0 < w_hi; base0 += 32 * kPrefetch) {
     int key[kPrefetch];
     load_keys(a, base0, w_hi, lane, true, key);
+    if (keep)
+#pragma unroll
+      for (int u = 0; u < kPrefetch; ++u) kept[u] = key[u];
 #pragma unroll
     for (int u = 0; u < kPrefetch; ++u) {
       if (base0 + u * 32 >= w_hi) break;
@@ -248,26 +262,32 @@ __global__ void __launch_bounds__(kSingle ? kSingleThreads : kMultiThreads)
   int my_drops = 0;
   for (int base0 = w_lo; base0 < w_hi; base0 += 32 * kPrefetch) {
     int key[kPrefetch];
-    load_keys(a, base0, w_hi, lane, false, key);
+    if (keep) {
+#pragma unroll
+      for (int u = 0; u < kPrefetch; ++u) key[u] = kept[u];
+    } else {
+      load_keys(a, base0, w_hi, lane, false, key);
+    }
 #pragma unroll
     for (int u = 0; u < kPrefetch; ++u) {
       if (base0 + u * 32 >= w_hi) break;
       const int slot = base0 + u * 32 + lane;
       const int e = key[u];
+      const float gw = (keep && a.wpos) ? kept_w[u] : 0.f;
       const uint32_t peers = match_key(e, nbits);
       if (e >= 0) {
         const int p = my_cnt[e] + __popc(peers & lanemask_lt());
         if (cap == 0) {
           a.order[p] = slot;
           if (a.pos) a.pos[slot] = p;
-          if (a.wpos) a.wpos[p] = a.gate_w[slot];
+          if (a.wpos) a.wpos[p] = keep ? gw : a.gate_w[slot];
         } else {
           const int r = p - tot[e];  // rank inside expert e
           if (r < cap) {
             const long q = (long)e * cap + r;
             a.order[q] = slot;
             if (a.pos) a.pos[slot] = (int)q;
-            if (a.wpos) a.wpos[q] = a.gate_w[slot];
+            if (a.wpos) a.wpos[q] = keep ? gw : a.gate_w[slot];
           } else {
             if (a.pos) a.pos[slot] = -1;
             ++my_drops;
@@ -292,14 +312,13 @@ __global__ void __launch_bounds__(kSingle ? kSingleThreads : kMultiThreads)
   //      included -- the waste static gating pays for).
   if (b == 0 && a.items) {
     __syncthreads();
-    for (int e = threadIdx.x; e < E; e += blockDim.x) {
-      const int rows = cap == 0 ? a.counts[e] : cap;
-      before[e] = (rows + a.tile_n - 1) / a.tile_n;
-    }
+    // counts from the splits in shared memory (tot), not a global read-back
+    auto rows_of = [&](int e) { return cap == 0 ? (e + 1 < E ? tot[e + 1] : grand) - tot[e] : cap; };
+    for (int e = threadIdx.x; e < E; e += blockDim.x) before[e] = (rows_of(e) + a.tile_n - 1) / a.tile_n;
     __syncthreads();
     const int n_items = block_exclusive_scan(before, E, scratch);
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
-      const int rows = cap == 0 ? a.counts[e] : cap;
+      const int rows = rows_of(e);
       const int row0 = cap == 0 ? tot[e] : e * cap;
       int it = before[e];
       for (int c = 0; c < rows; c += a.tile_n, ++it) {
