@@ -125,9 +125,8 @@ inline int encode_rows(moe::RowMaps* m, const void* ptr, uint64_t rows, uint64_t
     return !v || atoi(v) != 0;
   }();
   m->has_k2 = k2 && cols % 128 == 0;
-  if (m->has_k2 && ((st = encode_rows_k2(&m->k2r64, ptr, rows, cols, 64)) ||
-                    (st = encode_rows_k2(&m->k2r128, ptr, rows, cols, 128))))
-    return st;
+  for (int i = 0; m->has_k2 && i < moe::RowMaps::kK2Maps; ++i)
+    if ((st = encode_rows_k2(&m->k2[i], ptr, rows, cols, 8 * (i + 1)))) return st;
   return MOE_OK;
 }
 

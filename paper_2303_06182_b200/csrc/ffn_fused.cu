@@ -264,8 +264,9 @@ __global__ void __launch_bounds__(256, 1)
       // packed weights: the stage's KCH tiles are consecutive 16 KB tiles,
       // already in the swizzled smem order -> one 1-D bulk copy
       const uint8_t* wbulk = static_cast<const uint8_t*>(tr.gemm ? g.W2p : g.W1p);
-      // a full 128-row item at KCH = 2: the stage's token rows as one 3-D box
-      const bool b_k2 = BN == 128 && KCH == 2 && nrows == 128 && tB->has_k2 && !(g.dbg & 1);
+      // KCH = 2 and <= 128 rows: the stage's token rows as one 3-D box (both
+      // chunks, chunk stride nrows x 128 B -- the MMA thread uses the same)
+      const bool b_k2 = KCH == 2 && nrows <= 128 && tB->has_k2 && !(g.dbg & 1);
       for (int kb = 0; kb < KB; ++kb) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         ptx::mbar_arrive_expect_tx(&full[stage], bytes);
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(256, 1)
           uint8_t* b_dst = sB + stage * Cfg::kBBytes + c * Cfg::kBChunk;
           if (g.dbg & 1) continue;
           if (b_k2) {
-            if (c == 0) ptx::tma_load_3d(b_dst, &tB->k2r128, &full[stage], 0, it.row0, kb * KCH, pol_x);
+            if (c == 0) ptx::tma_load_3d(b_dst, &tB->k2[nrows / 8 - 1], &full[stage], 0, it.row0, kb * KCH, pol_x);
             continue;
           }
           int r = 0;
@@ -318,6 +319,8 @@ __global__ void __launch_bounds__(256, 1)
       const int nn = (it.len + 15) & ~15;
       const uint32_t idesc = ptx::idesc_bf16(kBlockM, nn);
       const int KB = tr.gemm ? KB2 : KB1;
+      const bool b_k2 = KCH == 2 && nn <= 128 && (tr.gemm ? hm : xpm).has_k2 && !(g.dbg & 1);
+      const int bstride = b_k2 ? nn * kChunkK * 2 : Cfg::kBChunk;  // token chunk stride in the stage
       ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
       ptx::tc_fence_after();
       const uint32_t d = tmem_base + acc * Cfg::kAccStride;
@@ -342,7 +345,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int kk = 0; kk < kChunkK / kUmmaK; ++kk)
             ptx::mma_bf16(d, da + ((c * Cfg::kAChunk + kk * kUmmaK * 2) >> 4),
-                          db + ((c * Cfg::kBChunk + kk * kUmmaK * 2) >> 4), idesc,
+                          db + ((c * bstride + kk * kUmmaK * 2) >> 4), idesc,
                           (kb | c | kk) != 0 ? 1u : 0u);
         ptx::mma_commit(&empty[stage]);
         if (++stage == STAGES) {

@@ -319,7 +319,9 @@ __global__ void __launch_bounds__(256, 1)
       }
       // both CTAs' A halves + all token rows, counted on the leader's barrier
       const uint32_t bytes = 2 * kABytes + kKch * nrows * kChunkK * 2;
-      const bool b_k2 = kKch == 2 && (half == 128 || half == 64) && half * 2 == kBN && tB->has_k2;
+      // this CTA's token rows of the stage (both chunks) as one 3-D box; the
+      // chunk stride is then half x 128 B (the MMA issuer uses the same)
+      const bool b_k2 = kKch == 2 && half >= 8 && half <= 128 && tB->has_k2;
       for (int kb = 0; kb < KB; ++kb) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         const uint32_t fb = leader_addr(&full[stage]);
@@ -328,9 +330,8 @@ __global__ void __launch_bounds__(256, 1)
         // packed weights: the stage's two consecutive (pre-swizzled) tiles as
         // one 256-row box
         if (g.packed) tma_load_2d_pair(sA + stage * kABytes, tA, fb, 0, (a_tile + kb * kKch) * kBlockM, pol_w);
-        if (b_k2)  // this CTA's full half of the token rows, both k chunks, one 3-D box
-          tma_load_3d_pair(sB + stage * kBBytes, half == 128 ? &tB->k2r128 : &tB->k2r64, fb, 0, b_row,
-                           kb * kKch, pol_x);
+        if (b_k2)
+          tma_load_3d_pair(sB + stage * kBBytes, &tB->k2[half / 8 - 1], fb, 0, b_row, kb * kKch, pol_x);
 #pragma unroll
         for (int c = 0; c < kKch; ++c) {
           const int k0 = kb * kStageK + c * kChunkK;
@@ -356,6 +357,9 @@ __global__ void __launch_bounds__(256, 1)
       const int nn = (it.len + 15) & ~15;
       const uint32_t idesc = ptx::idesc_bf16(2 * kBlockM, nn);
       const int KB = tr.gemm ? KB2 : KB1;
+      const int half = nn >> 1;
+      const bool b_k2 = kKch == 2 && half >= 8 && half <= 128 && (tr.gemm ? hm : xpm).has_k2;
+      const int bstride = b_k2 ? half * kChunkK * 2 : kBChunk;
       ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
       ptx::tc_fence_after();
       const uint32_t d = tmem_base + acc * kBN;
@@ -369,7 +373,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int kk = 0; kk < kChunkK / kUmmaK; ++kk)
             mma_bf16_pair(d, da + ((c * kAChunk + kk * kUmmaK * 2) >> 4),
-                          db + ((c * kBChunk + kk * kUmmaK * 2) >> 4), idesc,
+                          db + ((c * bstride + kk * kUmmaK * 2) >> 4), idesc,
                           (kb | c | kk) != 0 ? 1u : 0u);
         commit_pair(&empty[stage]);
         if (++stage == kStages) {

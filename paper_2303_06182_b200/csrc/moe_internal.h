@@ -161,9 +161,10 @@ struct FusedFfnArgs {
 struct RowMaps {
   CUtensorMap m8, m16, m32, m64;
   // 3-D views [k chunk][row][64 cols] with boxes of two consecutive 64-wide k
-  // chunks x 64 / 128 rows: one request per KCH = 2 stage for a full block of
-  // token rows (lands chunk-major, the smem layout of the stage)
-  CUtensorMap k2r64, k2r128;
+  // chunks x 8 (i + 1) rows (k2[i], 8..128 rows): a KCH = 2 stage's token rows
+  // as ONE request, landing chunk-major with a chunk stride of rows x 128 B
+  static constexpr int kK2Maps = 16;
+  CUtensorMap k2[kK2Maps];
   int has_k2;
 };
 cudaError_t fused_ffn_prepare();
