@@ -39,7 +39,7 @@ constexpr int kAChunk = kBlockM * kChunkK * 2;      // 16 KB
 // stages half of the item's token rows.
 template <int BN, int STAGES, int KCH>
 struct PairCfg {
-  static_assert(KCH == 2, "packed weights: one 256-row (two-tile) box per stage");
+  static_assert(KCH % 2 == 0, "packed weights: 256-row (two-tile) boxes");
   static constexpr int kBN = BN;
   static constexpr int kBChunk = (BN / 2) * kChunkK * 2;  // half of the token rows
   static constexpr int kTmemCols = 2 * BN;
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t bytes = 2 * kABytes + kKch * nrows * kChunkK * 2;
       // this CTA's token rows of the stage (both chunks) as one 3-D box; the
       // chunk stride is then half x 128 B (the MMA issuer uses the same)
-      const bool b_k2 = kKch == 2 && half >= 8 && half <= 128 && tB->has_k2;
+      const bool b_k2 = kKch % 2 == 0 && half >= 8 && half <= 128 && tB->has_k2;
       for (int kb = 0; kb < KB; ++kb) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         const uint32_t fb = leader_addr(&full[stage]);
@@ -329,9 +329,15 @@ __global__ void __launch_bounds__(256, 1)
         if (leader) ptx::mbar_arrive_expect_tx(&full[stage], bytes);
         // packed weights: the stage's two consecutive (pre-swizzled) tiles as
         // one 256-row box
-        if (g.packed) tma_load_2d_pair(sA + stage * kABytes, tA, fb, 0, (a_tile + kb * kKch) * kBlockM, pol_w);
-        if (b_k2)
-          tma_load_3d_pair(sB + stage * kBBytes, &tB->k2[half / 8 - 1], fb, 0, b_row, kb * kKch, pol_x);
+#pragma unroll
+        for (int c2 = 0; c2 < kKch; c2 += 2) {
+          if (g.packed)
+            tma_load_2d_pair(sA + stage * kABytes + c2 * kAChunk, tA, fb, 0, (a_tile + kb * kKch + c2) * kBlockM,
+                             pol_w);
+          if (b_k2)
+            tma_load_3d_pair(sB + stage * kBBytes + c2 * half * kChunkK * 2, &tB->k2[half / 8 - 1], fb, 0, b_row,
+                             kb * kKch + c2, pol_x);
+        }
 #pragma unroll
         for (int c = 0; c < kKch; ++c) {
           const int k0 = kb * kStageK + c * kChunkK;
@@ -358,7 +364,7 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t idesc = ptx::idesc_bf16(2 * kBlockM, nn);
       const int KB = tr.gemm ? KB2 : KB1;
       const int half = nn >> 1;
-      const bool b_k2 = kKch == 2 && half >= 8 && half <= 128 && (tr.gemm ? hm : xpm).has_k2;
+      const bool b_k2 = kKch % 2 == 0 && half >= 8 && half <= 128 && (tr.gemm ? hm : xpm).has_k2;
       const int bstride = b_k2 ? half * kChunkK * 2 : kBChunk;
       ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
       ptx::tc_fence_after();
@@ -532,7 +538,9 @@ cudaError_t launch_pair(const CUtensorMap& tmW1, const RowMaps& xp, const CUtens
 // 128-token items 4 stages of 128-deep k (two 64-wide chunks): LM FFN
 // 1.303 -> 1.284 ms, MT 1.384 -> 1.340 ms against 8 x 64-deep; 256-token items
 // 3 x 128-deep: MT seq 256 FFN 1.82 -> 1.78-1.80 ms, LM static 7.76 ->
-// 7.59-7.68 ms against 6 x 64.
+// 7.59-7.68 ms against 6 x 64.  Round 2, with one weight box and one 3-D
+// token box per two chunks: 2 stages of 256-deep k (KCH = 4, same bytes in
+// flight) lost to 4 x 128 (LM FFN 1.2730 vs 1.2630 ms, MT 1.3151 vs 1.2933 ms).
 cudaError_t fused_ffn_pair_prepare() {
   cudaError_t e = cudaFuncSetAttribute(fused_ffn_pair_kernel<256, 3, 2>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<256, 3, 2>::kSmem);
