@@ -246,7 +246,8 @@ def run_reference(args):
 
     S, TD, HD, E, k, mode, C, desc = WORKLOADS[args.workload]
     L = CpuLayer(S, TD, HD, E, k)
-    for _ in range(max(0, min(args.warmup, 1))):
+    warm = max(0, min(args.warmup, 3))  # full layer passes (~2.6 s each at LM)
+    for _ in range(warm):
         L.run()
     # each step: full layer passes until >= 10 s of CPU work, median pass
     vals, secs = [], []
@@ -261,7 +262,7 @@ def run_reference(args):
     sample = r["sample"]
     line = {
         "metric": "MoE-layer tokens/s (dynamic gating)", "value": v, "unit": "tokens/s",
-        "impl": "reference", "n_gpus": world, "steps": len(vals), "warmup": min(args.warmup, 1),
+        "impl": "reference", "n_gpus": world, "steps": len(vals), "warmup": warm,
         "ms_per_step": secs[len(secs) // 2] * 1e3, "p50_ms": secs[len(secs) // 2] * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (counter-hash uniform tokens; random-init experts)",
