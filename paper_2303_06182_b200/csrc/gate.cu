@@ -71,6 +71,10 @@ constexpr int kMaxStages = MOE_GATE_MAX_STAGES;
 // MOE_GATE_PROF stamps per CTA: entry, after griddepcontrol.wait, first stage
 // full (MMA thread), last MMA committed, accumulator ready (epilogue), end
 constexpr int kProf = 6;
+#ifndef MOE_GATE_TWO_PASS
+#define MOE_GATE_TWO_PASS 1
+#endif
+constexpr bool kGateTwoPass = MOE_GATE_TWO_PASS;
 
 struct GateLayout {
   int e_pad;      // E rounded up to 16
@@ -242,6 +246,77 @@ __device__ __forceinline__ void gate_epilogue(const GateArgs& a, uint32_t tmem_b
     }
     if (a.dbg & 32) bv[0] = __uint_as_float(ra[0] ^ ra[31]);
     c0 = c_end;
+  }
+  if constexpr (K == 2) {
+    // Two-pass top-2 (the scan is issue-bound: ~14 instructions per column
+    // in the one-pass form).  Pass 1: the two largest VALUES with min/max
+    // only (5 per column pair, 3-input max); pass 2, over the columns again
+    // from TMEM in descending order: the lowest id holding the top value and
+    // the lowest other id holding the second (equal values -> lower id, as
+    // in the one-pass lists).  Full 32-column chunks, no split-K partials
+    // and no logits output only.
+    if (kGateTwoPass && nparts == 0 && !a.logits && (a.E & 31) == 0 && !(a.dbg & 48)) {
+      float m1 = -INFINITY, m2 = -INFINITY;
+      auto max3 = [](float x, float y, float z) {
+        float r;
+        asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(x), "f"(y), "f"(z));
+        return r;
+      };
+      auto values = [&](uint32_t (&r)[32]) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float v = __uint_as_float(r[i]), w = __uint_as_float(r[i + 1]);
+          const float hi = fmaxf(v, w), lo = fminf(v, w);
+          m2 = max3(m2, lo, fminf(hi, m1));
+          m1 = max3(m1, v, w);
+        }
+      };
+      if (c0 < c_end) ptx::tmem_ld32(trow + c0, ra);
+      while (c0 < c_end) {
+        ptx::tmem_ld_wait();
+        reg_fence32(ra);
+        if (c0 + 32 < c_end) ptx::tmem_ld32(trow + c0 + 32, rb);
+        values(ra);
+        c0 += 32;
+        if (c0 >= c_end) break;
+        ptx::tmem_ld_wait();
+        reg_fence32(rb);
+        if (c0 + 32 < c_end) ptx::tmem_ld32(trow + c0 + 32, ra);
+        values(rb);
+        c0 += 32;
+      }
+      const bool tie = m1 == m2;
+      int i1 = 0x7fffffff, i2 = 0x7fffffff;
+      auto ids = [&](uint32_t (&r)[32], int cb) {
+#pragma unroll
+        for (int i = 31; i >= 0; --i) {
+          const float v = __uint_as_float(r[i]);
+          const bool p1 = v == m1, p2 = v == m2;
+          i2 = p2 ? (tie ? i1 : cb + i) : i2;
+          i1 = p1 ? cb + i : i1;
+        }
+      };
+      c0 = c_end - 32;
+      if (c0 >= c_begin) ptx::tmem_ld32(trow + c0, ra);
+      while (c0 >= c_begin) {
+        ptx::tmem_ld_wait();
+        reg_fence32(ra);
+        if (c0 - 32 >= c_begin) ptx::tmem_ld32(trow + c0 - 32, rb);
+        ids(ra, c0);
+        c0 -= 32;
+        if (c0 < c_begin) break;
+        ptx::tmem_ld_wait();
+        reg_fence32(rb);
+        if (c0 - 32 >= c_begin) ptx::tmem_ld32(trow + c0 - 32, ra);
+        ids(rb, c0);
+        c0 -= 32;
+      }
+      bv[0] = m1;
+      bv[1] = m2;
+      bi[0] = i1;
+      bi[1] = i2;
+      c0 = c_end;  // the one-pass loop below is skipped; the odd list stays empty
+    }
   }
   if (c0 < c_end) ptx::tmem_ld32(trow + c0, ra);
   while (c0 < c_end) {

@@ -41,11 +41,6 @@ namespace {
 
 constexpr int kMultiThreads = 512;
 constexpr int kSingleThreads = 1024;
-// <= 2048 slots: one 256-thread CTA -- the per-expert walks over the warps'
-// histograms (scan, bases) are 8 deep instead of 32, and every warp's 256
-// slots stay in registers between the histogram and the scatter
-constexpr int kSmallThreads = 256;
-constexpr int kSmallMaxSlots = 2048;
 // One CTA handles up to this many slots; above it the work is spread over a
 // cooperative grid (measured: one SM needs ~76 us for 32K slots at E=512,
 // 64 CTAs ~12 us).
@@ -146,8 +141,8 @@ __device__ __forceinline__ unsigned long long route_clock() {
 #define ROUTE_STAMP(j) \
   if (a.prof && blockIdx.x == 0 && threadIdx.x == 0) a.prof[j] = route_clock()
 
-template <bool kSingle, int kThreads = kSingle ? kSingleThreads : kMultiThreads>
-__global__ void __launch_bounds__(kThreads)
+template <bool kSingle>
+__global__ void __launch_bounds__(kSingle ? kSingleThreads : kMultiThreads)
     route_kernel(RouteArgs a) {
   if (!a.late_trigger) pdl_trigger();
   pdl_wait();
@@ -156,7 +151,7 @@ __global__ void __launch_bounds__(kThreads)
   // memset node between the gather and the FFN, which would break the PDL chain)
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.zero_n; i += gridDim.x * blockDim.x)
     a.zero[i] = 0;
-  constexpr int kWarps = kThreads / 32;
+  constexpr int kWarps = (kSingle ? kSingleThreads : kMultiThreads) / 32;
   extern __shared__ int smem[];
   __shared__ int warp_off[kWarps];
   const int E = a.num_experts;
@@ -443,16 +438,6 @@ cudaError_t launch_route(RouteArgs a, int max_blocks, cudaStream_t stream) {
     const char* v = getenv("MOE_ROUTE_SINGLE_MAX");  // A/B: largest slot count for the 1-CTA form
     return v ? atoi(v) : kSingleMaxSlots;
   }();
-  static const bool small_cta = [] {
-    const char* v = getenv("MOE_ROUTE_SMALL_CTA");  // A/B: 0 keeps 1024 threads for <= 2048 slots
-    return !v || atoi(v) != 0;
-  }();
-  if (small_cta && total <= std::min(single_max, kSmallMaxSlots) &&
-      smem_bytes(a.num_experts, kSmallThreads / 32) <= 48 * 1024) {
-    a.chunk = kSmallMaxSlots;
-    return launch_chain(route_kernel<true, kSmallThreads>, dim3(1), dim3(kSmallThreads),
-                        smem_bytes(a.num_experts, kSmallThreads / 32), stream, false, a);
-  }
   if (total <= std::min(single_max, kSingleMaxSlots) && single_smem <= 200 * 1024) {
     a.chunk = (total + kSingleThreads - 1) / kSingleThreads * kSingleThreads;
     if (a.chunk == 0) a.chunk = kSingleThreads;
