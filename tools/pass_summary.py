@@ -18,10 +18,11 @@ def ncu(kind, path):
     return out.split("\n", 2)[2] if out.count("\n") >= 2 else out
 
 
-for f in ("launches_lm.csv", "launches_ep1.csv"):
-    shutil.copy(os.path.join(src, f), os.path.join(P, f"{prefix}_ncu_{f}"))
+for f in ("launches_lm.csv", "launches_ep1.csv", "launches_mt.csv", "launches_mt-l256.csv", "launches_cfg1.csv"):
+    if os.path.exists(os.path.join(src, f)):
+        shutil.copy(os.path.join(src, f), os.path.join(P, f"{prefix}_ncu_{f}"))
 rows = []
-for w in ("lm", "mt", "mt_cpu", "cfg1", "lm-static", "mt-static", "mt-cache_slots32"):
+for w in ("lm", "mt", "mt_cpu", "mt-l256", "cfg1", "lm-static", "mt-static", "mt-cache_slots32"):
     f = os.path.join(src, f"bench_{w}.json")
     if not os.path.exists(f):
         continue
@@ -67,7 +68,12 @@ if os.path.exists(ch):
 txt += ["## ncu launch list, LM step (single-GPU layer)", "", ncu("launches", os.path.join(src, "launches_lm.csv")),
         "## ncu launch list, LM step through the expert-parallel kernels at world 1", "",
         ncu("launches", os.path.join(src, "launches_ep1.csv")),
-        "## ncu --set full, LM step", "", ncu("full", os.path.join(src, "full_lm.ncu-rep")),
+        ]
+for w in ("mt", "mt-l256", "cfg1"):
+    f = os.path.join(src, f"launches_{w}.csv")
+    if os.path.exists(f):
+        txt += [f"## ncu launch list, {w} step", "", ncu("launches", f)]
+txt += ["## ncu --set full, LM step", "", ncu("full", os.path.join(src, "full_lm.ncu-rep")),
         "## ncu --set full, EP kernels at world 1", "", ncu("full", os.path.join(src, "full_ep1.ncu-rep"))]
 open(os.path.join(P, f"{prefix}_ncu_summary.md"), "w").write("\n".join(txt).replace(src + "/", ""))
 print("\n".join(txt[:20]))
