@@ -470,7 +470,7 @@ __device__ __forceinline__ void gate_tile(const CUtensorMap& tmX, const CUtensor
       // ---------------------------------------------------- TMA producer
       // (one issuing thread: rotating the stage's requests over the warp's
       // lanes measured equal, LM 13.3 vs 13.4 us mainloop, same box)
-      const uint64_t pol_x = ptx::policy_evict_first();
+      const uint64_t pol_x = a.x_keep ? ptx::policy_evict_last() : ptx::policy_evict_first();
       const uint64_t pol_w = ptx::policy_evict_last();
       // this CTA's share of the Wg boxes (all of them without multicast)
       constexpr int MC = SPLIT ? 1 : C;  // CTAs sharing each Wg box
@@ -1035,6 +1035,11 @@ cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const G
   // measured (ncu, same box): 64-deep path (MT) 2 per stage 16.4 vs 17.5 us
   // (1) / 17.7 (3); 32-deep E = 512 path (LM) 1 per stage 24.8 vs 28.5 (2)
   b.kps = kps_env > 0 ? kps_env : (wide ? 2 : 1);
+  // X tiles stay in L2 for the gather, which re-reads X right after the route
+  // (same box: LM gather 17.9 -> 16.5 us, MT 16.2 -> 15.3 us; Xp stored with
+  // evict-last for the FFN measured no change).  MOE_GATE_X_EVICT_FIRST=1 restores.
+  static const bool x_first = getenv("MOE_GATE_X_EVICT_FIRST") && atoi(getenv("MOE_GATE_X_EVICT_FIRST"));
+  b.x_keep = x_first ? 0 : 1;
   static unsigned long long* prof_buf = nullptr;
   const int ctas = split ? tiles * C : tiles;
   if (prof) {

@@ -191,6 +191,7 @@ struct GateArgs {
   unsigned long long* prof = nullptr;  // experiments (MOE_GATE_PROF): per-CTA phase times
   int dbg = 0;  // ablations (MOE_GATE_DBG, wrong results): 1 no MMAs, 2 no loads, 4 no Wg, 8 no X
   int kps = 1;  // k-blocks per pipeline stage (MOE_GATE_KPS, 64-deep k-block path)
+  int x_keep = 0;  // X tiles read with evict-last (the gather re-reads X next) instead of evict-first
 };
 cudaError_t gate_prepare(int E);
 cudaError_t launch_gate(const CUtensorMap& tmX, const CUtensorMap& tmWg, const GateArgs& a,
