@@ -129,7 +129,117 @@ __global__ void __launch_bounds__(128) probe2d(const __grid_constant__ CUtensorM
   if (lane == 0) sink[blockIdx.x] = acc;
 }
 
+// FFN-shaped stage: one 1-D bulk copy of `wbytes` (the packed weight tiles)
+// plus the token rows either as one 3-D box {64, 128 rows, 2 chunks} (mode 0)
+// or as one more 1-D bulk of the same 32 KB (mode 1).  Issued by one thread.
+__global__ void __launch_bounds__(128) probe_mix(const __grid_constant__ CUtensorMap tm3, const char* buf,
+                                                 size_t window, int rows, size_t per_cta, int stages, int mode,
+                                                 unsigned long long* sink) {
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int half = 32768, stage_bytes = 2 * half;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)stages * stage_bytes);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const size_t n = per_cta / stage_bytes;
+  size_t off = ((size_t)blockIdx.x * 7919 * half) % (window / 2);
+  int r0 = (blockIdx.x * 7919 * 128) % rows, c0 = 0;
+  uint32_t phase_bits = 0;
+  unsigned long long acc = 0;
+  for (size_t i = 0; i < n + stages; ++i) {
+    const int s = static_cast<int>(i % stages);
+    if (i >= (size_t)stages) {
+      const uint32_t par = (phase_bits >> s) & 1u;
+      uint32_t ok = 0;
+      while (!ok)
+        asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}"
+                     : "=r"(ok)
+                     : "r"(su32(&bar[s])), "r"(par)
+                     : "memory");
+      phase_bits ^= 1u << s;
+      acc += *reinterpret_cast<volatile int*>(smem + (size_t)s * stage_bytes);
+    }
+    if (i < n) {
+      char* dst = smem + (size_t)s * stage_bytes;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&bar[s])), "r"(stage_bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       su32(dst)),
+                   "l"(buf + window / 2 + off), "r"(half), "r"(su32(&bar[s]))
+                   : "memory");
+      off += half;
+      if (off + half > window / 2) off = 0;
+      if (mode == 0) {
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+                su32(dst + half)),
+            "l"(reinterpret_cast<uint64_t>(&tm3)), "r"(su32(&bar[s])), "r"(0), "r"(r0), "r"(c0)
+            : "memory");
+      } else {
+        const size_t toff = ((size_t)r0 * 8192 + (size_t)c0 * 128) % (window / 2 - half);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         su32(dst + half)),
+                     "l"(buf + toff), "r"(half), "r"(su32(&bar[s]))
+                     : "memory");
+      }
+      c0 += 2;
+      if (c0 >= 64) {
+        c0 = 0;
+        r0 += 128;
+        if (r0 + 128 > rows) r0 = 0;
+      }
+    }
+  }
+  sink[blockIdx.x] = acc;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && argv[1][0] == 'm') {  // mixed mode: m <window_mb> <stages> <mode 0 = 3-D box, 1 = bulk>
+    const size_t window = (size_t)(argc > 2 ? atoi(argv[2]) : 48) << 20;
+    const int stages = argc > 3 ? atoi(argv[3]) : 3, mode = argc > 4 ? atoi(argv[4]) : 0;
+    const int rows = (int)(window / 2 / 8192);
+    char* buf;
+    unsigned long long* sink;
+    cudaMalloc(&buf, window);
+    cudaMemset(buf, 1, window);
+    cudaMalloc(&sink, 4096 * 8);
+    CUtensorMap tm;
+    cuuint64_t dims[3] = {64, (cuuint64_t)rows, 64};
+    cuuint64_t strides[2] = {8192, 128};
+    cuuint32_t box[3] = {64, 128, 2};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = cuTensorMapEncodeTiled(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, buf, dims, strides, box, estr,
+                                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      printf("encode failed %d\n", (int)r);
+      return 1;
+    }
+    const size_t smem = 1024 + (size_t)stages * 65536 + stages * 8;
+    cudaFuncSetAttribute(probe_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    printf("FFN-shaped stages: %d x (32 KB bulk + 32 KB %s)\n", stages, mode ? "bulk" : "3-D box {64,128,2}");
+    for (int ctas : {1, 32, 148}) {
+      const size_t per_cta = (size_t)64 << 20;
+      probe_mix<<<ctas, 128, smem>>>(tm, buf, window, rows, per_cta / 8, stages, mode, sink);
+      cudaEventRecord(a);
+      probe_mix<<<ctas, 128, smem>>>(tm, buf, window, rows, per_cta, stages, mode, sink);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      const double gbs = (double)per_cta * ctas / (ms * 1e-3) / 1e9;
+      printf("ctas %3d: %8.1f GB/s aggregate, %6.1f GB/s per CTA  err=%s\n", ctas, gbs, gbs / ctas,
+             cudaGetErrorString(cudaGetLastError()));
+    }
+    return 0;
+  }
   if (argc > 1 && argv[1][0] == 't') {  // tensor mode: t <window_mb> <boxes/stage> <stages> <lanes>
     const size_t window = (size_t)(argc > 2 ? atoi(argv[2]) : 48) << 20;
     const int boxes = argc > 3 ? atoi(argv[3]) : 2, stages = argc > 4 ? atoi(argv[4]) : 4,
