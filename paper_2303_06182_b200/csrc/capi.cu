@@ -68,6 +68,7 @@ int moe_ctx_create(int device, moe_ctx** out) {
   auto* c = new moe_ctx();
   c->device = device;
   c->sms = prop.multiProcessorCount;
+  c->l2_bytes = static_cast<size_t>(prop.l2CacheSize);
   e = gemm_prepare();
   if (e == cudaSuccess) e = fused_ffn_prepare();
   if (e != cudaSuccess) {
@@ -739,6 +740,21 @@ int moe::capi::layer_front(moe_layer* L, const void* X, int S, const int32_t* id
 }
 }  // extern "C++"
 
+// Drop consumed H lines from L2 without write-back only when the layer's H
+// does not fit comfortably in L2 (LM: 268 MB, MT: 101-201 MB): there the
+// write-back would cost HBM bandwidth the weight stream needs.  A small H
+// (configs[0]: 16.8 MB) stays dirty in L2 and the discard loop of the item's
+// last consumer sat on the FFN's critical path (same box, cfg1 FFN
+// 65.8 -> 61.0 us, step 81.1 -> 76.4 us).  MOE_FFN_DISCARD=0/1 forces it.
+static int ffn_discard_h(const moe_ctx* ctx, size_t h_bytes) {
+  static const int env = [] {
+    const char* v = getenv("MOE_FFN_DISCARD");
+    return v ? atoi(v) : -1;
+  }();
+  if (env >= 0) return env;
+  return h_bytes > ctx->l2_bytes / 2 ? 1 : 0;
+}
+
 // Grouped FFN over the items of experts [e_lo, e_hi) (all items if e_lo < 0).
 extern "C++" {
 int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaEvent_t* ev) {
@@ -795,12 +811,8 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
     }();
     const int per_item = HD / 128 + TD / 128;
     const int lag = lag_env > 0 ? lag_env : std::max(2, (8 * L->ctx->sms + per_item - 1) / per_item);
-    static const int discard = [] {
-      const char* v = getenv("MOE_FFN_DISCARD");
-      return v ? atoi(v) : 1;
-    }();
     fa.lag = lag;
-    fa.discard_h = discard;
+    fa.discard_h = ffn_discard_h(L->ctx, (size_t)L->rows_max * HD * 2);
     fa.dbg = getenv("MOE_FFN_DBG") ? atoi(getenv("MOE_FFN_DBG")) : 0;
     // the expert-cache slot pool is row-major: packed tiles only for the layer's own weights
     fa.packed = L->packed && !L->slot_of;
@@ -1186,7 +1198,7 @@ int moe_ffn_forward(moe_ffn* F, const void* X_rows, const int32_t* keys, const f
     fa.tile_ctr = F->done.p + 2 * F->items_max;
     const int per_item = HD / 128 + TD / 128;
     fa.lag = std::max(2, (8 * F->ctx->sms + per_item - 1) / per_item);
-    fa.discard_h = 1;
+    fa.discard_h = ffn_discard_h(F->ctx, (size_t)F->d.max_rows * HD * 2);
     fa.packed = F->packed;
     fa.W1p = F->w1p.p;
     fa.W2p = F->w2p.p;

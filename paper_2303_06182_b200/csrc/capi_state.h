@@ -196,6 +196,7 @@ using namespace moe::capi;
 struct moe_ctx {
   int device = 0;
   int sms = 0;
+  size_t l2_bytes = 0;
   int route_max_blocks = 0;
   int route_prepared_E = -1;
   DevBuf<int32_t> block_hist, err_flag, drop_mark;
