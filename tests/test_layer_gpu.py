@@ -526,3 +526,41 @@ def test_pack_in_place_holds_expert_weights_once(S, TD, HD, E, k):
     layer.check_errors()
     assert torch.equal(out, ref) and torch.equal(out2, ref)
     assert layer.view()["ffn_kernel"] in (1, 2)
+
+
+_OUT_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2303_06182_b200.layer import LayerShape, MoeLayer, make_tokens, make_weights
+S, TD, HD, E, k = map(int, sys.argv[2:7])
+shape = LayerShape(TD, HD, E, k)
+layer = MoeLayer(shape, S, weights=make_weights(shape, seed=2303061820))
+x = make_tokens(S, TD, seed=2303061820)
+for _ in range(3):  # repeated forwards: dirty / discarded H lines of the previous step
+    out = layer(x)
+torch.cuda.synchronize()
+layer.check_errors()
+np.save(sys.argv[7], out.float().cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("S,TD,HD,E,k", [(2048, 1024, 4096, 8, 1), (4096, 512, 1024, 64, 2)])
+def test_h_discard_does_not_change_outputs(S, TD, HD, E, k, tmp_path):
+    """The fused FFN drops consumed H lines from L2 only when H exceeds half of
+    L2 (capi.cu ffn_discard_h); forcing the discard on and off (separate
+    processes: MOE_FFN_DISCARD is read once) must give bitwise-equal layer
+    outputs over repeated forwards."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for d in ("1", "0"):
+        f = str(tmp_path / f"out_{d}.npy")
+        env = dict(os.environ, MOE_FFN_DISCARD=d)
+        r = subprocess.run([sys.executable, "-c", _OUT_SCRIPT, root, str(S), str(TD), str(HD), str(E), str(k), f],
+                           env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[d] = np.load(f)
+    assert np.array_equal(outs["1"], outs["0"])
+    assert np.isfinite(outs["0"]).all() and np.abs(outs["0"]).max() > 0
