@@ -343,12 +343,14 @@ int moe_cache_destroy(moe_cache* C) {
 }
 
 int moe_cache_forward(moe_cache* C, const void* X, int S, void* out, void* stream) {
+  MOE_NVTX("moe.cache_forward");
   if (!C || !X || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   return cache_forward(C, X, S, nullptr, nullptr, out, (cudaStream_t)stream);
 }
 
 int moe_cache_forward_routed(moe_cache* C, const void* X, const int32_t* idx, const float* w, int S,
                              void* out, void* stream) {
+  MOE_NVTX("moe.cache_forward_routed");
   if (!C || !X || !idx || !w || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   return cache_forward(C, X, S, idx, w, out, (cudaStream_t)stream);
 }

@@ -211,6 +211,7 @@ int moe::capi::route_common(moe_ctx* ctx, const int32_t* expert_idx, int S, int 
 int moe_route_dynamic(moe_ctx* ctx, const int32_t* expert_idx, int S, int k, int E,
                       int32_t* counts, int32_t* splits, int32_t* order, int32_t* pos,
                       void* stream) {
+  MOE_NVTX("moe.route_dynamic");
   if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
   int st = check_batch(S, k, E);
   if (st) return st;
@@ -385,6 +386,7 @@ int moe_exchange_counts_host(moe_ctx* ctx, const int32_t* experts, int S, int k,
 
 int moe_gate_topk(moe_ctx* ctx, const void* X, const void* Wg, int S, int TD, int E, int k,
                   int32_t* idx, float* w, float* logits, void* stream) {
+  MOE_NVTX("moe.gate_topk");
   if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
   int st = check_batch(S, k, E);
   if (st) return st;
@@ -887,11 +889,13 @@ static int layer_forward_impl(moe_layer* L, const void* X, int S, void* out, cud
 
 int moe_layer_forward_routed(moe_layer* L, const void* X, const int32_t* idx, const float* w, int S,
                              void* out, void* stream) {
+  MOE_NVTX("moe.layer_forward_routed");
   if (!L || !X || !out || !idx || !w) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   return layer_forward_impl(L, X, S, out, (cudaStream_t)stream, true, idx, w);
 }
 
 int moe_layer_forward(moe_layer* L, const void* X, int S, void* out, void* stream) {
+  MOE_NVTX("moe.layer_forward");
   if (!L || !X || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   return layer_forward_impl(L, X, S, out, (cudaStream_t)stream, true);
 }
@@ -921,6 +925,7 @@ int moe_layer_stage_times(moe_layer* L, int slot, float* ms) {
 }
 
 int moe_layer_forward_graph(moe_layer* L, const void* X, int S, void* out, void* stream) {
+  MOE_NVTX("moe.layer_forward_graph");
   if (!L || !X || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
   moe_layer::GraphEntry* hit = nullptr;
@@ -959,6 +964,7 @@ int moe_layer_forward_graph(moe_layer* L, const void* X, int S, void* out, void*
 }
 
 int moe_layer_forward_host(moe_layer* L, const void* X_host, int S, void* out_host, void* stream) {
+  MOE_NVTX("moe.layer_forward_host");
   if (!L || !X_host || !out_host) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   const size_t bytes = (size_t)L->d.max_tokens * L->d.token_dim * 2;
   int st;
@@ -975,6 +981,7 @@ int moe_layer_forward_host(moe_layer* L, const void* X_host, int S, void* out_ho
 
 int moe_layer_forward_host_batches(moe_layer* L, const void* const* X_host, const int* S,
                                    void* const* out_host, int n, void* stream) {
+  MOE_NVTX("moe.layer_forward_host_batches");
   if (!L || n < 0 || (n > 0 && (!X_host || !S || !out_host)))
     return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   if (!stream) return fail(MOE_ERR_INVALID_ARGUMENT, "pipelined forward needs a non-default stream");
@@ -1056,6 +1063,7 @@ int moe_route_dynamic_keyed(moe_ctx* ctx, const int32_t* expert_idx, int S, int 
                             int num_experts, const int32_t* key_map, int num_keys,
                             int32_t* counts, int32_t* splits, int32_t* order, int32_t* pos,
                             const float* gate_w, float* wpos, void* stream) {
+  MOE_NVTX("moe.route_dynamic_keyed");
   if (!ctx) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
   int st = check_batch(S, k, num_experts);
   if (st) return st;

@@ -823,6 +823,7 @@ static int ep_forward_impl(moe_ep* P, const void* X, int S, void* out, cudaStrea
 }  // extern "C++"
 
 int moe_ep_forward(moe_ep* P, const void* X, int S, void* out, void* stream) {
+  MOE_NVTX("moe.ep_forward");
   if (!P || !X || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   cudaSetDevice(P->ctx->device);
   return ep_forward_impl(P, X, S, out, (cudaStream_t)stream, true);
@@ -848,6 +849,7 @@ int moe_ep_stage_times(moe_ep* P, float* ms) {
 }
 
 int moe_ep_forward_graph(moe_ep* P, const void* X, int S, void* out, void* stream) {
+  MOE_NVTX("moe.ep_forward_graph");
   if (!P || !X || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
   cudaSetDevice(P->ctx->device);

@@ -6,10 +6,23 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <cstdlib>
 #include <utility>
 
 namespace moe {
+
+// NVTX range over a C ABI entry point (host enqueue time; nsys / Nsight
+// correlate it with the kernels it launches).  nvtx3 is header-only: with no
+// tool attached a push / pop is one call through a null-checked pointer.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define MOE_NVTX(name) ::moe::NvtxRange moe_nvtx_scope_(name)
 
 // ---- programmatic dependent launch (PDL)
 // Kernels of the layer chain are launched with programmatic stream

@@ -80,3 +80,17 @@ def test_no_silent_cpu_fallback_without_gpu():
     G._ctx = None
     with pytest.raises(_capi.MoeError):
         G.dynamic_dispatch(G.Batch([G.TokenAssignment([0], [1.0])]), G.GatingConfig(2, 1))
+
+
+def test_entry_points_carry_nvtx_ranges():
+    """Every forward / gate / route entry point of the C ABI opens an NVTX
+    range (csrc/moe_internal.h MOE_NVTX) so a profiler attributes kernels to
+    the call that launched them; the range names are string constants of the
+    library."""
+    path = os.path.join(ROOT, "paper_2303_06182_b200", "libmoe_b200.so")
+    data = open(path, "rb").read()
+    for name in ["moe.layer_forward", "moe.layer_forward_graph", "moe.layer_forward_host",
+                 "moe.layer_forward_host_batches", "moe.layer_forward_routed", "moe.gate_topk",
+                 "moe.route_dynamic", "moe.ep_forward", "moe.ep_forward_graph", "moe.cache_forward"]:
+        assert name.encode() + b"\0" in data, name
+    assert b"nvtxRangePushA" in data or b"NVTX" in data
