@@ -742,6 +742,7 @@ int moe::capi::layer_front(moe_layer* L, const void* X, int S, const int32_t* id
 }
 }  // extern "C++"
 
+extern "C++" {
 // Drop consumed H lines from L2 without write-back only when the layer's H
 // does not fit comfortably in L2 (LM: 268 MB, MT: 101-201 MB): there the
 // write-back would cost HBM bandwidth the weight stream needs.  A small H
@@ -758,7 +759,6 @@ static int ffn_discard_h(const moe_ctx* ctx, size_t h_bytes) {
 }
 
 // Grouped FFN over the items of experts [e_lo, e_hi) (all items if e_lo < 0).
-extern "C++" {
 int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaEvent_t* ev) {
   const int TD = L->d.token_dim, HD = L->d.hidden_dim;
   auto mark = [&](int i) {
