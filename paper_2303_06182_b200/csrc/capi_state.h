@@ -118,7 +118,8 @@ inline int encode_rows(moe::RowMaps* m, const void* ptr, uint64_t rows, uint64_t
   if ((st = encode_bf16(&m->m8, ptr, rows, cols, 8)) ||
       (st = encode_bf16(&m->m16, ptr, rows, cols, 16)) ||
       (st = encode_bf16(&m->m32, ptr, rows, cols, 32)) ||
-      (st = encode_bf16(&m->m64, ptr, rows, cols, 64)))
+      (st = encode_bf16(&m->m64, ptr, rows, cols, 64)) ||
+      (st = encode_bf16(&m->m256, ptr, rows, cols, 256)))
     return st;
   static const bool k2 = [] {
     const char* v = getenv("MOE_FFN_ROWS_K2");

@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(256, 1)
       ptx::prefetch_tmap(&m->m16);
       ptx::prefetch_tmap(&m->m32);
       ptx::prefetch_tmap(&m->m64);
+      ptx::prefetch_tmap(&m->m256);
     }
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
@@ -260,7 +261,11 @@ __global__ void __launch_bounds__(256, 1)
         }
         fence_proxy_async_global();
       }
-      const uint32_t bytes = ((g.dbg & 16) ? 0 : kABytes) + ((g.dbg & 1) ? 0 : KCH * nrows * kChunkK * 2);
+      // KCH = 1, > 128 rows: the chunk's token rows as one 256-row box (the
+      // rows past the item are never multiplied into stored columns)
+      const bool b_256 = KCH == 1 && BN == 256 && nrows > 128 && g.rows256 && !(g.dbg & 1);
+      const int tok_rows = b_256 ? 256 : nrows;
+      const uint32_t bytes = ((g.dbg & 16) ? 0 : kABytes) + ((g.dbg & 1) ? 0 : KCH * tok_rows * kChunkK * 2);
       // packed weights: the stage's KCH tiles are consecutive 16 KB tiles,
       // already in the swizzled smem order -> one 1-D bulk copy
       const uint8_t* wbulk = static_cast<const uint8_t*>(tr.gemm ? g.W2p : g.W1p);
@@ -285,6 +290,10 @@ __global__ void __launch_bounds__(256, 1)
           if (g.dbg & 1) continue;
           if (b_k2) {
             if (c == 0) ptx::tma_load_3d(b_dst, &tB->k2[nrows / 8 - 1], &full[stage], 0, it.row0, kb * KCH, pol_x);
+            continue;
+          }
+          if (b_256) {
+            ptx::tma_load_2d(b_dst, &tB->m256, &full[stage], k0, it.row0, pol_x);
             continue;
           }
           int r = 0;
@@ -519,6 +528,10 @@ cudaError_t launch_fused_ffn(const CUtensorMap& tmW1, const RowMaps& xp, const C
     const char* v = getenv("MOE_FFN_LATE_TRIGGER");
     return v ? atoi(v) : 1;
   }();
+  static const int rows256 = [] {
+    const char* v = getenv("MOE_FFN_ROWS256");
+    return v ? atoi(v) : 1;
+  }();
   static const int dyn_tail = [] {
     const char* v = getenv("MOE_FFN_DYN_TAIL");  // tiles claimed dynamically; 0 = lag * MT2, <0 = off
     return v ? atoi(v) : 0;
@@ -526,6 +539,7 @@ cudaError_t launch_fused_ffn(const CUtensorMap& tmW1, const RowMaps& xp, const C
   FusedFfnArgs args = args_in;
   args.full_fence = full_fence;
   args.dyn_tail = dyn_tail;
+  args.rows256 = rows256;
   // packed weights are always loaded as 1-D bulk copies by the 1-SM kernel
   // (the packed tensor maps' 256-row boxes are shaped for the CTA pair)
   if (args.packed && (!args.W1p || !args.W2p)) return cudaErrorInvalidValue;

@@ -156,6 +156,7 @@ struct FusedFfnArgs {
   int late_trigger;         // let the next kernel launch only as CTAs finish
   int pair_hint;            // the caller expects >= ~8 waves of CTA-pair tiles (see auto_pair)
   int dyn_tail;             // tail tiles claimed dynamically (0 = the last lag * MT2)
+  int rows256;              // 1-SM kernel, 256-token items: one 256-row token box per k chunk (MOE_FFN_ROWS256)
   // packed tiles' base addresses: the 1-SM kernel loads a stage's consecutive
   // weight tiles as ONE 1-D bulk copy (null: tensor-map loads)
   const void* W1p = nullptr;
@@ -173,6 +174,9 @@ struct FusedFfnArgs {
 // 16 and 8 -- a few TMA issues per k-block instead of n/16.
 struct RowMaps {
   CUtensorMap m8, m16, m32, m64;
+  // one 2-D box of 256 rows x 64 cols: a 256-token item's rows of one k chunk
+  // as ONE request (the 1-SM kernel at 256-token items, KCH = 1)
+  CUtensorMap m256;
   // 3-D views [k chunk][row][64 cols] with boxes of two consecutive 64-wide k
   // chunks x 8 (i + 1) rows (k2[i], 8..128 rows): a KCH = 2 stage's token rows
   // as ONE request, landing chunk-major with a chunk stride of rows x 128 B
