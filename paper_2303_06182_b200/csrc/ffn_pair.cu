@@ -250,7 +250,12 @@ __global__ void __launch_bounds__(256, 1)
   const int total = n * (P1 + P2);
   const int cid = blockIdx.x >> 1;
   const int ncl = gridDim.x >> 1;
-  const int t_dyn = g.tile_ctr ? max(0, total - (g.dyn_tail > 0 ? g.dyn_tail / 2 : L * P2)) : total;
+  // dynamically claimed tail: at least the GEMM2-only segment of the last L
+  // items, and at least ~7 waves of pair-tiles (same box, FFN stage: LM
+  // 1259.6 -> 1256.5 us, MT 1289.8 -> 1287.9 us, MT seq 256 1682 -> 1644 us
+  // against the segment alone (120 pair-tiles); ~1500 and all-dynamic were
+  // slower; profiles/r02_s17_ffn_tail_sweep.txt, r02_s18_ffn_tail_default_ab.txt)
+  const int t_dyn = g.tile_ctr ? max(0, total - (g.dyn_tail > 0 ? g.dyn_tail / 2 : max(L * P2, 7 * ncl))) : total;
   int rs = 0;
   uint32_t rph = 0;
   // leader producer: claim the next tail tile, publish it in both CTAs' rings
