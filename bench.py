@@ -156,6 +156,12 @@ def ffn_bytes(rows, active, TD, HD, one_launch):
     return active * 2 * HD * TD * 2 + rows * TD * 2 + rows * TD * 2 + h
 
 
+# Read-only HBM ceiling measured on B200 for the FFN's weight-stream pattern
+# (1-D bulk TMA into 148 SMs, profiles/r01_s2_hbm_read_ceiling.txt): the copy
+# peak in MEASURED_PEAKS counts reads + writes, so a read stream can exceed it.
+READ_CEILING_GBS = 7430.0
+
+
 def layer_roofline(S, TD, HD, E, k, active, hbm_gbs, tflops):
     """F = 2 S TD E + 4 k S TD HD; B = S TD 2 + E TD 2 +
     A 2 TD HD 2 + S TD 2 (bf16).  T_roof = max(F / P_tc, B / BW)."""
@@ -840,7 +846,12 @@ def run_b200(args):
                      "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
                      "peak_kind": peak_kind + (" (sustained)" if tensor_bound and ffn_ms > 1.0 else ""),
                      "algorithmic_bytes_per_step": ffn_b, "algorithmic_flops_per_step": ffn_f,
-                     "traffic": traffic},
+                     "traffic": traffic,
+                     # the peak is MEASURED_PEAKS' copy bandwidth (read + write); a read-only
+                     # weight stream can exceed it: its measured ceiling on B200 is
+                     # READ_CEILING_GBS (profiles/r01_s2_hbm_read_ceiling.txt)
+                     **({"read_ceiling_gbs": READ_CEILING_GBS,
+                         "frac_of_read_ceiling": achieved / READ_CEILING_GBS} if not tensor_bound else {})},
         "layer_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms_per_step, "flops": F,
                            "bytes": B, "peaks": {"hbm_gbs": hbm_gbs, "bf16_tflops": tflops}},
         "stage_ms": {n: float(m) for n, m in zip(STAGES, mean_stage)},
