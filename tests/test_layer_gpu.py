@@ -564,3 +564,27 @@ def test_h_discard_does_not_change_outputs(S, TD, HD, E, k, tmp_path):
         outs[d] = np.load(f)
     assert np.array_equal(outs["1"], outs["0"])
     assert np.isfinite(outs["0"]).all() and np.abs(outs["0"]).max() > 0
+
+
+@pytest.mark.parametrize("S,TD,HD,E,k", [(8192, 1024, 4096, 128, 2), (2048, 1024, 4096, 8, 1)])
+def test_ffn_schedule_does_not_change_outputs(S, TD, HD, E, k, tmp_path):
+    """Which CTA (pair) runs a tile is a scheduling choice: the round-robin body,
+    the dynamically claimed tail (default: >= 7 waves of pair-tiles in the
+    CTA-pair kernel) and an all-dynamic schedule must give bitwise-equal layer
+    outputs (MOE_FFN_DYN_TAIL is read once: separate processes).  The first
+    shape runs the CTA-pair kernel, the second (configs[0]) the 1-SM kernel."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for t in ("0", "2", "100000"):
+        f = str(tmp_path / f"out_{t}.npy")
+        env = dict(os.environ, MOE_FFN_DYN_TAIL=t)
+        r = subprocess.run([sys.executable, "-c", _OUT_SCRIPT, root, str(S), str(TD), str(HD), str(E), str(k), f],
+                           env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[t] = np.load(f)
+    assert np.array_equal(outs["0"], outs["2"])
+    assert np.array_equal(outs["0"], outs["100000"])
+    assert np.isfinite(outs["0"]).all() and np.abs(outs["0"]).max() > 0
