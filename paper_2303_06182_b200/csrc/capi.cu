@@ -812,7 +812,14 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
       return v ? atoi(v) : 0;
     }();
     const int per_item = HD / 128 + TD / 128;
-    const int lag = lag_env > 0 ? lag_env : std::max(2, (8 * L->ctx->sms + per_item - 1) / per_item);
+    // dynamic gating at 256-token items (MT at seq 256: ~1 item per expert,
+    // MMA-heavy tiles) runs best with most GEMM1 tiles ahead of GEMM2: 4x the
+    // lag (same box, FFN 1686-1689 -> 1652-1662 us, profiles/r02_s24_l256_lag_ab.txt;
+    // the static capacity-padded items and 128-token items lose 3-6 % with it,
+    // profiles/r02_s22_lag_256_items.txt)
+    const int lag_mult = (L->d.mode == MOE_GATING_DYNAMIC && L->tile_n == 256) ? 4 : 1;
+    const int lag = lag_env > 0 ? lag_env
+                                : lag_mult * std::max(2, (8 * L->ctx->sms + per_item - 1) / per_item);
     fa.lag = lag;
     fa.discard_h = ffn_discard_h(L->ctx, (size_t)L->rows_max * HD * 2);
     fa.dbg = getenv("MOE_FFN_DBG") ? atoi(getenv("MOE_FFN_DBG")) : 0;
