@@ -813,11 +813,13 @@ int moe::capi::layer_ffn(moe_layer* L, cudaStream_t s, int e_lo, int e_hi, cudaE
     }();
     const int per_item = HD / 128 + TD / 128;
     // dynamic gating at 256-token items (MT at seq 256: ~1 item per expert,
-    // MMA-heavy tiles) runs best with most GEMM1 tiles ahead of GEMM2: 4x the
-    // lag (same box, FFN 1686-1689 -> 1652-1662 us, profiles/r02_s24_l256_lag_ab.txt;
+    // MMA-heavy tiles) runs best with (nearly) every GEMM1 tile ahead of GEMM2:
+    // 8x the lag (same box, FFN 1686-1689 -> 1652-1662 us at 4x,
+    // profiles/r02_s24_l256_lag_ab.txt; 1637-1647 vs 1653-1664 us at 8x vs 4x,
+    // r02_s26_l256_lag_tail.txt;
     // the static capacity-padded items and 128-token items lose 3-6 % with it,
     // profiles/r02_s22_lag_256_items.txt)
-    const int lag_mult = (L->d.mode == MOE_GATING_DYNAMIC && L->tile_n == 256) ? 4 : 1;
+    const int lag_mult = (L->d.mode == MOE_GATING_DYNAMIC && L->tile_n == 256) ? 8 : 1;
     const int lag = lag_env > 0 ? lag_env
                                 : lag_mult * std::max(2, (8 * L->ctx->sms + per_item - 1) / per_item);
     fa.lag = lag;
